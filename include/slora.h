@@ -1,0 +1,230 @@
+/*
+ * slora.h -- C ABI of the B200-native S-LoRA hot path (arXiv 2311.03285):
+ * heterogeneous batched LoRA over Unified Paging.
+ *
+ * P:L = PAPER.md line L (the paper's text; citations are documentation).
+ * S:L = SPEC.md line L (interface / error names only).
+ *
+ * Conventions (every function):
+ *   - returns slora_status; SLORA_OK == 0.  On error nothing was enqueued and
+ *     the pool's bookkeeping is unchanged; slora_last_error() returns a
+ *     thread-local one-line detail ("needed=64 free=5").
+ *   - asynchronous CUDA faults surface as SLORA_ERR_CUDA on a later call or on
+ *     slora_sync().
+ *   - `stream` arguments are cudaStream_t passed as void* (0 = legacy default
+ *     stream).  No call synchronizes the device on the hot path.
+ *   - a pool (and every batch made from it) is externally serialized: one
+ *     thread at a time.
+ *   - ownership: the pool owns its metadata, its pinned staging and its
+ *     device page tables; the pool's page buffer, x, y and v are caller-owned
+ *     device memory that must outlive the calls using them.
+ *   - no C++ type, exception or torch type crosses this boundary.
+ *
+ * Data layout in HBM
+ *   pool buffer: capacity_pages pages of page_elems = hidden / tp_size
+ *     elements of `dtype` each; page p starts at byte p * page_elems * esize.
+ *     KV pages and adapter pages are interleaved.
+ *   adapter tensors (reading R1): A (h x r) is stored TRANSPOSED -- one page
+ *     row per rank column j (its h input elements); B (r x d) one page row per
+ *     rank row.  "a LoRA weight tensor of rank R takes up R pages".
+ *   under N-way tensor parallelism (reading R3/R4) the pool on
+ *   rank k holds only k's shards, each still r pages of H/N elements:
+ *     q,k,v: A1 column shard (rank columns k*r/N..), each column of length h
+ *            spans N pages; B1 column shard (output columns k*d/N..).
+ *     o    : A2 row shard (input rows k*d/N..), B2 column shard (k*h/N..).
+ */
+#ifndef SLORA_H
+#define SLORA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct slora_pool* slora_pool_t;   /* opaque, owned by the library */
+typedef struct slora_batch* slora_batch_t; /* opaque, owned by the library */
+
+typedef enum { SLORA_F32 = 0, SLORA_F16 = 1, SLORA_BF16 = 2 } slora_dtype;
+
+/* Which free page is handed out (reading R10): LIFO free stack that pops
+ * 0,1,2,... initially, or a splitmix64-seeded Fisher-Yates shuffle of it
+ * (for i = cap-1..1: j = splitmix64() % (i+1); swap).  Frees push in release
+ * order. */
+typedef enum { SLORA_ORDER_ASCENDING = 0, SLORA_ORDER_SHUFFLE = 1 } slora_alloc_order;
+
+typedef enum {
+    SLORA_OK = 0,
+    SLORA_ERR_INVALID_ARG = 1,
+    SLORA_ERR_SHAPE = 2,              /* shape error                         */
+    SLORA_ERR_OUT_OF_PAGES = 3,       /* InsufficientPages(needed, free)    */
+    SLORA_ERR_ALREADY_RESIDENT = 4,
+    SLORA_ERR_NOT_RESIDENT = 5,
+    SLORA_ERR_PINNED = 6,             /* PinnedEviction                     */
+    SLORA_ERR_NOT_PINNED = 7,
+    SLORA_ERR_STALE_HANDLE = 8,       /* double free / use of a freed handle / a
+                                         batch prepared before an eviction */
+    SLORA_ERR_FREE_PAGE_READ = 9,
+    SLORA_ERR_NONRESIDENT_ADAPTER = 10, /* batch names an adapter not loaded */
+    SLORA_ERR_SEGMENT_OVERLAP = 11,   /* reserved; segments are derived here */
+    SLORA_ERR_TOKEN_COUNT_NOT_ONE = 12, /* decode-only call on a multi-token segment */
+    SLORA_ERR_INDIVISIBLE = 13,       /* IndivisibleDimension               */
+    SLORA_ERR_CUDA = 14,
+    SLORA_ERR_NO_DEVICE = 15          /* device call on a bookkeeping-only pool     */
+} slora_status;
+
+const char* slora_status_string(slora_status s);
+const char* slora_last_error(void);
+
+/* ------------------------------------------------------------------ a1 ---
+ * Pool create ("allocate a large buffer statically ... each page
+ * corresponding to a vector of H").  The buffer is caller-owned (torch).
+ * device = -1 makes a bookkeeping-only pool (no CUDA calls; device_buffer must
+ * be NULL and adapter loads take host_w = NULL): used by CPU tests. */
+typedef struct {
+    int32_t device;             /* CUDA ordinal, or -1 = bookkeeping only      */
+    slora_dtype dtype;
+    int64_t hidden;             /* H; d = h = H for q/k/v/o (reading R2)       */
+    int32_t num_layers;         /* L                                          */
+    int32_t tp_size;            /* N >= 1; N | hidden                         */
+    int32_t tp_rank;            /* 0 <= k < N                                 */
+    int64_t capacity_pages;     /* >= 1                                       */
+    void* device_buffer;        /* >= capacity_pages*page_elems*esize bytes, 16B aligned */
+    int64_t device_buffer_bytes;
+    int32_t max_adapters;       /* adapter slots (resident adapters), >= 1    */
+    slora_alloc_order alloc_order;
+    uint64_t seed;              /* for SLORA_ORDER_SHUFFLE                    */
+} slora_pool_config;
+
+slora_status slora_pool_create(const slora_pool_config* cfg, slora_pool_t* out);
+slora_status slora_pool_destroy(slora_pool_t pool); /* synchronizes the device */
+
+typedef struct {
+    int64_t capacity_pages, used_pages, free_pages;
+    int64_t largest_free_run;   /* longest run of consecutive free page ids    */
+    int64_t kv_pages, adapter_pages;
+    int64_t page_elems;         /* hidden / tp_size                           */
+    int32_t resident_adapters;
+} slora_frag_report;
+
+/* S:161-163 fragmentation_report. */
+slora_status slora_fragmentation_report(slora_pool_t pool, slora_frag_report* out);
+
+/* ------------------------------------------------------------------ a2 ---
+ * Adapter load, host -> pool pages ("fetch ... the LoRA adapters needed
+ * for the currently running batch").  Pages needed: L * 4 * 2 * rank
+ * (every tensor shard takes `rank` pages, see the layout note above).
+ *   host_w: the FULL (unsharded) adapter, dtype of the pool, canonical layout:
+ *     for layer l in 0..L-1, for proj p in (q,k,v,o): A (h x r, row-major)
+ *     then B (r x d, row-major); h = d = hidden.  The library packs its TP
+ *     shard into its own pinned staging, copies it H2D and scatters it into
+ *     pages on `stream`; host_w may be reused as soon as the call returns.
+ *     Must be NULL for a bookkeeping-only pool, non-NULL otherwise.
+ *   scale: multiplies this adapter's delta (reading R6; 1.0 = the paper).
+ *   Errors: INVALID_ARG (rank < 1, bad pointer), INDIVISIBLE (N does not
+ *     divide rank), ALREADY_RESIDENT, OUT_OF_PAGES (pages or slots).
+ *   Pages are claimed in pop order layer, proj, tensor (A then B), row, chunk.
+ *   The load waits (stream-ordered) for the last page release. */
+slora_status slora_adapter_load(slora_pool_t pool, int64_t adapter_id, int32_t rank,
+                                const void* host_w, float scale, void* stream,
+                                int32_t* slot_out);
+/* Release an adapter's pages (errors NOT_RESIDENT, PINNED).  The release is
+ * stream-ordered: a later load waits for `stream`'s queued work.  Batches
+ * prepared before the eviction become STALE_HANDLE. */
+slora_status slora_adapter_evict(slora_pool_t pool, int64_t adapter_id, void* stream,
+                                 int64_t* released_out);
+slora_status slora_adapter_pin(slora_pool_t pool, int64_t adapter_id);   /* NOT_RESIDENT */
+slora_status slora_adapter_unpin(slora_pool_t pool, int64_t adapter_id); /* NOT_RESIDENT, NOT_PINNED */
+/* The adapter's page ids in claim order (n_out = count; copies min(cap, n)). */
+slora_status slora_adapter_pages(slora_pool_t pool, int64_t adapter_id, int32_t* out,
+                                 int64_t cap, int64_t* n_out);
+
+/* ------------------------------------------------------------------ a3 ---
+ * KV cache bookkeeping: K and V of a request are two
+ * (S, H) tensors per layer (reading R11) -> 2 * S * L pages, claimed in order
+ * layer, kind (K=0, V=1), position.  pages_out (nullable) receives them.
+ * Errors: INVALID_ARG (n < 0, request already live), OUT_OF_PAGES;
+ * append/free/pages of a request that is not live: STALE_HANDLE. */
+slora_status slora_kv_alloc(slora_pool_t pool, int64_t request_id, int32_t n_tokens,
+                            int32_t* pages_out);
+slora_status slora_kv_append(slora_pool_t pool, int64_t request_id, int32_t n_tokens,
+                             int32_t* pages_out);
+slora_status slora_kv_free(slora_pool_t pool, int64_t request_id, void* stream,
+                           int64_t* released_out);
+slora_status slora_kv_pages(slora_pool_t pool, int64_t request_id, int32_t layer, int32_t kind,
+                            int32_t* out, int64_t cap, int64_t* n_out);
+
+/* Copy page rows to dst (n x page_elems, device) -- the SPEC gather op
+ * (S:157-160), for tests.  FREE_PAGE_READ if a page is free. */
+slora_status slora_gather_pages(slora_pool_t pool, const int32_t* pages_host, int32_t n,
+                                void* dst_device, void* stream);
+
+/* ------------------------------------------------------------------ a4 ---
+ * Batch descriptor.  token_adapter_host[i] = adapter id of token i or -1
+ * (no adapter: its y rows are never written, reading R7).  prepare groups
+ * tokens by adapter into segments (each adapter's weights are read once per
+ * call, reading R8), attaches ranks and page tables, packs (segment x
+ * projection) work into balanced units (no padding to a max rank), chooses
+ * MBGMV or MBGMM per segment by token count (reading R9) and uploads the
+ * descriptor on `stream`.  Errors: NONRESIDENT_ADAPTER.  The descriptor is
+ * valid until the next prepare of the same batch or an eviction. */
+slora_status slora_batch_create(slora_pool_t pool, slora_batch_t* out);
+slora_status slora_batch_destroy(slora_batch_t batch);
+slora_status slora_batch_prepare(slora_batch_t batch, const int64_t* token_adapter_host, int32_t T,
+                                 void* stream);
+
+typedef struct {
+    int32_t T;                 /* tokens in the batch                         */
+    int32_t adapted_tokens;    /* tokens with an adapter                      */
+    int32_t segments;          /* distinct adapters in the batch              */
+    int64_t sum_rank_tokens;   /* NR = sum over adapted tokens of its rank    */
+    int64_t weight_bytes_per_proj; /* sum over segments of this rank's shard bytes of A and B */
+    int32_t mbgmm_segments;    /* segments routed to the tensor-core kernel   */
+} slora_batch_info;
+slora_status slora_batch_get_info(slora_batch_t batch, slora_batch_info* out);
+
+/* ---------------------------------------------------------------- a5+a7 --
+ * Fused shrink -> expand on one GPU (Eq. lora_factored P:121 per token; the
+ * rank-r intermediate stays on chip):
+ *   for every projection p in proj_mask (bit p: 0=q 1=k 2=v 3=o) and every
+ *   adapted token i with adapter a:
+ *     y_p[i, :] = round( y_p[i, :] + scale_a * (x[i, :] A_{a,layer,p}) B_{a,layer,p} )
+ *   x: T x hidden, row stride ldx elements; y[p]: T x hidden, stride ldy[p];
+ *   pool dtype; 16-byte aligned rows.  fp32 accumulation; one rounding.
+ *   Only for tp_size == 1 (else INVALID_ARG). */
+slora_status slora_lora_apply(slora_pool_t pool, slora_batch_t batch, int32_t layer,
+                              uint32_t proj_mask, const void* x, int64_t ldx,
+                              void* const y[4], const int64_t ldy[4], void* stream);
+
+/* Split form (for tensor parallelism).
+ * shrink: v = x A_shard in fp32.  For projection p, the stored A shard has
+ *   r/div rank columns, div = tp_size for q,k,v and 1 for o (and 1 when
+ *   tp_size == 1); x has the shard's input width (hidden for q,k,v;
+ *   hidden/tp_size for o under TP).  v layout (fp32, dense):
+ *     [proj in mask order][segment][token][r/div]
+ *   with slora_lora_v_elems(batch, mask, div) elements in total.
+ * expand: y_p[i, :] += scale_a * v_i B_shard, y width hidden/tp_size.
+ *   v is read as v_blocks equal blocks laid out back to back, block b holding
+ *   rank columns [b*r/v_blocks, (b+1)*r/v_blocks) in the shrink layout above
+ *   (v_blocks = tp_size after the q/k/v all-gather, 1 after the o
+ *   all-reduce or on one GPU). */
+slora_status slora_lora_v_elems(slora_batch_t batch, uint32_t proj_mask, int32_t div,
+                                int64_t* out);
+slora_status slora_lora_shrink(slora_pool_t pool, slora_batch_t batch, int32_t layer,
+                               uint32_t proj_mask, const void* x, int64_t ldx, float* v,
+                               void* stream);
+slora_status slora_lora_expand(slora_pool_t pool, slora_batch_t batch, int32_t layer,
+                               uint32_t proj_mask, const float* v, int32_t v_blocks,
+                               void* const y[4], const int64_t ldy[4], void* stream);
+
+/* Wait for `stream` and surface any deferred CUDA error. */
+slora_status slora_sync(slora_pool_t pool, void* stream);
+
+/* Number of this library's kernel launches so far (for bench accounting). */
+int64_t slora_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SLORA_H */
