@@ -1,0 +1,430 @@
+#!/usr/bin/env python
+"""Benchmark of the S-LoRA hot path on B200 (BASELINE.json metric:
+"LoRA-layer tokens/s and achieved HBM GB/s vs peak at 1/2/4/8 B200").
+
+One STEP = one pass of the whole hot path over one synthetic batch:
+  a4 batch descriptor (slora_batch_prepare: group by adapter, pack units,
+     upload), then for each of the model's 32 layers
+  a5+a7 q/k/v fused shrink->expand (one launch) and o fused shrink->expand
+     (one launch) -- on N > 1 GPUs the split shrink -> NCCL all-gather /
+     all-reduce -> expand of S-LoRA TP (a6, a8 fold into the base partial).
+value = adapted tokens x layers / step time (LoRA-layer tokens/s, i.e.
+T / per-layer LoRA time), whole job.  Default workload: BASELINE configs[2]
+decode (Llama-7B h=4096, 2000 adapters, ranks {64,32,16,8} round-robin,
+Zipf alpha=1, decode batch 64, fp16) -- the north_star's ">= 70% of HBM"
+target.  Weights of 32 layers (~3 GB) rotate through the timed region, far
+larger than the 126 MB L2 (no flush needed; stated in config).
+
+--impl reference: the fp64 CPU oracle (oracle/), timed on host cores on a
+bounded sample of the same workload (the tier's reference arm).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from synth import workload as wl  # noqa: E402
+
+METRIC = "LoRA-layer tokens/s and achieved HBM GB/s vs peak at 1/2/4/8 B200"
+UNIT = "tokens/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default=None, help="c1 | c2 | c2-mixed | c3 | c4 (default: c2, or tp preset)")
+    ap.add_argument("--layers", type=int, default=None)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile-steps", type=int, default=0, help="untimed steps only (for ncu)")
+    return ap.parse_args()
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def measured_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.1)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 6:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[2:6]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ setup
+class Workload:
+    def __init__(self, cfg, layers, tp, rank, device, stream):
+        import torch
+        from paper_2311_03285_b200 import Batch, Pool
+        self.cfg, self.L, self.N, self.k = cfg, layers, tp, rank
+        self.batch = wl.make_batch(cfg)
+        b = self.batch
+        self.T, self.H = b.T, cfg.hidden
+        self.P = self.H // tp
+        es = wl.elem_bytes(cfg.dtype)
+        need = sum(layers * 8 * r for r in b.ranks.values())
+        kv_tokens = 16  # KV pages of every request interleaved with adapter pages
+        kv_pages = 2 * kv_tokens * layers * len(b.requests)
+        self.pool = Pool(self.H, layers, need + kv_pages + 64, dtype=cfg.dtype, device=device, tp_size=tp,
+                         tp_rank=rank, order="shuffle", seed=1234 + rank,
+                         max_adapters=max(256, len(b.ranks) + 8))
+        rid = 0
+        reqs = list(b.requests)
+        for i, a in enumerate(b.unique):
+            if rid < len(reqs):
+                self.pool.kv_alloc(rid, kv_tokens)
+                rid += 1
+            host = wl.adapter_host_buffer(cfg, a, layers)
+            self.pool.adapter_load(a, b.ranks[a], host, stream=stream)
+        while rid < len(reqs):
+            self.pool.kv_alloc(rid, kv_tokens)
+            rid += 1
+        torch.cuda.synchronize()
+        self.dbatch = Batch(self.pool)
+        self.dbatch.prepare(b.token_adapter, stream=stream)
+        td = {"f32": torch.float32, "f16": torch.float16, "bf16": torch.bfloat16}[cfg.dtype]
+        self.td = td
+        dev = f"cuda:{device}"
+        g = torch.Generator(device=dev).manual_seed(5 + rank)
+        # activations resident in HBM: x per layer, y per (layer, proj)
+        self.x = torch.randn((layers, self.T, self.H), generator=g, device=dev).to(td)
+        if tp == 1:
+            self.y = torch.randn((layers, 4, self.T, self.H), generator=g, device=dev).to(td)
+        else:
+            self.y = torch.randn((layers, 3, self.T, self.P), generator=g, device=dev).to(td)
+            self.z = torch.randn((layers, self.T, self.P), generator=g, device=dev).to(td)
+            self.base = torch.randn((layers, self.T, self.H), generator=g, device=dev).to(td)
+        self.es = es
+        # algorithmic bytes per step: unique-adapter weight shards
+        # + x once per call + y read+write; tables excluded (KB-sized)
+        Tad = int((b.token_adapter >= 0).sum())
+        wbytes = sum(r * 2 * self.P * es for r in b.ranks.values())  # per projection, this rank's shard
+        if tp == 1:
+            self.bytes_qkv = 3 * wbytes + Tad * self.H * es + 3 * 2 * Tad * self.H * es
+            self.bytes_o = wbytes + Tad * self.H * es + 2 * Tad * self.H * es
+        else:
+            self.bytes_qkv = 3 * wbytes + Tad * self.H * es + 3 * 2 * Tad * self.P * es
+            self.bytes_o = wbytes + Tad * self.P * es + 2 * Tad * self.P * es
+        self.Tad = Tad
+        self.flops_layer = sum(4 * 2 * r * 2 * self.H // tp for r in
+                               [b.ranks[a] for a in b.token_adapter if a >= 0])
+
+    def step(self, stream, events=None, tpl=None):
+        """One step: prepare + all layers.  events: list to append
+        (start, end, kind) CUDA event pairs around each launch."""
+        import torch
+        b = self.dbatch
+        b.prepare(self.batch.token_adapter, stream=stream)
+        H, P = self.H, self.P
+        for l in range(self.L):
+            if self.N == 1:
+                ys = [self.y[l, p] for p in range(4)]
+                e0 = torch.cuda.Event(enable_timing=True) if events is not None else None
+                if e0: e0.record(stream)
+                b.apply(l, "qkv", self.x[l], H, ys, [H] * 4, stream=stream)
+                if e0:
+                    e1 = torch.cuda.Event(enable_timing=True); e1.record(stream)
+                    e2 = torch.cuda.Event(enable_timing=True); e2.record(stream)
+                b.apply(l, "o", self.x[l], H, ys, [H] * 4, stream=stream)
+                if e0:
+                    e3 = torch.cuda.Event(enable_timing=True); e3.record(stream)
+                    events.append((e0, e1, "qkv"))
+                    events.append((e2, e3, "o"))
+            else:
+                tpl.qkv(l, self.x[l], H, [self.y[l, p] for p in range(3)], [P, P, P], stream=stream)
+                tpl.o(l, self.z[l], P, self.base[l], H, stream=stream)
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    from paper_2311_03285_b200 import launch_count
+    from paper_2311_03285_b200.tp import LibraryOps, TPLoraLayer
+
+    ws, rank, local = dist_env()
+    if ws > 1 and not dist.is_initialized():
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    torch.cuda.set_device(local)
+    name = args.workload or "c2"
+    cfg = wl.CONFIGS[name]
+    layers = args.layers or cfg.num_layers
+    if name == "c0":
+        layers = 1
+    stream = torch.cuda.current_stream()
+    W = Workload(cfg, layers, ws, rank, local, stream)
+    tpl = None
+    if ws > 1:
+        tpl = TPLoraLayer(LibraryOps(W.dbatch), device=f"cuda:{local}")
+        tpl.buffers_for()
+    if args.profile_steps:
+        for _ in range(args.profile_steps):
+            W.step(stream, tpl=tpl)
+        torch.cuda.synchronize()
+        return
+    warm = max(3, args.warmup)
+    for _ in range(warm):
+        W.step(stream, tpl=tpl)
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.2)
+    # ---- timed region: K steps, per-launch events on the launching stream
+    events = [] if ws == 1 else None
+    n0 = launch_count()
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for _ in range(args.steps):
+        W.step(stream, events=events, tpl=tpl)
+    t1.record(stream)
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    launches = launch_count() - n0
+    ck = clocks.stop()
+    ms = t0.elapsed_time(t1) / args.steps
+    if ws > 1:
+        tt = torch.tensor([ms], device=f"cuda:{local}")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    tokens_step = W.Tad * layers
+    value = tokens_step / (ms / 1e3)
+    peaks, peak_kind = measured_peaks()
+    roofline = None
+    if events is not None:
+        dur = {"qkv": [], "o": []}
+        for a, b, kind in events:
+            dur[kind].append(a.elapsed_time(b))
+        kern_ms = (sum(dur["qkv"]) + sum(dur["o"])) / args.steps
+        bytes_step = (W.bytes_qkv + W.bytes_o) * layers
+        achieved = bytes_step / (kern_ms / 1e3) / 1e9
+        traffic = None
+        try:
+            prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json")))
+            if prof.get("workload") == cfg.name:
+                traffic = prof.get("dram_bytes_per_launch")
+        except Exception:
+            pass
+        roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                    "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": traffic,
+                    "peak_source": f"{peak_kind} copy bandwidth (MEASURED_PEAKS.json hbm_gbs)",
+                    "kernel": "lora_unit_kernel<__half, kFused> (MBGMV cluster gather-shrink-expand)",
+                    "alg_bytes_per_launch": {"qkv": W.bytes_qkv, "o": W.bytes_o},
+                    "avg_launch_us": {"qkv": round(1e3 * float(np.mean(dur["qkv"])), 2),
+                                      "o": round(1e3 * float(np.mean(dur["o"])), 2)},
+                    "kernel_share_of_step": round(kern_ms / ms, 4),
+                    "frac_of_8TBs_spec": round(achieved / 8000.0, 4)}
+    out = {"metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+           "warmup": warm, "ms_per_step": round(ms, 4), "higher_is_better": True,
+           "scaling": "strong", "vs_baseline": None, "dtype": cfg.dtype,
+           "data": "synthetic (seeded; random-init adapters; Zipf adapter popularity)",
+           "config": {"workload": cfg.name, "hidden": cfg.hidden, "ranks": list(cfg.rank_list),
+                      "n_adapters": cfg.n_adapters, "alpha": cfg.alpha, "tokens": W.T,
+                      "adapted_tokens": W.Tad, "unique_adapters": len(W.batch.ranks), "layers": layers,
+                      "projections": "q,k,v,o", "parallelism": f"tp{ws}",
+                      "l2": "inputs larger than L2 (adapter pages of all layers ~%.2f GB rotate)" %
+                            (layers * (W.bytes_qkv + W.bytes_o) / 1e9),
+                      "step": "batch_prepare + layers x (qkv apply, o apply)"},
+           "gpu_launches": int(launches), "clocks": ck}
+    if roofline:
+        out["roofline"] = roofline
+    if ws == 1 and not args.no_e2e:
+        out["e2e"] = run_e2e(W, stream, max(3, args.steps // 2))
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(cfg, W.batch, budget_s=10.0)
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if ws > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def run_e2e(W, stream, steps):
+    """Same metric through the public API with HOST buffers: every step copies
+    x (all layers) and y (all layers, projections) H2D from pinned memory,
+    prepares the batch from the host token map, runs the layers and reads
+    every y back D2H."""
+    import torch
+    xh = W.x.cpu().pin_memory()
+    yh = W.y.cpu().pin_memory()
+    yo = torch.empty_like(yh).pin_memory()
+    bi = xh.numel() * xh.element_size() + yh.numel() * yh.element_size() + W.T * 8
+    bo = yo.numel() * yo.element_size()
+
+    def one():
+        W.x.copy_(xh, non_blocking=True)
+        W.y.copy_(yh, non_blocking=True)
+        W.step(stream)
+        yo.copy_(W.y, non_blocking=True)
+
+    for _ in range(2):
+        one()
+    torch.cuda.synchronize()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for _ in range(steps):
+        one()
+    t1.record(stream)
+    torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1) / steps
+    return {"value": round(W.Tad * W.L / (ms / 1e3), 1), "unit": UNIT, "h2d_bytes_per_step": int(bi),
+            "d2h_bytes_per_step": int(bo), "ms_per_step": round(ms, 4)}
+
+
+# --------------------------------------------------------------- oracle arm
+def oracle_sample(cfg, batch):
+    """One layer (q,k,v,o deltas) of the workload's batch, oracle inputs."""
+    import oracle
+    ids = batch.unique
+    slot = np.array([ids.index(a) if a >= 0 else -1 for a in batch.token_adapter], np.int64)
+    T, H = batch.T, cfg.hidden
+    x = oracle.to_f64(wl.activations(cfg, T, H, 100), cfg.dtype)
+    proj = []
+    for p in range(4):
+        As, Bs = [], []
+        for a in ids:
+            A, B = wl.adapter_weights(cfg, a, 0, p, batch.ranks[a])
+            As.append(oracle.to_f64(A, cfg.dtype))
+            Bs.append(oracle.to_f64(B, cfg.dtype))
+        y = oracle.to_f64(wl.activations(cfg, T, H, 200 + p), cfg.dtype)
+        proj.append((As, Bs, y))
+    return x, slot, proj
+
+
+def oracle_layer(x, slot, proj, nthreads):
+    import oracle
+    for As, Bs, y in proj:
+        oracle.lora_apply(x, y, As, Bs, slot, nthreads=nthreads)
+
+
+def cpu_baseline(cfg, batch, budget_s=10.0):
+    cores = os.cpu_count() or 1
+    x, slot, proj = oracle_sample(cfg, batch)
+    Tad = int((slot >= 0).sum())
+    oracle_layer(x, slot, proj, cores)
+    n = 0
+    t0 = time.perf_counter()
+    while time.perf_counter() - t0 < budget_s:
+        oracle_layer(x, slot, proj, cores)
+        n += 1
+    dt = (time.perf_counter() - t0) / n
+    return {"value": round(Tad / dt, 2), "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"{n} repetitions of one layer's q,k,v,o deltas of the {cfg.name} batch "
+                      f"({Tad} tokens, {len(batch.ranks)} adapters), fp64 C oracle, {cores} threads"}
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    name = args.workload or "c2"
+    cfg = wl.CONFIGS[name]
+    batch = wl.make_batch(cfg)
+    cores = os.cpu_count() or 1
+    x, slot, proj = oracle_sample(cfg, batch)
+    Tad = int((slot >= 0).sum())
+    for _ in range(max(3, args.warmup)):
+        oracle_layer(x, slot, proj, cores)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        oracle_layer(x, slot, proj, cores)
+    ms = (time.perf_counter() - t0) * 1e3 / args.steps
+    value = Tad / (ms / 1e3)
+    sample = (f"each step = one layer's q,k,v,o deltas of the {cfg.name} batch ({Tad} tokens, "
+              f"{len(batch.ranks)} adapters), fp64 C oracle on {cores} host threads")
+    out = {"impl": "reference", "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": ws,
+           "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": round(ms, 3),
+           "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+           "dtype": "f64", "data": "synthetic (seeded)",
+           "config": {"workload": cfg.name, "hidden": cfg.hidden, "ranks": list(cfg.rank_list),
+                      "tokens": batch.T, "layers": 1, "parallelism": "host threads"},
+           "cpu_baseline": {"value": round(value, 2), "unit": UNIT, "cores": cores, "kind": "oracle",
+                            "sample": sample},
+           "e2e": {"value": round(value, 2), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,104 @@
+"""S-LoRA tensor parallelism over torch.distributed (Sec. 6.1,
+P:316-331; Fig. lora_tp), one process per GPU.
+
+Per attention layer on rank k of N (readings R3/R4/R13 in DESIGN.md):
+  q, k, v  ("can be seen as W1"): A1 column shard (r/N rank columns),
+           B1 column shard (d/N output columns).
+             v_k = x A1_k                 slora_lora_shrink  (fp32, B x r/N)
+             v   = all_gather(v_k)        one concatenated collective for
+                                          q, k and v (reading R14)
+             y_k += v B1_k                slora_lora_expand (v_blocks = N)
+  o        ("can be seen as W2"): A2 row shard, B2 column shard.
+             u_k = z_k A2_k               slora_lora_shrink  (fp32 partial, B x r)
+             u   = all_reduce(u_k)
+             P_k[:, k-th h/N slice] += u B2_k   slora_lora_expand into the base
+                                          partial sum (add_2 fold): the base
+                                          layer's own all-reduce then carries
+                                          the LoRA result.
+The compute steps are the library's CUDA kernels; this module only orders
+them around the two collectives and owns the exchange buffers.  Element
+counts exchanged per device equal: 3(N-1)/N * NR for the all-gather
+and 2(N-1)/N * NR for the all-reduce (NR = sum over tokens of the rank).
+"""
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+
+class LibraryOps:
+    """The compute steps, bound to a prepared slora Batch (CUDA kernels)."""
+
+    def __init__(self, batch):
+        self.batch = batch
+
+    def v_elems(self, projs, div):
+        return self.batch.v_elems(projs, div)
+
+    def shrink(self, layer, projs, x, ldx, v, stream):
+        self.batch.shrink(layer, projs, x, ldx, v, stream)
+
+    def expand(self, layer, projs, v, v_blocks, ys, ldys, stream):
+        self.batch.expand(layer, projs, v, v_blocks, ys, ldys, stream)
+
+
+class TPLoraLayer:
+    """Orchestrates shrink -> collective -> expand on one rank.
+
+    `ops` provides v_elems/shrink/expand (LibraryOps on a GPU; tests inject a
+    CPU emulation to exercise the exchange logic with gloo)."""
+
+    def __init__(self, ops, group=None, device=None):
+        self.ops = ops
+        self.group = group
+        self.N = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.device = device
+        self._buf = {}
+        self.sent_elems = {"allgather": 0, "allreduce": 0}
+
+    def _get(self, key, n):
+        t = self._buf.get(key)
+        if t is None or t.numel() < n:
+            t = torch.empty(max(n, 1), dtype=torch.float32, device=self.device)
+            self._buf[key] = t
+        return t[:n]
+
+    def buffers_for(self):
+        """Pre-size exchange buffers (call after batch prepare)."""
+        n_loc = self.ops.v_elems("qkv", self.N)
+        self._get("v_loc", n_loc)
+        self._get("v_all", n_loc * self.N)
+        self._get("u", self.ops.v_elems("o", 1))
+
+    def qkv(self, layer, x, ldx, y_shards, ld_y, stream=None):
+        """y_shards: q, k, v column shards (T x H/N each)."""
+        n_loc = self.ops.v_elems("qkv", self.N)
+        if n_loc == 0:
+            return
+        v_loc = self._get("v_loc", n_loc)
+        self.ops.shrink(layer, "qkv", x, ldx, v_loc, stream)
+        if self.N > 1:
+            v_all = self._get("v_all", n_loc * self.N)
+            dist.all_gather_into_tensor(v_all, v_loc, group=self.group)
+            self.sent_elems["allgather"] += (self.N - 1) * n_loc
+        else:
+            v_all = v_loc
+        self.ops.expand(layer, "qkv", v_all, self.N, list(y_shards) + [None], list(ld_y) + [0], stream)
+
+    def o(self, layer, z_shard, ldz, base_partial, ld_base, stream=None):
+        """z_shard: this rank's T x H/N slice of the attention output;
+        base_partial: this rank's T x H base partial sum (z_k W2_k).  The LoRA
+        output lands in its column slice k; the caller's base all-reduce then
+        completes both (fold)."""
+        n = self.ops.v_elems("o", 1)
+        if n == 0:
+            return
+        u = self._get("u", n)
+        self.ops.shrink(layer, "o", z_shard, ldz, u, stream)
+        if self.N > 1:
+            dist.all_reduce(u, group=self.group)
+            self.sent_elems["allreduce"] += 2 * (self.N - 1) * n // self.N
+        P = base_partial.shape[1] // self.N
+        y_slice = base_partial[:, self.rank * P:(self.rank + 1) * P]
+        self.ops.expand(layer, "o", u, 1, [None, None, None, y_slice], [0, 0, 0, ld_base], stream)
