@@ -107,6 +107,46 @@ uint64_t splitmix64(uint64_t& st) {
 }
 
 int esize_of(slora_dtype d) { return d == SLORA_F32 ? 4 : 2; }
+
+// Kernel configuration for one (mode, K, D).  C = the smallest split (cluster
+// size) whose per-CTA slices are whole 16-byte vectors and at most 4 KB (one
+// warp's worth of 16-byte vectors per slice row x 8 warps), so the producer
+// streams the largest slices and the most SMs stay usable (small clusters
+// pack GPCs best).  SLORA_SPLIT overrides.  ns = ring slots filling smem.
+KernelCfg make_kernel_cfg(int mode, int64_t K, int64_t D, int64_t P, int es, int dtype) {
+    (void)P;
+    KernelCfg k;
+    k.mode = mode;
+    k.K = K;
+    k.D = D;
+    static int forced = [] {
+        const char* s = getenv("SLORA_SPLIT");
+        return s ? atoi(s) : 0;
+    }();
+    auto valid = [&](int C) {
+        if (mode != kExpand && (K % C || ((K / C) * es) % 16 || (K / C) * es > 8192)) return false;
+        if (mode != kShrink && (D % C || ((D / C) * es) % 16 || (D / C) * es > 4096)) return false;
+        if (mode == kFused && (K / C) * es > 4096) return false;
+        return true;
+    };
+    int C = 0;
+    if (forced > 0 && forced <= 16 && valid(forced)) C = forced;
+    for (int c = 1; c <= 16 && !C; ++c)
+        if (valid(c)) C = c;
+    if (!C) return k;
+    k.C = C;
+    const size_t budget = size_t(227) * 1024;
+    const size_t base = lora_smem_bytes(mode, C, K, D, 0, es);
+    const size_t per_slot = lora_smem_bytes(mode, C, K, D, 1, es) - base;
+    int ns = int((budget - base) / per_slot);
+    ns = std::min(ns, kMaxSlots);
+    if (ns < 2) return k;
+    k.ns = ns;
+    k.smem = lora_smem_bytes(mode, C, K, D, ns, es);
+    k.n_clusters = lora_max_clusters(mode, dtype, C, k.smem);
+    k.ok = k.n_clusters > 0;
+    return k;
+}
 }  // namespace
 
 struct slora_pool {
@@ -129,6 +169,9 @@ struct slora_pool {
     bool stage_used[2] = {false, false};
     cudaEvent_t release_ev = nullptr;
     bool release_pending = false;
+    // kernel configurations: 0 fused (K=D=H), 1 shrink q/k/v (K=H),
+    // 2 shrink o (K=H/N), 3 expand (D=H/N)
+    KernelCfg kcfg[4];
 
     int64_t free_pages() const { return int64_t(free_stack.size()); }
     int N() const { return cfg.tp_size; }
@@ -156,9 +199,11 @@ struct slora_batch {
     std::vector<int32_t> tok_idx;
     std::vector<DevUnit> units[5];
     std::vector<DevItem> items[5];
-    int32_t max_rows[5] = {}, max_toks[5] = {}, max_v[5] = {};
+    // LPT schedules: [kernel cfg][nproj] -> per-cluster unit lists
+    std::vector<int32_t> sched_off[4][5], sched[4][5];
     // device descriptor blob
     size_t off_segs = 0, off_tok = 0, off_units[5] = {}, off_items[5] = {};
+    size_t off_sched_off[4][5] = {}, off_sched[4][5] = {};
     size_t blob_cap = 0;
     void* blob_host = nullptr;
     void* blob_dev = nullptr;
@@ -233,6 +278,17 @@ extern "C" slora_status slora_pool_create(const slora_pool_config* cfg, slora_po
         }
         if ((e = cudaEventCreateWithFlags(&p->release_ev, cudaEventDisableTiming)))
             return cleanup(e, "cudaEventCreate");
+        const int dt = cfg->dtype == SLORA_F32 ? kF32 : (cfg->dtype == SLORA_F16 ? kF16 : kBF16);
+        const int64_t H = cfg->hidden;
+        p->kcfg[0] = make_kernel_cfg(kFused, H, H, P, es, dt);
+        p->kcfg[1] = make_kernel_cfg(kShrink, H, P, P, es, dt);
+        p->kcfg[2] = make_kernel_cfg(kShrink, cfg->tp_size > 1 ? P : H, P, P, es, dt);
+        p->kcfg[3] = make_kernel_cfg(kExpand, P, P, P, es, dt);
+        if (cfg->tp_size == 1 && !p->kcfg[0].ok) {
+            slora_status s = fail(SLORA_ERR_SHAPE, "no valid MBGMV split for hidden %lld", (long long)H);
+            delete p;
+            return s;
+        }
     }
     *out = p;
     return ok();
@@ -393,6 +449,7 @@ extern "C" slora_status slora_adapter_load(slora_pool_t p, int64_t id, int32_t r
                                            float scale, void* stream, int32_t* slot_out) {
     if (check_pool(p)) return SLORA_ERR_INVALID_ARG;
     if (rank < 1) return fail(SLORA_ERR_INVALID_ARG, "rank < 1");
+    if (rank > kRowCap) return fail(SLORA_ERR_SHAPE, "rank %d > %d (max rank of the MBGMV path)", rank, kRowCap);
     if (rank % p->N()) return fail(SLORA_ERR_INDIVISIBLE, "rank %d %% tp_size %d", rank, p->N());
     if (p->dev && !host_w) return fail(SLORA_ERR_INVALID_ARG, "host_w is NULL");
     if (!p->dev && host_w) return fail(SLORA_ERR_NO_DEVICE, "bookkeeping-only pool takes host_w = NULL");
@@ -573,24 +630,21 @@ extern "C" slora_status slora_gather_pages(slora_pool_t p, const int32_t* pages,
 
 // ------------------------------------------------------------------- batch
 namespace {
-constexpr int kRowCap = 64;    // A (and B) rows staged per unit
-constexpr int kTokCap = 8;     // x rows staged per unit
-constexpr int kVCap = 512;     // v entries per unit
-
+// Items = (segment x projection x token chunk); units = items packed by
+// first-fit decreasing on rank under the kernel's caps (kRowCap rows,
+// kTokCap token slots, kVCap v entries, kMaxItemsPerUnit items): an r = 64
+// item fills a unit alone, eight r = 8 items share one -- rank-heterogeneous
+// balancing without padding to a maximum rank.
 void build_units(slora_batch* b, int nproj) {
     auto& units = b->units[nproj];
     auto& items = b->items[nproj];
     units.clear();
     items.clear();
-    int rmax = 0;
-    for (const DevSeg& s : b->segs) rmax = std::max(rmax, s.rank);
-    const int row_cap = std::max(kRowCap, rmax);
-    const int v_cap = std::max(kVCap, rmax);
     struct It { DevItem it; int rank; };
     std::vector<It> all;
     for (int si = 0; si < int(b->segs.size()); ++si) {
         const DevSeg& s = b->segs[size_t(si)];
-        const int tmax = std::max(1, std::min(kTokCap, v_cap / s.rank));
+        const int tmax = std::max(1, std::min(kTokCap, kVCap / s.rank));
         for (int pi = 0; pi < nproj; ++pi)
             for (int t0 = 0; t0 < s.n_tok; t0 += tmax) {
                 DevItem it{};
@@ -601,7 +655,6 @@ void build_units(slora_batch* b, int nproj) {
                 all.push_back({it, s.rank});
             }
     }
-    // first-fit decreasing by rank (largest first = LPT order of units)
     std::stable_sort(all.begin(), all.end(), [](const It& a, const It& c) { return a.rank > c.rank; });
     struct Bin { std::vector<DevItem> its; int rows = 0, toks = 0, v = 0; };
     std::vector<Bin> bins;
@@ -609,7 +662,7 @@ void build_units(slora_batch* b, int nproj) {
         const int r = x.rank, nt = x.it.nt;
         Bin* target = nullptr;
         for (Bin& bn : bins)
-            if (bn.rows + r <= row_cap && bn.toks + nt <= kTokCap && bn.v + nt * r <= v_cap &&
+            if (bn.rows + r <= kRowCap && bn.toks + nt <= kTokCap && bn.v + nt * r <= kVCap &&
                 int(bn.its.size()) < kMaxItemsPerUnit) {
                 target = &bn;
                 break;
@@ -627,7 +680,6 @@ void build_units(slora_batch* b, int nproj) {
         target->v += nt * r;
         target->its.push_back(it);
     }
-    b->max_rows[nproj] = b->max_toks[nproj] = b->max_v[nproj] = 0;
     for (Bin& bn : bins) {
         DevUnit u{};
         u.item_begin = int32_t(items.size());
@@ -637,9 +689,41 @@ void build_units(slora_batch* b, int nproj) {
         u.ventries = bn.v;
         for (auto& it : bn.its) items.push_back(it);
         units.push_back(u);
-        b->max_rows[nproj] = std::max(b->max_rows[nproj], bn.rows);
-        b->max_toks[nproj] = std::max(b->max_toks[nproj], bn.toks);
-        b->max_v[nproj] = std::max(b->max_v[nproj], bn.v);
+    }
+}
+
+// LPT static schedule of units over the kernel's persistent clusters: units
+// by decreasing cost, each to the least-loaded cluster.  Cost = bytes one
+// cluster CTA streams for the unit + a fixed per-unit overhead.
+void build_schedule(slora_batch* b, const KernelCfg& k, int es, int nproj, std::vector<int32_t>& off,
+                    std::vector<int32_t>& sched) {
+    off.clear();
+    sched.clear();
+    const auto& units = b->units[nproj];
+    if (!k.ok || units.empty()) {
+        off.assign(1, 0);
+        return;
+    }
+    const int G = std::max(1, std::min<int>(k.n_clusters, int(units.size())));
+    const double KSb = k.mode == kExpand ? 0.0 : double(k.K / k.C) * es;
+    const double DSb = k.mode == kShrink ? 0.0 : double(k.D / k.C) * es;
+    std::vector<std::pair<double, int>> cost;
+    for (int u = 0; u < int(units.size()); ++u) {
+        const DevUnit& U = units[size_t(u)];
+        cost.push_back({U.rows * (KSb + DSb) + U.toks * KSb + 8192.0, u});
+    }
+    std::stable_sort(cost.begin(), cost.end(), [](auto& a, auto& c) { return a.first > c.first; });
+    std::vector<double> load(size_t(G), 0.0);
+    std::vector<std::vector<int32_t>> lists(static_cast<size_t>(G));
+    for (auto& cu : cost) {
+        size_t g = size_t(std::min_element(load.begin(), load.end()) - load.begin());
+        load[g] += cu.first;
+        lists[g].push_back(cu.second);
+    }
+    off.push_back(0);
+    for (auto& l : lists) {
+        for (int32_t u : l) sched.push_back(u);
+        off.push_back(int32_t(sched.size()));
     }
 }
 }  // namespace
@@ -720,11 +804,13 @@ extern "C" slora_status slora_batch_prepare(slora_batch_t b, const int64_t* tok_
         b->segs.push_back(sg);
     }
     for (int np = 1; np <= 4; ++np) build_units(b, np);
+    for (int kc = 0; kc < 4; ++kc)
+        for (int np = 1; np <= 4; ++np) build_schedule(b, p->kcfg[kc], p->es, np, b->sched_off[kc][np], b->sched[kc][np]);
     b->epoch = p->epoch;
     b->prepared = true;
     if (!p->dev) return ok();
 
-    // ---- upload: [segs][tok_idx][units/items for nproj 1..4]
+    // ---- upload: [segs][tok_idx][units/items per nproj][schedules per cfg x nproj]
     auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
     size_t off = 0;
     b->off_segs = off;
@@ -737,6 +823,13 @@ extern "C" slora_status slora_batch_prepare(slora_batch_t b, const int64_t* tok_
         b->off_items[np] = off;
         off = al(off + b->items[np].size() * sizeof(DevItem));
     }
+    for (int kc = 0; kc < 4; ++kc)
+        for (int np = 1; np <= 4; ++np) {
+            b->off_sched_off[kc][np] = off;
+            off = al(off + b->sched_off[kc][np].size() * sizeof(int32_t));
+            b->off_sched[kc][np] = off;
+            off = al(off + b->sched[kc][np].size() * sizeof(int32_t));
+        }
     const size_t need = std::max<size_t>(off, 256);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     CUDA_TRY(cudaSetDevice(p->cfg.device));
@@ -752,12 +845,20 @@ extern "C" slora_status slora_batch_prepare(slora_batch_t b, const int64_t* tok_
         b->blob_cap = cap;
     }
     uint8_t* h = static_cast<uint8_t*>(b->blob_host);
-    memcpy(h + b->off_segs, b->segs.data(), b->segs.size() * sizeof(DevSeg));
-    memcpy(h + b->off_tok, b->tok_idx.data(), b->tok_idx.size() * sizeof(int32_t));
+    auto put = [&](size_t o, const void* src, size_t n) {
+        if (n) memcpy(h + o, src, n);
+    };
+    put(b->off_segs, b->segs.data(), b->segs.size() * sizeof(DevSeg));
+    put(b->off_tok, b->tok_idx.data(), b->tok_idx.size() * sizeof(int32_t));
     for (int np = 1; np <= 4; ++np) {
-        memcpy(h + b->off_units[np], b->units[np].data(), b->units[np].size() * sizeof(DevUnit));
-        memcpy(h + b->off_items[np], b->items[np].data(), b->items[np].size() * sizeof(DevItem));
+        put(b->off_units[np], b->units[np].data(), b->units[np].size() * sizeof(DevUnit));
+        put(b->off_items[np], b->items[np].data(), b->items[np].size() * sizeof(DevItem));
     }
+    for (int kc = 0; kc < 4; ++kc)
+        for (int np = 1; np <= 4; ++np) {
+            put(b->off_sched_off[kc][np], b->sched_off[kc][np].data(), b->sched_off[kc][np].size() * sizeof(int32_t));
+            put(b->off_sched[kc][np], b->sched[kc][np].data(), b->sched[kc][np].size() * sizeof(int32_t));
+        }
     CUDA_TRY(cudaMemcpyAsync(b->blob_dev, b->blob_host, need, cudaMemcpyHostToDevice, s));
     CUDA_TRY(cudaEventRecord(b->upload_ev, s));
     b->upload_pending = true;
@@ -777,28 +878,6 @@ extern "C" slora_status slora_batch_get_info(slora_batch_t b, slora_batch_info* 
 
 // ----------------------------------------------------------------- compute
 namespace {
-// Split count C: the largest of 16, 8, 4, 2, 1 that divides K and D into
-// 16-byte-multiple slices of >= 512 bytes (>= 1 slice when impossible) and
-// keeps each K slice inside one page.  Env SLORA_SPLIT overrides.
-int choose_split(int64_t K, int64_t D, int64_t P, int es, bool need_k, bool need_d) {
-    static int forced = [] {
-        const char* s = getenv("SLORA_SPLIT");
-        return s ? atoi(s) : 0;
-    }();
-    auto valid = [&](int C) {
-        if (need_k && (K % C || ((K / C) * es) % 16 || P % (K / C))) return false;
-        if (need_d && (D % C || ((D / C) * es) % 16)) return false;
-        return true;
-    };
-    auto big = [&](int C) { return (!need_k || (K / C) * es >= 512) && (!need_d || (D / C) * es >= 512); };
-    if (forced > 0 && valid(forced)) return forced;
-    for (int C : {16, 8, 4, 2, 1})
-        if (valid(C) && big(C)) return C;
-    for (int C : {1, 2, 4, 8, 16})
-        if (valid(C)) return C;
-    return 0;
-}
-
 slora_status common_checks(slora_pool* p, slora_batch* b, int32_t layer, uint32_t mask) {
     if (!p || !b) return fail(SLORA_ERR_INVALID_ARG, "null pool/batch");
     if (b->pool != p) return fail(SLORA_ERR_INVALID_ARG, "batch belongs to another pool");
@@ -814,8 +893,9 @@ bool aligned16(const void* ptr, int64_t ld, int es) {
     return !(reinterpret_cast<uintptr_t>(ptr) & 15) && (ld * es) % 16 == 0;
 }
 
-void fill_common(slora_pool* p, slora_batch* b, int32_t layer, uint32_t mask, LoraParams& q) {
+void fill_common(slora_pool* p, slora_batch* b, int kc, int32_t layer, uint32_t mask, LoraParams& q) {
     memset(&q, 0, sizeof(q));
+    const KernelCfg& k = p->kcfg[kc];
     q.pool = p->cfg.device_buffer;
     q.page_elems = p->P;
     q.slot_tab = p->slot_tab_dev;
@@ -828,11 +908,14 @@ void fill_common(slora_pool* p, slora_batch* b, int32_t layer, uint32_t mask, Lo
     q.nproj = np;
     q.units = reinterpret_cast<const DevUnit*>(base + b->off_units[np]);
     q.items = reinterpret_cast<const DevItem*>(base + b->off_items[np]);
-    q.n_units = int32_t(b->units[np].size());
+    q.sched_off = reinterpret_cast<const int32_t*>(base + b->off_sched_off[kc][np]);
+    q.sched = reinterpret_cast<const int32_t*>(base + b->off_sched[kc][np]);
+    q.n_clusters = int32_t(b->sched_off[kc][np].size()) - 1;
     q.layer = layer;
-    q.rcap = std::max(1, b->max_rows[np]);
-    q.tcap = std::max(1, b->max_toks[np]);
-    q.vcap = std::max(1, b->max_v[np]);
+    q.C = k.C;
+    q.K = int32_t(k.K);
+    q.D = int32_t(k.D);
+    q.ns = k.ns;
     q.NR = b->NR;
     const int N = p->N();
     for (int pj = 0; pj < 4; ++pj) {
@@ -841,12 +924,13 @@ void fill_common(slora_pool* p, slora_batch* b, int32_t layer, uint32_t mask, Lo
     }
 }
 
-slora_status launch(slora_pool* p, LoraParams& q, int mode, void* stream) {
-    const size_t smem = lora_smem_bytes(q, mode, p->es);
-    if (smem > size_t(227) * 1024) return fail(SLORA_ERR_SHAPE, "unit needs %zu bytes of shared memory", smem);
+slora_status launch(slora_pool* p, int kc, LoraParams& q, void* stream) {
+    const KernelCfg& k = p->kcfg[kc];
+    if (!k.ok) return fail(SLORA_ERR_SHAPE, "no valid kernel configuration for K=%lld D=%lld", (long long)k.K,
+                           (long long)k.D);
     CUDA_TRY(cudaSetDevice(p->cfg.device));
     const int dt = p->cfg.dtype == SLORA_F32 ? kF32 : (p->cfg.dtype == SLORA_F16 ? kF16 : kBF16);
-    CUDA_TRY(launch_lora(q, mode, dt, static_cast<cudaStream_t>(stream), smem));
+    CUDA_TRY(launch_lora(q, k.mode, dt, static_cast<cudaStream_t>(stream), k.smem));
     return ok();
 }
 }  // namespace
@@ -865,10 +949,7 @@ extern "C" slora_status slora_lora_apply(slora_pool_t p, slora_batch_t b, int32_
             if (!y[pj] || !aligned16(y[pj], ldy[pj], p->es) || ldy[pj] < p->cfg.hidden)
                 return fail(SLORA_ERR_SHAPE, "y[%d] alignment/stride", pj);
     LoraParams q;
-    fill_common(p, b, layer, mask, q);
-    q.K = q.D = int32_t(p->cfg.hidden);
-    q.C = choose_split(q.K, q.D, p->P, p->es, true, true);
-    if (!q.C) return fail(SLORA_ERR_SHAPE, "hidden %lld cannot be split into 16-byte slices", (long long)p->cfg.hidden);
+    fill_common(p, b, 0, layer, mask, q);
     q.x = x;
     q.ldx = ldx;
     for (int pj = 0; pj < 4; ++pj) {
@@ -876,7 +957,7 @@ extern "C" slora_status slora_lora_apply(slora_pool_t p, slora_batch_t b, int32_
         q.ldy[pj] = ldy[pj];
     }
     q.v_blocks = 1;
-    return launch(p, q, kFused, stream);
+    return launch(p, 0, q, stream);
 }
 
 extern "C" slora_status slora_lora_v_elems(slora_batch_t b, uint32_t mask, int32_t div, int64_t* out) {
@@ -897,20 +978,16 @@ extern "C" slora_status slora_lora_shrink(slora_pool_t p, slora_batch_t b, int32
     if (N > 1 && (mask & 0x8) && (mask & 0x7))
         return fail(SLORA_ERR_INVALID_ARG, "under TP shrink q/k/v and o in separate calls");
     if (b->adapted == 0) return ok();
-    const bool is_o = (mask & 0x8) != 0;
-    const int64_t K = (N > 1 && is_o) ? p->P : p->cfg.hidden;
+    const int kc = (N > 1 && (mask & 0x8)) ? 2 : 1;
+    const int64_t K = p->kcfg[kc].K;
     if (!x || !v) return fail(SLORA_ERR_INVALID_ARG, "null x/v");
     if (!aligned16(x, ldx, p->es) || ldx < K) return fail(SLORA_ERR_SHAPE, "x alignment/stride");
     LoraParams q;
-    fill_common(p, b, layer, mask, q);
-    q.K = int32_t(K);
-    q.D = int32_t(p->P);
-    q.C = choose_split(q.K, q.D, p->P, p->es, true, false);
-    if (!q.C) return fail(SLORA_ERR_SHAPE, "cannot split K=%lld", (long long)K);
+    fill_common(p, b, kc, layer, mask, q);
     q.x = x;
     q.ldx = ldx;
     q.v_out = v;
-    return launch(p, q, kShrink, stream);
+    return launch(p, kc, q, stream);
 }
 
 extern "C" slora_status slora_lora_expand(slora_pool_t p, slora_batch_t b, int32_t layer, uint32_t mask,
@@ -928,18 +1005,14 @@ extern "C" slora_status slora_lora_expand(slora_pool_t p, slora_batch_t b, int32
             if (!y[pj] || !aligned16(y[pj], ldy[pj], p->es) || ldy[pj] < p->P)
                 return fail(SLORA_ERR_SHAPE, "y[%d] alignment/stride", pj);
     LoraParams q;
-    fill_common(p, b, layer, mask, q);
-    q.K = int32_t(p->P);
-    q.D = int32_t(p->P);
-    q.C = choose_split(q.K, q.D, p->P, p->es, false, true);
-    if (!q.C) return fail(SLORA_ERR_SHAPE, "cannot split D=%lld", (long long)p->P);
+    fill_common(p, b, 3, layer, mask, q);
     q.v_in = v;
     q.v_blocks = v_blocks;
     for (int pj = 0; pj < 4; ++pj) {
         q.y[pj] = y[pj];
         q.ldy[pj] = ldy[pj];
     }
-    return launch(p, q, kExpand, stream);
+    return launch(p, 3, q, stream);
 }
 
 extern "C" slora_status slora_sync(slora_pool_t p, void* stream) {

@@ -1,20 +1,40 @@
 // kernels.cu -- sm_100a kernels of the S-LoRA hot path.
 //
-//   lora_unit_kernel<T, MODE>   MBGMV gather-shrink-expand over Unified Paging
-//       (Sec. 5.3; Eq. lora_factored).
-//       One thread-block cluster of C CTAs per work unit; CTA c owns the c-th
-//       1/C slice of the hidden dimension.  Page rows of A and B and the
-//       unit's x rows are staged into shared memory by cp.async.bulk
-//       (one bulk copy per page slice, completion on an mbarrier), so a single
-//       issuing warp puts the whole unit's bytes in flight at once.  Shrink:
-//       fp32 dot products over the CTA's K slice with warp-shuffle reductions;
-//       the C partial v vectors are combined through distributed shared
-//       memory (reduce-scatter + broadcast, fixed order c = 0..C-1); expand:
-//       fp32 axpys of the B page slices into y.  The rank-r intermediate never
-//       leaves the cluster.  Reduction order depends only on (K, C), never on
-//       page placement or batch order.
-//   scatter_kernel   adapter load: staging -> pages (A transposed).
-//   gather_kernel    test-only page gather.
+// mbgmv_kernel<T, MODE>: MBGMV gather-shrink-expand over Unified Paging
+//   (Sec. 5.3; Eq. lora_factored).
+//
+//   Persistent, warp-specialized, one thread-block cluster of C CTAs per
+//   schedule lane.  CTA c of a cluster owns the c-th 1/C slice of the hidden
+//   dimension (K for the shrink, D for the expand).  Each cluster walks its
+//   LPT-balanced list of work units (host-built, api.cpp).
+//
+//   producer warp (warp 8): resolves the unit's items -> adapter page tables,
+//     then streams every page slice the unit needs -- x rows into a
+//     double-buffered unit stage, A rows and then B rows into a ring of
+//     kRowsPerSlot-row slots -- with cp.async.bulk (TMA engine), completion
+//     tracked by mbarrier transaction counts.  It runs ahead of the
+//     consumers by the ring depth, across unit boundaries, so the next unit's
+//     pages are in flight while the current one is expanded.
+//   consumer warps (0..7):
+//     shrink: one A page-slice row per warp, fp32 dot products with the
+//       unit's x rows (16-byte smem vectors, warp-shuffle reductions); each
+//       partial v entry is pushed straight into slot [c] of every cluster
+//       CTA's exchange buffer (st.shared::cluster), then one remote mbarrier
+//       arrive per peer.  Every CTA sums the C partials in the fixed order
+//       c = 0..C-1 -> identical v on all CTAs; the rank-r intermediate never
+//       leaves distributed shared memory.
+//     expand: each thread owns 8 output columns (one 16-byte vector) of a
+//       subset of the unit's tokens and accumulates v_j * B_j over the B rows
+//       in fp32 registers; y is prefetched into registers at the start and
+//       written back once (one rounding).
+//   Reduction order depends only on (K, C): results are bit-identical under
+//   any page placement, batch permutation or schedule.
+//
+// MODE kShrink (TP): no expand; v written to global in the C-ABI layout.
+// MODE kExpand (TP): no shrink; v read from global (v_blocks rank blocks).
+//
+// scatter_kernel: adapter load, staging -> pages (A transposed).
+// gather_kernel:  test-only page gather.
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
@@ -40,9 +60,18 @@ __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
 __device__ __forceinline__ void fence_mbar_init() {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                  : "memory");
+}
+// arrive on the barrier at the same smem offset in cluster CTA `rank`
+__device__ __forceinline__ void mbar_arrive_remote(uint64_t* bar, uint32_t rank) {
+    uint32_t a;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(a) : "r"(smem_u32(bar)), "r"(rank));
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(a) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     asm volatile(
@@ -53,8 +82,17 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
-// 1-D bulk copy global -> own shared memory, completes on `bar` (TMA engine;
-// SASS UBLKCP).  bytes % 16 == 0, both addresses 16-byte aligned.
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAITC_%=:\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAITC_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+// 1-D bulk copy global -> own shared memory on the TMA engine (SASS UBLKCP),
+// completing `bytes` of transaction count on `bar`.
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
     asm volatile(
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -70,22 +108,24 @@ __device__ __forceinline__ uint32_t cluster_ctarank() {
 __device__ __forceinline__ void cluster_sync_all() {
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
-__device__ __forceinline__ uint32_t mapa_u32(uint32_t addr, uint32_t rank) {
-    uint32_t r;
-    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+__device__ __forceinline__ void st_dsmem(const float* local, uint32_t rank, float v) {
+    uint32_t a;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(a) : "r"(smem_u32(local)), "r"(rank));
+    asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(a), "f"(v) : "memory");
+}
+__device__ __forceinline__ void fence_cluster() { asm volatile("fence.acq_rel.cluster;" ::: "memory"); }
+__device__ __forceinline__ void consumer_sync() {
+    asm volatile("bar.sync 1, %0;" ::"n"(kConsumerWarps * 32) : "memory");
+}
+__device__ __forceinline__ uint4 ld_global_nc(const void* p) {
+    uint4 r;
+    asm volatile("ld.global.nc.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
     return r;
-}
-__device__ __forceinline__ float ld_dsmem(uint32_t addr) {
-    float v;
-    asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(addr) : "memory");
-    return v;
-}
-__device__ __forceinline__ void st_dsmem(uint32_t addr, float v) {
-    asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
 }
 
 // ---------------------------------------------------- element conversions
-// A 16-byte vector holds VE elements.
 template <typename T> struct Vec;
 template <> struct Vec<float> {
     static constexpr int VE = 4;
@@ -135,231 +175,425 @@ template <> struct Vec<__nv_bfloat16> {
     }
 };
 
-struct SmemLayout {
-    size_t a, b, x, vp, v, bar, total;
+// ------------------------------------------------------------ smem layout
+struct ItemMeta {
+    const int32_t* tab;  // page table of (adapter, layer, proj): A rows then B rows
+    int32_t rowA, ra;    // first A row in the unit stream, stored A rows (r / a_div)
+    int32_t rowB, r;     // first B row, B rows (= rank)
+    int32_t ts, nt;      // token slots
+    int32_t v_off;       // first v entry (local units: r/a_div per token in shrink modes)
+    int32_t vf_off;      // first v entry in full-rank units (expand)
+    int32_t proj, arp;   // projection id, pages per stored A row
+    float scale;
+    int32_t seg, t0;
+    int32_t pad;
 };
-__host__ __device__ inline SmemLayout smem_layout(const LoraParams& p, int mode, int es) {
+struct UnitMeta {
+    int32_t n_items, RA, RB, toks, E, EF, pad0, pad1;
+    int32_t tok[kTokCap];        // token row of each slot
+    int32_t tok_item[kTokCap];   // item of each slot
+    ItemMeta it[kMaxItemsPerUnit];
+    uint8_t rowA_item[kRowCap];
+    uint8_t rowB_item[kRowCap];
+};
+
+struct SmemLayout {
+    size_t bars, meta, xbuf, vfull, xrows, ring, total, row_bytes;
+};
+__host__ __device__ inline size_t al128(size_t x) { return (x + 127) & ~size_t(127); }
+__host__ __device__ inline SmemLayout smem_layout(int mode, int C, int64_t K, int64_t D, int ns, int es) {
     SmemLayout L{};
-    const size_t KS = p.K / p.C, DS = p.D / p.C;
+    const size_t KS = size_t(K / C), DS = size_t(D / C);
+    size_t rb = 0;
+    if (mode != kExpand) rb = KS * es;
+    if (mode != kShrink && DS * es > rb) rb = DS * es;
+    L.row_bytes = (rb + 15) & ~size_t(15);
     size_t off = 0;
-    auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 15) & ~size_t(15); return o; };
-    L.bar = take(16);
-    L.a = take(mode == kExpand ? 0 : size_t(p.rcap) * KS * es);
-    L.b = take(mode == kShrink ? 0 : size_t(p.rcap) * DS * es);
-    L.x = take(mode == kExpand ? 0 : size_t(p.tcap) * KS * es);
-    L.vp = take(mode == kExpand ? 0 : size_t(p.vcap) * 4);
-    L.v = take(mode == kShrink ? 0 : size_t(p.vcap) * 4);
+    L.bars = off;
+    off = al128(off + sizeof(uint64_t) * (2 * kMaxSlots + 6));
+    L.meta = off;
+    off = al128(off + 2 * sizeof(UnitMeta));
+    L.xbuf = off;
+    off = al128(off + (mode != kExpand ? size_t(2) * C * kVCap * 4 : 0));
+    L.vfull = off;
+    off = al128(off + size_t(kVCap) * 4);
+    L.xrows = off;
+    off = al128(off + (mode != kExpand ? size_t(2) * kTokCap * KS * es : 0));
+    L.ring = off;
+    off = al128(off + size_t(ns) * kRowsPerSlot * L.row_bytes);
     L.total = off;
     return L;
+}
+size_t lora_smem_bytes(int mode, int C, int64_t K, int64_t D, int ns, int esize) {
+    return smem_layout(mode, C, K, D, ns, esize).total;
 }
 
 // ------------------------------------------------------------ the kernel
 template <typename T, int MODE>
-__global__ void __launch_bounds__(kThreads) lora_unit_kernel(const __grid_constant__ LoraParams p) {
+__global__ void __launch_bounds__(kThreads, 1) mbgmv_kernel(const __grid_constant__ LoraParams p) {
     extern __shared__ __align__(128) unsigned char smem[];
     using V = Vec<T>;
     constexpr int VE = V::VE;
     constexpr int ES = sizeof(T);
     const int C = p.C;
-    const int unit = blockIdx.x / C;
+    const int cl = int(blockIdx.x) / C;
     const int c = (MODE == kExpand) ? int(blockIdx.x % C) : int(cluster_ctarank());
-    const int KS = p.K / C, DS = p.D / C;
+    const int64_t KS = p.K / C, DS = p.D / C;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const SmemLayout L = smem_layout(p, MODE, ES);
-    uint64_t* bar = reinterpret_cast<uint64_t*>(smem + L.bar);
-    T* sA = reinterpret_cast<T*>(smem + L.a);
-    T* sB = reinterpret_cast<T*>(smem + L.b);
-    T* sX = reinterpret_cast<T*>(smem + L.x);
-    float* sVp = reinterpret_cast<float*>(smem + L.vp);
-    float* sV = reinterpret_cast<float*>(smem + L.v);
+    const SmemLayout L = smem_layout(MODE, C, p.K, p.D, p.ns, ES);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.bars);
+    uint64_t* empty = full + kMaxSlots;
+    uint64_t* xfull = empty + kMaxSlots;
+    uint64_t* xempty = xfull + 2;
+    uint64_t* exch = xempty + 2;
+    UnitMeta* meta = reinterpret_cast<UnitMeta*>(smem + L.meta);
+    float* xbuf = reinterpret_cast<float*>(smem + L.xbuf);  // [2][C][kVCap]
+    float* vfull = reinterpret_cast<float*>(smem + L.vfull);
+    T* xrows = reinterpret_cast<T*>(smem + L.xrows);        // [2][kTokCap][KS]
+    unsigned char* ring = smem + L.ring;                     // [ns][kRowsPerSlot][row_bytes]
+    const int ns = p.ns;
+    const size_t rowb = L.row_bytes;
 
-    const DevUnit U = p.units[unit];
+    if (tid == 0) {
+        for (int s = 0; s < ns; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], kConsumerWarps);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&xfull[b], 1);
+            mbar_init(&xempty[b], kConsumerWarps);
+            mbar_init(&exch[b], C);
+        }
+        fence_mbar_init();
+    }
+    if (MODE == kExpand) __syncthreads();
+    else cluster_sync_all();  // peers arrive on our barriers / write our smem
+
+    const int u_beg = p.sched_off[cl], u_end = p.sched_off[cl + 1];
     const T* pool = reinterpret_cast<const T*>(p.pool);
     const int64_t P = p.page_elems;
 
-    if (tid == 0) {
-        mbar_init(&bar[0], 1);
-        mbar_init(&bar[1], 1);
-        fence_mbar_init();
-    }
-    __syncthreads();
-
-    // ---------------- issue every page-slice copy of the unit (warp 0) ----
-    if (warp == 0) {
-        if (lane == 0) {
-            uint32_t bytes_ax = 0, bytes_b = 0;
-            for (int ii = 0; ii < U.n_items; ++ii) {
-                const DevItem it = p.items[U.item_begin + ii];
+    if (warp == kConsumerWarps) {
+        // ============================ producer ============================
+        int slot = 0;
+        uint32_t lap = 0;
+        for (int i = 0; u_beg + i < u_end; ++i) {
+            const int ub = i & 1;
+            if (i >= 2) mbar_wait(&xempty[ub], ((i >> 1) - 1) & 1);
+            UnitMeta& M = meta[ub];
+            const DevUnit U = p.units[p.sched[u_beg + i]];
+            // ---- resolve items (one lane per item)
+            int ra = 0, rr = 0, ve = 0, vf = 0;
+            ItemMeta im{};
+            if (lane < U.n_items) {
+                const DevItem it = p.items[U.item_begin + lane];
                 const DevSeg sg = p.segs[it.seg];
                 const int proj = p.proj_ids[it.pi];
-                if (MODE != kExpand) bytes_ax += uint32_t(sg.rank / p.a_div[proj] + it.nt) * KS * ES;
-                if (MODE != kShrink) bytes_b += uint32_t(sg.rank) * DS * ES;
+                const int div = (MODE == kExpand) ? 1 : p.a_div[proj];
+                im.tab = p.slot_tab[sg.slot] + int64_t((p.layer * 4 + proj) * 2) * sg.rank;
+                im.ra = sg.rank / div;
+                im.r = sg.rank;
+                im.ts = it.tok_slot;
+                im.nt = it.nt;
+                im.v_off = it.v_off / div;
+                im.vf_off = it.v_off;
+                im.proj = proj;
+                im.arp = p.a_row_pages[proj];
+                im.scale = sg.scale;
+                im.seg = it.seg;
+                im.t0 = it.t0;
+                ra = im.ra;
+                rr = im.r;
+                ve = im.nt * im.ra;
+                vf = im.nt * im.r;
+                for (int t = 0; t < it.nt; ++t) {
+                    M.tok[it.tok_slot + t] = p.tok_idx[sg.tok_off + it.t0 + t];
+                    M.tok_item[it.tok_slot + t] = lane;
+                }
             }
-            if (MODE != kExpand) mbar_arrive_expect_tx(&bar[0], bytes_ax);
-            if (MODE != kShrink) mbar_arrive_expect_tx(&bar[1], bytes_b);
-        }
-        __syncwarp();
-        for (int ii = 0; ii < U.n_items; ++ii) {
-            const DevItem it = p.items[U.item_begin + ii];
-            const DevSeg sg = p.segs[it.seg];
-            const int proj = p.proj_ids[it.pi];
-            const int32_t* tab = p.slot_tab[sg.slot] + int64_t((p.layer * 4 + proj) * 2) * sg.rank;
+            // exclusive prefix sums over items -> row offsets
+            int pa = ra, pb = rr;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int xa = __shfl_up_sync(0xffffffffu, pa, o);
+                const int xb = __shfl_up_sync(0xffffffffu, pb, o);
+                if (lane >= o) { pa += xa; pb += xb; }
+            }
+            if (lane < U.n_items) {
+                im.rowA = pa - ra;
+                im.rowB = pb - rr;
+                M.it[lane] = im;
+                for (int j = 0; j < ra; ++j) M.rowA_item[im.rowA + j] = uint8_t(lane);
+                for (int j = 0; j < rr; ++j) M.rowB_item[im.rowB + j] = uint8_t(lane);
+            }
+            int tot_ve = ve, tot_vf = vf;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                tot_ve += __shfl_xor_sync(0xffffffffu, tot_ve, o);
+                tot_vf += __shfl_xor_sync(0xffffffffu, tot_vf, o);
+            }
+            const int RA = __shfl_sync(0xffffffffu, pa, 31);
+            const int RB = __shfl_sync(0xffffffffu, pb, 31);
+            if (lane == 0) {
+                M.n_items = U.n_items;
+                M.RA = RA;
+                M.RB = RB;
+                M.toks = U.toks;
+                M.E = tot_ve;
+                M.EF = tot_vf;
+            }
+            __syncwarp();
+            // ---- x rows of the unit (meta is published by the same arrive)
             if (MODE != kExpand) {
-                const int rl = sg.rank / p.a_div[proj];
-                const int rp = p.a_row_pages[proj];
-                const int64_t k0 = int64_t(c) * KS;
-                for (int j = lane; j < rl; j += 32) {
-                    const int32_t page = tab[j * rp + int(k0 / P)];
-                    bulk_g2s(sA + size_t(it.row_off + j) * KS, pool + page * P + (k0 % P), KS * ES, &bar[0]);
+                if (lane == 0) mbar_arrive_expect_tx(&xfull[ub], uint32_t(U.toks * KS * ES));
+                __syncwarp();
+                if (lane < U.toks) {
+                    const T* x = reinterpret_cast<const T*>(p.x);
+                    bulk_g2s(xrows + (size_t(ub) * kTokCap + lane) * KS, x + int64_t(M.tok[lane]) * p.ldx + c * KS,
+                             uint32_t(KS * ES), &xfull[ub]);
                 }
-                const T* x = reinterpret_cast<const T*>(p.x);
-                for (int t = lane; t < it.nt; t += 32) {
-                    const int32_t tok = p.tok_idx[sg.tok_off + it.t0 + t];
-                    bulk_g2s(sX + size_t(it.tok_slot + t) * KS, x + tok * p.ldx + k0, KS * ES, &bar[0]);
+            } else {
+                if (lane == 0) mbar_arrive(&xfull[ub]);
+            }
+            // ---- A rows (K slice c), then B rows (D slice c)
+            for (int phase = 0; phase < 2; ++phase) {
+                if (phase == 0 && MODE == kExpand) continue;
+                if (phase == 1 && MODE == kShrink) continue;
+                const int R = phase == 0 ? RA : RB;
+                for (int base = 0; base < R; base += kRowsPerSlot) {
+                    mbar_wait(&empty[slot], (lap & 1) ^ 1);
+                    const int row = base + lane;
+                    uint32_t bytes = 0;
+                    if (lane < kRowsPerSlot && row < R) bytes = uint32_t((phase == 0 ? KS : DS) * ES);
+                    uint32_t tot = bytes;
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+                    if (lane == 0) mbar_arrive_expect_tx(&full[slot], tot);
+                    __syncwarp();
+                    if (bytes) {
+                        unsigned char* dst = ring + (size_t(slot) * kRowsPerSlot + lane) * rowb;
+                        if (phase == 0) {
+                            const ItemMeta& it = M.it[M.rowA_item[row]];
+                            const int j = row - it.rowA;
+                            int64_t k = int64_t(c) * KS;
+                            const int64_t kend = k + KS;
+                            while (k < kend) {  // a slice may span pages (TP q/k/v rows)
+                                const int32_t page = it.tab[j * it.arp + int(k / P)];
+                                const int64_t len = min(P - k % P, kend - k);
+                                bulk_g2s(dst, pool + int64_t(page) * P + k % P, uint32_t(len * ES), &full[slot]);
+                                dst += len * ES;
+                                k += len;
+                            }
+                        } else {
+                            const ItemMeta& it = M.it[M.rowB_item[row]];
+                            const int j = row - it.rowB;
+                            const int32_t page = it.tab[it.r + j];
+                            bulk_g2s(dst, pool + int64_t(page) * P + int64_t(c) * DS, uint32_t(DS * ES), &full[slot]);
+                        }
+                    }
+                    if (++slot == ns) { slot = 0; ++lap; }
                 }
+            }
+        }
+    } else {
+        // ============================ consumers ===========================
+        int slot = 0;
+        uint32_t lap = 0;
+        const int nvec_k = int(KS / VE);
+        const int cvs = int(DS / VE);
+        const int nwc = (cvs + 31) / 32;                    // warps covering the columns
+        const int ntg = kConsumerWarps / (nwc > 0 ? nwc : 1); // token groups
+        const int wc = warp % (nwc > 0 ? nwc : 1);
+        const int tg = warp / (nwc > 0 ? nwc : 1);
+        const int cv = wc * 32 + lane;
+        for (int i = 0; u_beg + i < u_end; ++i) {
+            const int ub = i & 1;
+            mbar_wait(&xfull[ub], (i >> 1) & 1);
+            const UnitMeta& M = meta[ub];
+            if (MODE != kExpand) {
+                // ------------------------------ shrink ------------------------------
+                const T* xr = xrows + size_t(ub) * kTokCap * KS;
+                float* xb = xbuf + size_t(ub) * C * kVCap;
+                for (int base = 0; base < M.RA; base += kRowsPerSlot) {
+                    mbar_wait(&full[slot], lap & 1);
+                    const int row = base + warp;
+                    if (row < M.RA) {
+                        const ItemMeta& it = M.it[M.rowA_item[row]];
+                        const int j = row - it.rowA;
+                        const uint4* arow = reinterpret_cast<const uint4*>(ring + (size_t(slot) * kRowsPerSlot + warp) * rowb);
+                        float acc[kTokCap];
+#pragma unroll
+                        for (int t = 0; t < kTokCap; ++t) acc[t] = 0.f;
+                        for (int q = lane; q < nvec_k; q += 32) {
+                            float a[VE];
+                            V::to_f32(arow[q], a);
+#pragma unroll
+                            for (int t = 0; t < kTokCap; ++t) {
+                                if (t < it.nt) {
+                                    float xv[VE];
+                                    V::to_f32(reinterpret_cast<const uint4*>(xr + size_t(it.ts + t) * KS)[q], xv);
+#pragma unroll
+                                    for (int e = 0; e < VE; ++e) acc[t] = fmaf(xv[e], a[e], acc[t]);
+                                }
+                            }
+                        }
+#pragma unroll
+                        for (int t = 0; t < kTokCap; ++t) {
+                            if (t < it.nt) {
+                                float s = acc[t];
+#pragma unroll
+                                for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+                                acc[t] = s;
+                            }
+                        }
+                        // lane (t, cc) pushes token t's partial into CTA cc's slot [c]
+                        for (int w = lane; w < it.nt * C; w += 32) {
+                            const int t = w / C, cc = w % C;
+                            float s = 0.f;
+#pragma unroll
+                            for (int tt = 0; tt < kTokCap; ++tt)
+                                if (tt == t) s = acc[tt];
+                            const float* dst = xb + size_t(c) * kVCap + it.v_off + t * it.ra + j;
+                            st_dsmem(dst, uint32_t(cc), s);
+                        }
+                    }
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&empty[slot]);
+                    if (++slot == ns) { slot = 0; ++lap; }
+                }
+                fence_cluster();
+                consumer_sync();
+                if (tid == 0)
+                    for (int cc = 0; cc < C; ++cc) mbar_arrive_remote(&exch[ub], uint32_t(cc));
+                mbar_wait_cluster(&exch[ub], (i >> 1) & 1);
+                // combine the C partials in fixed order
+                for (int e = tid; e < M.E; e += kConsumerWarps * 32) {
+                    float s = 0.f;
+                    for (int cc = 0; cc < C; ++cc) s += xb[size_t(cc) * kVCap + e];
+                    if (MODE == kFused) {
+                        vfull[e] = s;
+                    } else if (e % C == c) {
+                        // global v layout: [proj idx][segment][token][r/div]
+                        int ii = 0;
+                        while (ii + 1 < M.n_items && M.it[ii + 1].v_off <= e) ++ii;
+                        const ItemMeta& it = M.it[ii];
+                        const DevSeg sg = p.segs[it.seg];
+                        const int div = it.r / it.ra;
+                        int pi = 0;
+                        for (int q = 0; q < p.nproj; ++q)
+                            if (p.proj_ids[q] == it.proj) pi = q;
+                        const int64_t base = int64_t(pi) * (p.NR / div) + (sg.vrow_off + int64_t(it.t0) * it.r) / div;
+                        p.v_out[base + (e - it.v_off)] = s;
+                    }
+                }
+                consumer_sync();
+            } else {
+                // v from global: block layout of slora_lora_expand
+                const int vb = p.v_blocks;
+                const int64_t stride = int64_t(p.nproj) * (p.NR / vb);
+                for (int e = tid; e < M.EF; e += kConsumerWarps * 32) {
+                    int ii = 0;
+                    while (ii + 1 < M.n_items && M.it[ii + 1].vf_off <= e) ++ii;
+                    const ItemMeta& it = M.it[ii];
+                    const DevSeg sg = p.segs[it.seg];
+                    int pi = 0;
+                    for (int q = 0; q < p.nproj; ++q)
+                        if (p.proj_ids[q] == it.proj) pi = q;
+                    const int r = it.r, rb = r / vb;
+                    const int le = e - it.vf_off, t = le / r, j = le % r;
+                    const int64_t base = int64_t(pi) * (p.NR / vb) + (sg.vrow_off + int64_t(it.t0) * r) / vb;
+                    vfull[e] = p.v_in[int64_t(j / rb) * stride + base + int64_t(t) * rb + (j % rb)];
+                }
+                consumer_sync();
             }
             if (MODE != kShrink) {
-                const int32_t* tabB = tab + sg.rank;
-                const int64_t d0 = int64_t(c) * DS;
-                for (int j = lane; j < sg.rank; j += 32) {
-                    const int32_t page = tabB[j];
-                    bulk_g2s(sB + size_t(it.row_off + j) * DS, pool + page * P + d0, DS * ES, &bar[1]);
-                }
-            }
-        }
-    }
-
-    if (MODE != kExpand) {
-        // ---------------- shrink: partial v over this CTA's K slice -------
-        mbar_wait(&bar[0], 0);
-        const int nvec = KS / VE;
-        for (int ii = 0; ii < U.n_items; ++ii) {
-            const DevItem it = p.items[U.item_begin + ii];
-            const DevSeg sg = p.segs[it.seg];
-            const int rl = sg.rank / p.a_div[p.proj_ids[it.pi]];
-            for (int j = warp; j < rl; j += kThreads / 32) {
-                const T* arow = sA + size_t(it.row_off + j) * KS;
-                for (int t = 0; t < it.nt; ++t) {
-                    const T* xrow = sX + size_t(it.tok_slot + t) * KS;
-                    float acc = 0.f;
-                    for (int q = lane; q < nvec; q += 32) {
-                        float a[VE], xv[VE];
-                        V::to_f32(reinterpret_cast<const uint4*>(arow)[q], a);
-                        V::to_f32(reinterpret_cast<const uint4*>(xrow)[q], xv);
+                // ------------------------------ expand ------------------------------
+                uint4 yv[kTokCap];
+                float acc[kTokCap][VE];
 #pragma unroll
-                        for (int e = 0; e < VE; ++e) acc = fmaf(xv[e], a[e], acc);
+                for (int t = 0; t < kTokCap; ++t) {
+#pragma unroll
+                    for (int e = 0; e < VE; ++e) acc[t][e] = 0.f;
+                    if (t % ntg == tg && t < M.toks && cv < cvs) {
+                        const ItemMeta& it = M.it[M.tok_item[t]];
+                        const T* y = reinterpret_cast<const T*>(p.y[it.proj]);
+                        yv[t] = *reinterpret_cast<const uint4*>(y + int64_t(M.tok[t]) * p.ldy[it.proj] + c * DS +
+                                                                int64_t(cv) * VE);
                     }
-#pragma unroll
-                    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-                    if (lane == 0) sVp[it.v_off / p.a_div[p.proj_ids[it.pi]] + t * rl + j] = acc;
                 }
-            }
-        }
-        __syncthreads();
-        // ---------------- combine the C partials (DSMEM) -----------------
-        // entries of this unit in "local" units (rank / a_div per item)
-        int E = 0;
-        for (int ii = 0; ii < U.n_items; ++ii) {
-            const DevItem it = p.items[U.item_begin + ii];
-            E += it.nt * (p.segs[it.seg].rank / p.a_div[p.proj_ids[it.pi]]);
-        }
-        cluster_sync_all();  // every CTA's sVp is complete and visible
-        const int per = (E + C - 1) / C;
-        const int e0 = c * per, e1 = min(E, e0 + per);
-        for (int e = e0 + tid; e < e1; e += kThreads) {
-            const uint32_t a_local = smem_u32(sVp + e);
-            float s = 0.f;
-            for (int cc = 0; cc < C; ++cc) s += ld_dsmem(mapa_u32(a_local, cc));
-            if (MODE == kFused) {
-                const uint32_t v_local = smem_u32(sV + e);
-                for (int cc = 0; cc < C; ++cc) st_dsmem(mapa_u32(v_local, cc), s);
-            } else {
-                // locate the item holding entry e, write v in the global layout
-                int acc_e = 0;
-                for (int ii = 0; ii < U.n_items; ++ii) {
-                    const DevItem it = p.items[U.item_begin + ii];
-                    const DevSeg sg = p.segs[it.seg];
-                    const int div = p.a_div[p.proj_ids[it.pi]];
-                    const int n_e = it.nt * (sg.rank / div);
-                    if (e < acc_e + n_e) {
-                        const int64_t base = int64_t(it.pi) * (p.NR / div) +
-                                             (sg.vrow_off + int64_t(it.t0) * sg.rank) / div;
-                        p.v_out[base + (e - acc_e)] = s;
-                        break;
+                for (int base = 0; base < M.RB; base += kRowsPerSlot) {
+                    mbar_wait(&full[slot], lap & 1);
+                    if (cv < cvs) {
+                        const int nr = min(kRowsPerSlot, M.RB - base);
+                        for (int q = 0; q < nr; ++q) {
+                            const int row = base + q;
+                            const ItemMeta& it = M.it[M.rowB_item[row]];
+                            const int j = row - it.rowB;
+                            // does this thread own a token of the item?
+                            bool any = false;
+#pragma unroll
+                            for (int t = 0; t < kTokCap; ++t)
+                                any |= (t % ntg == tg) && t >= it.ts && t < it.ts + it.nt;
+                            if (!any) continue;
+                            float b[VE];
+                            V::to_f32(reinterpret_cast<const uint4*>(ring + (size_t(slot) * kRowsPerSlot + q) * rowb)[cv], b);
+#pragma unroll
+                            for (int t = 0; t < kTokCap; ++t) {
+                                if ((t % ntg == tg) && t >= it.ts && t < it.ts + it.nt) {
+                                    const float vj = vfull[it.vf_off + (t - it.ts) * it.r + j];
+#pragma unroll
+                                    for (int e = 0; e < VE; ++e) acc[t][e] = fmaf(vj, b[e], acc[t][e]);
+                                }
+                            }
+                        }
                     }
-                    acc_e += n_e;
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&empty[slot]);
+                    if (++slot == ns) { slot = 0; ++lap; }
+                }
+#pragma unroll
+                for (int t = 0; t < kTokCap; ++t) {
+                    if (t % ntg == tg && t < M.toks && cv < cvs) {
+                        const ItemMeta& it = M.it[M.tok_item[t]];
+                        T* y = reinterpret_cast<T*>(p.y[it.proj]);
+                        float yf[VE];
+                        V::to_f32(yv[t], yf);
+#pragma unroll
+                        for (int e = 0; e < VE; ++e) yf[e] = yf[e] + it.scale * acc[t][e];
+                        *reinterpret_cast<uint4*>(y + int64_t(M.tok[t]) * p.ldy[it.proj] + c * DS + int64_t(cv) * VE) =
+                            V::from_f32(yf);
+                    }
                 }
             }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&xempty[ub]);
         }
-        cluster_sync_all();  // all remote reads/writes done (also: safe exit)
     }
+    if (MODE != kExpand) cluster_sync_all();  // no CTA leaves while peers may touch its smem
+}
 
-    if (MODE == kShrink) return;
-
-    if (MODE == kExpand) {
-        // v from global, block layout of slora_lora_expand
-        const int vb = p.v_blocks;
-        const int64_t stride = int64_t(p.nproj) * (p.NR / vb);
-        for (int ii = 0; ii < U.n_items; ++ii) {
-            const DevItem it = p.items[U.item_begin + ii];
-            const DevSeg sg = p.segs[it.seg];
-            const int r = sg.rank, rb = r / vb;
-            const int n = it.nt * r;
-            const int64_t base = int64_t(it.pi) * (p.NR / vb) + (sg.vrow_off + int64_t(it.t0) * r) / vb;
-            for (int e = tid; e < n; e += kThreads) {
-                const int t = e / r, j = e % r;
-                sV[it.v_off + e] = p.v_in[int64_t(j / rb) * stride + base + int64_t(t) * rb + (j % rb)];
-            }
-        }
-        __syncthreads();
-    }
-
-    // ---------------- expand: y += scale * v B over this CTA's D slice ----
-    mbar_wait(&bar[1], 0);
-    const int ncv = DS / VE;
-    int task0 = 0;
-    for (int ii = 0; ii < U.n_items; ++ii) {
-        const DevItem it = p.items[U.item_begin + ii];
-        const DevSeg sg = p.segs[it.seg];
-        const int r = sg.rank;
-        const int ntask = it.nt * ncv;
-        const int proj = p.proj_ids[it.pi];
-        T* y = reinterpret_cast<T*>(p.y[proj]);
-        // threads continue numbering across items so all stay busy
-        int first = (tid - task0) % kThreads;
-        if (first < 0) first += kThreads;
-        for (int task = first; task < ntask; task += kThreads) {
-            const int t = task / ncv, cv = task % ncv;
-            float acc[VE];
-#pragma unroll
-            for (int e = 0; e < VE; ++e) acc[e] = 0.f;
-            const float* vrow = sV + it.v_off + t * r;
-            for (int j = 0; j < r; ++j) {
-                float b[VE];
-                V::to_f32(reinterpret_cast<const uint4*>(sB + size_t(it.row_off + j) * DS)[cv], b);
-                const float vj = vrow[j];
-#pragma unroll
-                for (int e = 0; e < VE; ++e) acc[e] = fmaf(vj, b[e], acc[e]);
-            }
-            const int32_t tok = p.tok_idx[sg.tok_off + it.t0 + t];
-            uint4* yp = reinterpret_cast<uint4*>(y + tok * p.ldy[proj] + int64_t(c) * DS) + cv;
-            float yv[VE];
-            V::to_f32(*yp, yv);
-#pragma unroll
-            for (int e = 0; e < VE; ++e) yv[e] = yv[e] + sg.scale * acc[e];
-            *yp = V::from_f32(yv);
-        }
-        task0 = (task0 + ntask) % kThreads;
+template <typename T, int MODE>
+static void* kernel_ptr() {
+    return reinterpret_cast<void*>(&mbgmv_kernel<T, MODE>);
+}
+static void* kernel_for(int mode, int dtype) {
+    switch (dtype * 3 + mode) {
+        case 0: return kernel_ptr<float, kFused>();
+        case 1: return kernel_ptr<float, kShrink>();
+        case 2: return kernel_ptr<float, kExpand>();
+        case 3: return kernel_ptr<__half, kFused>();
+        case 4: return kernel_ptr<__half, kShrink>();
+        case 5: return kernel_ptr<__half, kExpand>();
+        case 6: return kernel_ptr<__nv_bfloat16, kFused>();
+        case 7: return kernel_ptr<__nv_bfloat16, kShrink>();
+        default: return kernel_ptr<__nv_bfloat16, kExpand>();
     }
 }
 
-size_t lora_smem_bytes(const LoraParams& p, int mode, int esize) { return smem_layout(p, mode, esize).total; }
-
 template <typename T, int MODE>
 static cudaError_t launch_t(const LoraParams& p, cudaStream_t s, size_t smem) {
-    auto kern = lora_unit_kernel<T, MODE>;
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(unsigned(p.n_units) * unsigned(p.C));
+    cfg.gridDim = dim3(unsigned(p.n_clusters) * unsigned(p.C));
     cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
@@ -375,7 +609,7 @@ static cudaError_t launch_t(const LoraParams& p, cudaStream_t s, size_t smem) {
     cfg.attrs = attr;
     cfg.numAttrs = na;
     count_launch();
-    return cudaLaunchKernelEx(&cfg, kern, p);
+    return cudaLaunchKernelEx(&cfg, mbgmv_kernel<T, MODE>, p);
 }
 
 template <typename T>
@@ -388,7 +622,7 @@ static cudaError_t launch_mode(const LoraParams& p, int mode, cudaStream_t s, si
 }
 
 cudaError_t launch_lora(const LoraParams& p, int mode, int dtype, cudaStream_t s, size_t smem) {
-    if (p.n_units == 0) return cudaSuccess;
+    if (p.n_clusters == 0) return cudaSuccess;
     switch (dtype) {
         case kF32: return launch_mode<float>(p, mode, s, smem);
         case kF16: return launch_mode<__half>(p, mode, s, smem);
@@ -396,27 +630,45 @@ cudaError_t launch_lora(const LoraParams& p, int mode, int dtype, cudaStream_t s
     }
 }
 
-template <typename T>
-static cudaError_t configure_t() {
-    const int max_smem = 227 * 1024;
-    cudaError_t e;
-    e = cudaFuncSetAttribute(lora_unit_kernel<T, kFused>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem);
-    if (e) return e;
-    e = cudaFuncSetAttribute(lora_unit_kernel<T, kShrink>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem);
-    if (e) return e;
-    e = cudaFuncSetAttribute(lora_unit_kernel<T, kExpand>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem);
-    if (e) return e;
-    e = cudaFuncSetAttribute(lora_unit_kernel<T, kFused>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-    if (e) return e;
-    return cudaFuncSetAttribute(lora_unit_kernel<T, kShrink>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+int lora_max_clusters(int mode, int dtype, int C, size_t smem) {
+    void* k = kernel_for(mode, dtype);
+    if (mode == kExpand) {
+        int blocks = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks, k, kThreads, smem) != cudaSuccess) return 0;
+        int dev = 0, sms = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        return blocks * sms / C;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(unsigned(C));
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = unsigned(C);
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, k, &cfg) != cudaSuccess) return 0;
+    return n;
 }
 
 cudaError_t configure_lora_kernels(int /*device*/) {
-    cudaError_t e = configure_t<float>();
-    if (e) return e;
-    e = configure_t<__half>();
-    if (e) return e;
-    return configure_t<__nv_bfloat16>();
+    const int max_smem = 227 * 1024;
+    for (int dt = 0; dt < 3; ++dt)
+        for (int m = 0; m < 3; ++m) {
+            void* k = kernel_for(m, dt);
+            cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem);
+            if (e) return e;
+            if (m != kExpand) {
+                e = cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+                if (e) return e;
+            }
+        }
+    return cudaSuccess;
 }
 
 // ------------------------------------------------------------- adapter load

@@ -22,29 +22,35 @@ struct DevSeg {
 static_assert(sizeof(DevSeg) == 32, "DevSeg layout");
 
 // A work item = (segment, projection index within the call's mask, token
-// chunk).  Items are packed into units of balanced size; one cluster of C
-// CTAs processes one unit, CTA c owning the c-th 1/C slice of the K (shrink)
-// and D (expand) dimensions.
+// chunk).  Items are packed into units (<= kRowCap A/B rows, <= kTokCap token
+// slots, <= kVCap v entries); a cluster of C CTAs processes a unit, CTA c
+// owning the c-th 1/C slice of K (shrink) and of D (expand).
 struct DevItem {
     int32_t seg;
     int32_t pi;        // index of the projection in the call's mask order
     int32_t t0, nt;    // token chunk [t0, t0+nt) of the segment
-    int32_t row_off;   // first smem row of this item (full-rank units)
-    int32_t tok_slot;  // first x row slot in smem
-    int32_t v_off;     // first v entry (full-rank units) within the unit
+    int32_t row_off;   // first row of this item within the unit (full rank units)
+    int32_t tok_slot;  // first token slot within the unit
+    int32_t v_off;     // first v entry within the unit (full rank units)
     int32_t pad;
 };
 static_assert(sizeof(DevItem) == 32, "DevItem layout");
 
 struct DevUnit {
     int32_t item_begin, n_items;
-    int32_t rows, toks, ventries;  // totals (full-rank units)
+    int32_t rows, toks, ventries;  // totals (full rank units)
     int32_t pad[3];
 };
 static_assert(sizeof(DevUnit) == 32, "DevUnit layout");
 
 constexpr int kMaxItemsPerUnit = 16;
-constexpr int kThreads = 256;
+constexpr int kRowCap = 64;      // rows (sum of ranks) per unit; max rank 64 on this path
+constexpr int kTokCap = 8;       // token slots per unit
+constexpr int kVCap = 512;       // v entries per unit
+constexpr int kConsumerWarps = 8;
+constexpr int kThreads = (kConsumerWarps + 1) * 32;  // + 1 producer warp
+constexpr int kRowsPerSlot = 8;  // page-slice rows per ring slot
+constexpr int kMaxSlots = 16;
 
 enum Mode : int { kFused = 0, kShrink = 1, kExpand = 2 };
 enum DType : int { kF32 = 0, kF16 = 1, kBF16 = 2 };
@@ -57,15 +63,17 @@ struct LoraParams {
     const int32_t* tok_idx;
     const DevUnit* units;
     const DevItem* items;
-    int32_t n_units;
+    const int32_t* sched_off;     // [n_clusters + 1] per-cluster unit lists (LPT)
+    const int32_t* sched;
+    int32_t n_clusters;
     int32_t nproj;
     int32_t proj_ids[4];
     int32_t layer;
-    int32_t C;                    // K/D split (cluster size for fused/shrink)
+    int32_t C;                    // K/D split = cluster size (fused / shrink)
     int32_t K, D;                 // A-row length, B-row length (elements)
     int32_t a_div[4];             // A rank columns stored = r / a_div[p]
     int32_t a_row_pages[4];       // pages per stored A row
-    int32_t rcap, tcap, vcap;     // smem capacities (rows, x rows, v entries)
+    int32_t ns;                   // ring slots
     const void* x;
     int64_t ldx;
     void* y[4];
@@ -76,9 +84,21 @@ struct LoraParams {
     int64_t NR;                   // sum over adapted tokens of rank
 };
 
-// launchers (kernels.cu); return cudaError_t of the launch
+// Per-launch kernel configuration (chosen on the host, see api.cpp).
+struct KernelCfg {
+    int mode = 0;
+    int C = 0, ns = 0;
+    int64_t K = 0, D = 0;
+    size_t smem = 0;
+    int n_clusters = 0;           // persistent clusters (grid = n_clusters * C)
+    bool ok = false;
+};
+
+// smem bytes for a launch (host and device agree via smem_layout in kernels.cu)
+size_t lora_smem_bytes(int mode, int C, int64_t K, int64_t D, int ns, int esize);
+// number of persistent clusters that can be co-resident (occupancy API)
+int lora_max_clusters(int mode, int dtype, int C, size_t smem);
 cudaError_t launch_lora(const LoraParams& p, int mode, int dtype, cudaStream_t s, size_t smem);
-size_t lora_smem_bytes(const LoraParams& p, int mode, int esize);
 cudaError_t configure_lora_kernels(int device);
 
 // Adapter scatter: jobs describe how rows of a packed staging buffer land in
