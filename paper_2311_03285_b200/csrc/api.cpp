@@ -114,7 +114,7 @@ int esize_of(slora_dtype d) { return d == SLORA_F32 ? 4 : 2; }
 // streams the largest slices and the most SMs stay usable (small clusters
 // pack GPCs best).  SLORA_SPLIT overrides.  ns = ring slots filling smem.
 KernelCfg make_kernel_cfg(int mode, int64_t K, int64_t D, int64_t P, int es, int dtype) {
-    (void)P;
+
     KernelCfg k;
     k.mode = mode;
     k.K = K;
@@ -124,9 +124,13 @@ KernelCfg make_kernel_cfg(int mode, int64_t K, int64_t D, int64_t P, int es, int
         return s ? atoi(s) : 0;
     }();
     auto valid = [&](int C) {
-        if (mode != kExpand && (K % C || ((K / C) * es) % 16 || (K / C) * es > 8192)) return false;
+        if (mode != kExpand && (K % C || ((K / C) * es) % 16 || (K / C) * es > 4096)) return false;
+        if (mode != kExpand)
+            for (int c = 0; c < C; ++c) {  // pages one CTA's K slice spans
+                const int64_t k0 = c * (K / C), k1 = k0 + K / C - 1;
+                if (k1 / P - k0 / P + 1 > kMaxChunks) return false;
+            }
         if (mode != kShrink && (D % C || ((D / C) * es) % 16 || (D / C) * es > 4096)) return false;
-        if (mode == kFused && (K / C) * es > 4096) return false;
         return true;
     };
     int C = 0;

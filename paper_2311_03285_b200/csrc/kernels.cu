@@ -193,6 +193,8 @@ struct UnitMeta {
     int32_t tok[kTokCap];        // token row of each slot
     int32_t tok_item[kTokCap];   // item of each slot
     ItemMeta it[kMaxItemsPerUnit];
+    int32_t pa[kRowCap][kMaxChunks];  // pages of this CTA's K slice of each A row
+    int32_t pb[kRowCap];              // page of each B row
     uint8_t rowA_item[kRowCap];
     uint8_t rowB_item[kRowCap];
 };
@@ -210,7 +212,7 @@ __host__ __device__ inline SmemLayout smem_layout(int mode, int C, int64_t K, in
     L.row_bytes = (rb + 15) & ~size_t(15);
     size_t off = 0;
     L.bars = off;
-    off = al128(off + sizeof(uint64_t) * (2 * kMaxSlots + 6));
+    off = al128(off + sizeof(uint64_t) * (2 * kMaxSlots + 8));
     L.meta = off;
     off = al128(off + 2 * sizeof(UnitMeta));
     L.xbuf = off;
@@ -246,6 +248,7 @@ __global__ void __launch_bounds__(kThreads, 1) mbgmv_kernel(const __grid_constan
     uint64_t* xfull = empty + kMaxSlots;
     uint64_t* xempty = xfull + 2;
     uint64_t* exch = xempty + 2;
+    uint64_t* mfull = exch + 2;
     UnitMeta* meta = reinterpret_cast<UnitMeta*>(smem + L.meta);
     float* xbuf = reinterpret_cast<float*>(smem + L.xbuf);  // [2][C][kVCap]
     float* vfull = reinterpret_cast<float*>(smem + L.vfull);
@@ -263,6 +266,7 @@ __global__ void __launch_bounds__(kThreads, 1) mbgmv_kernel(const __grid_constan
             mbar_init(&xfull[b], 1);
             mbar_init(&xempty[b], kConsumerWarps);
             mbar_init(&exch[b], C);
+            mbar_init(&mfull[b], 1);
         }
         fence_mbar_init();
     }
@@ -273,16 +277,16 @@ __global__ void __launch_bounds__(kThreads, 1) mbgmv_kernel(const __grid_constan
     const T* pool = reinterpret_cast<const T*>(p.pool);
     const int64_t P = p.page_elems;
 
-    if (warp == kConsumerWarps) {
-        // ============================ producer ============================
-        int slot = 0;
-        uint32_t lap = 0;
+    if (warp == kConsumerWarps + 1) {
+        // ============================ resolver ============================
+        // Resolves unit i (items -> segments -> adapter page tables -> the
+        // page ids of every row slice this CTA will stream) one unit ahead of
+        // the streamer, so the streaming loop issues copies from smem only.
         for (int i = 0; u_beg + i < u_end; ++i) {
             const int ub = i & 1;
             if (i >= 2) mbar_wait(&xempty[ub], ((i >> 1) - 1) & 1);
             UnitMeta& M = meta[ub];
             const DevUnit U = p.units[p.sched[u_beg + i]];
-            // ---- resolve items (one lane per item)
             int ra = 0, rr = 0, ve = 0, vf = 0;
             ItemMeta im{};
             if (lane < U.n_items) {
@@ -311,7 +315,7 @@ __global__ void __launch_bounds__(kThreads, 1) mbgmv_kernel(const __grid_constan
                     M.tok_item[it.tok_slot + t] = lane;
                 }
             }
-            // exclusive prefix sums over items -> row offsets
+            // inclusive prefix sums over items -> row offsets
             int pa = ra, pb = rr;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
@@ -343,11 +347,39 @@ __global__ void __launch_bounds__(kThreads, 1) mbgmv_kernel(const __grid_constan
                 M.EF = tot_vf;
             }
             __syncwarp();
-            // ---- x rows of the unit (meta is published by the same arrive)
+            // page ids of every row slice (independent loads, one per lane)
             if (MODE != kExpand) {
-                if (lane == 0) mbar_arrive_expect_tx(&xfull[ub], uint32_t(U.toks * KS * ES));
+                for (int q = lane; q < RA; q += 32) {
+                    const ItemMeta& it = M.it[M.rowA_item[q]];
+                    const int j = q - it.rowA;
+                    const int64_t k0 = int64_t(c) * KS;
+                    const int ch0 = int(k0 / P), ch1 = int((k0 + KS - 1) / P);
+                    for (int ch = ch0; ch <= ch1; ++ch) M.pa[q][ch - ch0] = it.tab[j * it.arp + ch];
+                }
+            }
+            if (MODE != kShrink) {
+                for (int q = lane; q < RB; q += 32) {
+                    const ItemMeta& it = M.it[M.rowB_item[q]];
+                    M.pb[q] = it.tab[it.r + (q - it.rowB)];
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&mfull[ub]);
+        }
+    } else if (warp == kConsumerWarps) {
+        // ============================ streamer ============================
+        int slot = 0;
+        uint32_t lap = 0;
+        for (int i = 0; u_beg + i < u_end; ++i) {
+            const int ub = i & 1;
+            mbar_wait(&mfull[ub], (i >> 1) & 1);
+            const UnitMeta& M = meta[ub];
+            const int RA = M.RA, RB = M.RB, toks = M.toks;
+            // ---- x rows of the unit (the same arrive publishes the meta)
+            if (MODE != kExpand) {
+                if (lane == 0) mbar_arrive_expect_tx(&xfull[ub], uint32_t(toks * KS * ES));
                 __syncwarp();
-                if (lane < U.toks) {
+                if (lane < toks) {
                     const T* x = reinterpret_cast<const T*>(p.x);
                     bulk_g2s(xrows + (size_t(ub) * kTokCap + lane) * KS, x + int64_t(M.tok[lane]) * p.ldx + c * KS,
                              uint32_t(KS * ES), &xfull[ub]);
@@ -360,35 +392,28 @@ __global__ void __launch_bounds__(kThreads, 1) mbgmv_kernel(const __grid_constan
                 if (phase == 0 && MODE == kExpand) continue;
                 if (phase == 1 && MODE == kShrink) continue;
                 const int R = phase == 0 ? RA : RB;
+                const uint32_t row_bytes = uint32_t((phase == 0 ? KS : DS) * ES);
                 for (int base = 0; base < R; base += kRowsPerSlot) {
+                    const int nrow = min(kRowsPerSlot, R - base);
                     mbar_wait(&empty[slot], (lap & 1) ^ 1);
-                    const int row = base + lane;
-                    uint32_t bytes = 0;
-                    if (lane < kRowsPerSlot && row < R) bytes = uint32_t((phase == 0 ? KS : DS) * ES);
-                    uint32_t tot = bytes;
-#pragma unroll
-                    for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
-                    if (lane == 0) mbar_arrive_expect_tx(&full[slot], tot);
+                    if (lane == 0) mbar_arrive_expect_tx(&full[slot], uint32_t(nrow) * row_bytes);
                     __syncwarp();
-                    if (bytes) {
+                    if (lane < nrow) {
+                        const int row = base + lane;
                         unsigned char* dst = ring + (size_t(slot) * kRowsPerSlot + lane) * rowb;
                         if (phase == 0) {
-                            const ItemMeta& it = M.it[M.rowA_item[row]];
-                            const int j = row - it.rowA;
                             int64_t k = int64_t(c) * KS;
                             const int64_t kend = k + KS;
+                            int ch = 0;
                             while (k < kend) {  // a slice may span pages (TP q/k/v rows)
-                                const int32_t page = it.tab[j * it.arp + int(k / P)];
+                                const int32_t page = M.pa[row][ch++];
                                 const int64_t len = min(P - k % P, kend - k);
                                 bulk_g2s(dst, pool + int64_t(page) * P + k % P, uint32_t(len * ES), &full[slot]);
                                 dst += len * ES;
                                 k += len;
                             }
                         } else {
-                            const ItemMeta& it = M.it[M.rowB_item[row]];
-                            const int j = row - it.rowB;
-                            const int32_t page = it.tab[it.r + j];
-                            bulk_g2s(dst, pool + int64_t(page) * P + int64_t(c) * DS, uint32_t(DS * ES), &full[slot]);
+                            bulk_g2s(dst, pool + int64_t(M.pb[row]) * P + int64_t(c) * DS, row_bytes, &full[slot]);
                         }
                     }
                     if (++slot == ns) { slot = 0; ++lap; }
@@ -508,13 +533,17 @@ __global__ void __launch_bounds__(kThreads, 1) mbgmv_kernel(const __grid_constan
             }
             if (MODE != kShrink) {
                 // ------------------------------ expand ------------------------------
+                // token slots owned by this thread: t % ntg == tg (bit mask)
+                uint32_t own = 0;
+                if (cv < cvs)
+                    for (int t = tg; t < M.toks; t += ntg) own |= 1u << t;
                 uint4 yv[kTokCap];
                 float acc[kTokCap][VE];
 #pragma unroll
                 for (int t = 0; t < kTokCap; ++t) {
 #pragma unroll
                     for (int e = 0; e < VE; ++e) acc[t][e] = 0.f;
-                    if (t % ntg == tg && t < M.toks && cv < cvs) {
+                    if (own >> t & 1u) {
                         const ItemMeta& it = M.it[M.tok_item[t]];
                         const T* y = reinterpret_cast<const T*>(p.y[it.proj]);
                         yv[t] = *reinterpret_cast<const uint4*>(y + int64_t(M.tok[t]) * p.ldy[it.proj] + c * DS +
@@ -523,24 +552,21 @@ __global__ void __launch_bounds__(kThreads, 1) mbgmv_kernel(const __grid_constan
                 }
                 for (int base = 0; base < M.RB; base += kRowsPerSlot) {
                     mbar_wait(&full[slot], lap & 1);
-                    if (cv < cvs) {
+                    if (own) {
                         const int nr = min(kRowsPerSlot, M.RB - base);
                         for (int q = 0; q < nr; ++q) {
                             const int row = base + q;
                             const ItemMeta& it = M.it[M.rowB_item[row]];
+                            const uint32_t m = own & (((1u << it.nt) - 1u) << it.ts);
+                            if (!m) continue;
                             const int j = row - it.rowB;
-                            // does this thread own a token of the item?
-                            bool any = false;
-#pragma unroll
-                            for (int t = 0; t < kTokCap; ++t)
-                                any |= (t % ntg == tg) && t >= it.ts && t < it.ts + it.nt;
-                            if (!any) continue;
                             float b[VE];
                             V::to_f32(reinterpret_cast<const uint4*>(ring + (size_t(slot) * kRowsPerSlot + q) * rowb)[cv], b);
+                            const float* vcol = vfull + it.vf_off + j - it.ts * it.r;
 #pragma unroll
                             for (int t = 0; t < kTokCap; ++t) {
-                                if ((t % ntg == tg) && t >= it.ts && t < it.ts + it.nt) {
-                                    const float vj = vfull[it.vf_off + (t - it.ts) * it.r + j];
+                                if (m >> t & 1u) {
+                                    const float vj = vcol[t * it.r];
 #pragma unroll
                                     for (int e = 0; e < VE; ++e) acc[t][e] = fmaf(vj, b[e], acc[t][e]);
                                 }
@@ -553,7 +579,7 @@ __global__ void __launch_bounds__(kThreads, 1) mbgmv_kernel(const __grid_constan
                 }
 #pragma unroll
                 for (int t = 0; t < kTokCap; ++t) {
-                    if (t % ntg == tg && t < M.toks && cv < cvs) {
+                    if (own >> t & 1u) {
                         const ItemMeta& it = M.it[M.tok_item[t]];
                         T* y = reinterpret_cast<T*>(p.y[it.proj]);
                         float yf[VE];

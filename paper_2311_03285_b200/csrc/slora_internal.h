@@ -48,7 +48,8 @@ constexpr int kRowCap = 64;      // rows (sum of ranks) per unit; max rank 64 on
 constexpr int kTokCap = 8;       // token slots per unit
 constexpr int kVCap = 512;       // v entries per unit
 constexpr int kConsumerWarps = 8;
-constexpr int kThreads = (kConsumerWarps + 1) * 32;  // + 1 producer warp
+constexpr int kThreads = (kConsumerWarps + 2) * 32;  // + streamer warp + resolver warp
+constexpr int kMaxChunks = 4;    // pages one CTA's K slice of an A row may span
 constexpr int kRowsPerSlot = 8;  // page-slice rows per ring slot
 constexpr int kMaxSlots = 16;
 
