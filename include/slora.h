@@ -221,6 +221,12 @@ slora_status slora_lora_expand(slora_pool_t pool, slora_batch_t batch, int32_t l
 /* Wait for `stream` and surface any deferred CUDA error. */
 slora_status slora_sync(slora_pool_t pool, void* stream);
 
+/* Debug: when the environment variable SLORA_TRACE=1 is set at pool creation,
+ * the next kernel launches record per-CTA event timestamps (ns, %globaltimer)
+ * for CTAs 0..15, 64 slots each.  Copies min(n, 1024) values to out_host
+ * (synchronizes the device); INVALID_ARG when tracing is off. */
+slora_status slora_debug_trace(slora_pool_t pool, int64_t* out_host, int32_t n);
+
 /* Number of this library's kernel launches so far (for bench accounting). */
 int64_t slora_launch_count(void);
 

@@ -176,6 +176,7 @@ struct slora_pool {
     // kernel configurations: 0 fused (K=D=H), 1 shrink q/k/v (K=H),
     // 2 shrink o (K=H/N), 3 expand (D=H/N)
     KernelCfg kcfg[4];
+    long long* trace_dev = nullptr;   // SLORA_TRACE=1: kernel event timestamps
 
     int64_t free_pages() const { return int64_t(free_stack.size()); }
     int N() const { return cfg.tp_size; }
@@ -288,6 +289,11 @@ extern "C" slora_status slora_pool_create(const slora_pool_config* cfg, slora_po
         p->kcfg[1] = make_kernel_cfg(kShrink, H, P, P, es, dt);
         p->kcfg[2] = make_kernel_cfg(kShrink, cfg->tp_size > 1 ? P : H, P, P, es, dt);
         p->kcfg[3] = make_kernel_cfg(kExpand, P, P, P, es, dt);
+        const char* tr = getenv("SLORA_TRACE");
+        if (tr && atoi(tr) == 1) {
+            if ((e = cudaMalloc(&p->trace_dev, 1024 * sizeof(long long)))) return cleanup(e, "cudaMalloc trace");
+            cudaMemset(p->trace_dev, 0, 1024 * sizeof(long long));
+        }
         if (cfg->tp_size == 1 && !p->kcfg[0].ok) {
             slora_status s = fail(SLORA_ERR_SHAPE, "no valid MBGMV split for hidden %lld", (long long)H);
             delete p;
@@ -934,6 +940,7 @@ slora_status launch(slora_pool* p, int kc, LoraParams& q, void* stream) {
                            (long long)k.D);
     CUDA_TRY(cudaSetDevice(p->cfg.device));
     const int dt = p->cfg.dtype == SLORA_F32 ? kF32 : (p->cfg.dtype == SLORA_F16 ? kF16 : kBF16);
+    q.trace = p->trace_dev;
     CUDA_TRY(launch_lora(q, k.mode, dt, static_cast<cudaStream_t>(stream), k.smem));
     return ok();
 }
@@ -1025,5 +1032,14 @@ extern "C" slora_status slora_sync(slora_pool_t p, void* stream) {
     CUDA_TRY(cudaSetDevice(p->cfg.device));
     CUDA_TRY(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
     CUDA_TRY(cudaGetLastError());
+    return ok();
+}
+
+extern "C" slora_status slora_debug_trace(slora_pool_t p, int64_t* out, int32_t n) {
+    if (check_pool(p) || !out || n < 0) return fail(SLORA_ERR_INVALID_ARG, "null argument");
+    if (!p->trace_dev) return fail(SLORA_ERR_INVALID_ARG, "tracing is off (set SLORA_TRACE=1 before pool create)");
+    CUDA_TRY(cudaSetDevice(p->cfg.device));
+    CUDA_TRY(cudaDeviceSynchronize());
+    CUDA_TRY(cudaMemcpy(out, p->trace_dev, sizeof(int64_t) * size_t(std::min(n, 1024)), cudaMemcpyDeviceToHost));
     return ok();
 }

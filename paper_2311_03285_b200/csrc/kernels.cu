@@ -41,6 +41,7 @@
 
 #include <atomic>
 #include <cstdint>
+#include <cstdlib>
 
 #include "slora_internal.h"
 
@@ -124,6 +125,16 @@ __device__ __forceinline__ uint4 ld_global_nc(const void* p) {
                  : "l"(p));
     return r;
 }
+
+__device__ __forceinline__ long long gtimer() {
+    long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define TRACE(ev)                                                                       \
+    do {                                                                                \
+        if (p.trace && blockIdx.x < 16 && (ev) < 64) p.trace[blockIdx.x * 64 + (ev)] = gtimer(); \
+    } while (0)
 
 // ---------------------------------------------------- element conversions
 template <typename T> struct Vec;
@@ -230,6 +241,151 @@ size_t lora_smem_bytes(int mode, int C, int64_t K, int64_t D, int ns, int esize)
     return smem_layout(mode, C, K, D, ns, esize).total;
 }
 
+// ------------------------------------------------------ v4 building blocks
+// Mixed-precision FMA: f16/bf16 x f16/bf16 + f32 -> f32 in ONE instruction
+// (SASS FHFMA, with .H1 operand selects for the upper halves): the product
+// of two 16-bit floats is exact in fp32, so this equals convert + fmaf.
+__device__ __forceinline__ float fma16(uint32_t a, uint32_t b, float c, __half*) {
+    asm("fma.rn.f32.f16 %0, %1, %2, %0;" : "+f"(c) : "h"((unsigned short)a), "h"((unsigned short)b));
+    return c;
+}
+__device__ __forceinline__ float fma16(uint32_t a, uint32_t b, float c, __nv_bfloat16*) {
+    asm("fma.rn.f32.bf16 %0, %1, %2, %0;" : "+f"(c) : "h"((unsigned short)a), "h"((unsigned short)b));
+    return c;
+}
+// acc0/acc1 += <a, x> over one 16-byte vector (two interleaved chains)
+template <typename T>
+__device__ __forceinline__ void dot16(const uint4& a, const uint4& x, float& acc0, float& acc1) {
+    const uint32_t aw[4] = {a.x, a.y, a.z, a.w}, xw[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        acc0 = fma16(aw[i] & 0xffffu, xw[i] & 0xffffu, acc0, (T*)nullptr);
+        acc1 = fma16(aw[i] >> 16, xw[i] >> 16, acc1, (T*)nullptr);
+    }
+}
+template <>
+__device__ __forceinline__ void dot16<float>(const uint4& a, const uint4& x, float& acc0, float& acc1) {
+    acc0 = fmaf(__uint_as_float(a.x), __uint_as_float(x.x), acc0);
+    acc1 = fmaf(__uint_as_float(a.y), __uint_as_float(x.y), acc1);
+    acc0 = fmaf(__uint_as_float(a.z), __uint_as_float(x.z), acc0);
+    acc1 = fmaf(__uint_as_float(a.w), __uint_as_float(x.w), acc1);
+}
+
+// async remote store: value into CTA `rank`'s smem at the address of `local`,
+// completing 4 bytes of transaction count on that CTA's barrier `bar`.
+__device__ __forceinline__ void st_async_f32(const float* local, const uint64_t* bar, uint32_t rank, float v) {
+    uint32_t a, b;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(a) : "r"(smem_u32(local)), "r"(rank));
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(b) : "r"(smem_u32(bar)), "r"(rank));
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];" ::"r"(a),
+                 "r"(__float_as_uint(v)), "r"(b)
+                 : "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+struct Ring {
+    int slot = 0;
+    uint32_t lap = 0;
+    __device__ __forceinline__ void advance(int ns) {
+        if (++slot == ns) { slot = 0; ++lap; }
+    }
+};
+
+// Shrink of one stored A row slice for NT tokens: v_t = <A_j, x_t> over the
+// CTA's K slice; partials pushed to slot [c] of every cluster CTA.
+template <typename T, int NT>
+__device__ __forceinline__ void shrink_row(const uint4* arow, const T* xr, int64_t KS, int nvec, const ItemMeta& it,
+                                           int j, float* xb, uint64_t* xbar, int C, int c, int lane) {
+    float a0[NT], a1[NT];
+#pragma unroll
+    for (int t = 0; t < NT; ++t) a0[t] = a1[t] = 0.f;
+    const uint4* xv = reinterpret_cast<const uint4*>(xr + size_t(it.ts) * KS);
+    const int xstride = int(KS * sizeof(T) / 16);
+    for (int q = lane; q < nvec; q += 32) {
+        const uint4 a = arow[q];
+#pragma unroll
+        for (int t = 0; t < NT; ++t) dot16<T>(a, xv[t * xstride + q], a0[t], a1[t]);
+    }
+    float out[NT];
+#pragma unroll
+    for (int t = 0; t < NT; ++t) {
+        float s = a0[t] + a1[t];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        out[t] = s;
+    }
+    for (int w = lane; w < NT * C; w += 32) {
+        const int t = w / C, cc = w % C;
+        float s = 0.f;
+#pragma unroll
+        for (int tt = 0; tt < NT; ++tt)
+            if (tt == t) s = out[tt];
+        st_async_f32(xb + size_t(c) * kVCap + it.v_off + t * it.ra + j, xbar, uint32_t(cc), s);
+    }
+}
+
+// Expand of one item (all its B rows) for NT tokens: y_t += scale * v_t B over
+// this thread's 16-byte column vector; walks ring slots at 8-row boundaries.
+template <typename T, int NT>
+__device__ __forceinline__ void expand_item(const LoraParams& p, const UnitMeta& M, const ItemMeta& it,
+                                            const unsigned char* ring, size_t rowb, uint64_t* full, uint64_t* empty,
+                                            Ring& rg, int ns, int& row, const float* vfull, bool active, int cv,
+                                            int64_t cDS, int lane) {
+    using V = Vec<T>;
+    constexpr int VE = V::VE;
+    float acc[NT][VE];
+#pragma unroll
+    for (int t = 0; t < NT; ++t)
+#pragma unroll
+        for (int e = 0; e < VE; ++e) acc[t][e] = 0.f;
+    T* y = reinterpret_cast<T*>(p.y[it.proj]);
+    const int64_t ldy = p.ldy[it.proj];
+    // y is prefetched into registers for small token counts (hidden behind the
+    // row loop); larger items load it after the loop to stay within registers
+    constexpr bool kPrefetchY = NT <= 4;
+    uint4 yv[kPrefetchY ? NT : 1];
+    if (kPrefetchY && active) {
+#pragma unroll
+        for (int t = 0; t < NT; ++t)
+            yv[kPrefetchY ? t : 0] =
+                *reinterpret_cast<const uint4*>(y + int64_t(M.tok[it.ts + t]) * ldy + cDS + int64_t(cv) * VE);
+    }
+    for (int j = 0; j < it.r; ++j, ++row) {
+        if ((row & (kRowsPerSlot - 1)) == 0) {
+            if (row > 0) {
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[rg.slot]);
+                rg.advance(ns);
+            }
+            mbar_wait(&full[rg.slot], rg.lap & 1);
+        }
+        if (active) {
+            float b[VE];
+            V::to_f32(reinterpret_cast<const uint4*>(ring + (size_t(rg.slot) * kRowsPerSlot +
+                                                            (row & (kRowsPerSlot - 1))) * rowb)[cv], b);
+            const float* vc = vfull + it.vf_off + j;
+#pragma unroll
+            for (int t = 0; t < NT; ++t) {
+                const float vj = vc[t * it.r];
+#pragma unroll
+                for (int e = 0; e < VE; ++e) acc[t][e] = fmaf(vj, b[e], acc[t][e]);
+            }
+        }
+    }
+    if (active) {
+#pragma unroll
+        for (int t = 0; t < NT; ++t) {
+            float yf[VE];
+            uint4* yp = reinterpret_cast<uint4*>(y + int64_t(M.tok[it.ts + t]) * ldy + cDS + int64_t(cv) * VE);
+            V::to_f32(kPrefetchY ? yv[kPrefetchY ? t : 0] : *yp, yf);
+#pragma unroll
+            for (int e = 0; e < VE; ++e) yf[e] = yf[e] + it.scale * acc[t][e];
+            *yp = V::from_f32(yf);
+        }
+    }
+}
+
 // ------------------------------------------------------------ the kernel
 template <typename T, int MODE>
 __global__ void __launch_bounds__(kThreads, 1) mbgmv_kernel(const __grid_constant__ LoraParams p) {
@@ -257,6 +413,7 @@ __global__ void __launch_bounds__(kThreads, 1) mbgmv_kernel(const __grid_constan
     const int ns = p.ns;
     const size_t rowb = L.row_bytes;
 
+    if (tid == 0) TRACE(0);
     if (tid == 0) {
         for (int s = 0; s < ns; ++s) {
             mbar_init(&full[s], 1);
@@ -265,13 +422,15 @@ __global__ void __launch_bounds__(kThreads, 1) mbgmv_kernel(const __grid_constan
         for (int b = 0; b < 2; ++b) {
             mbar_init(&xfull[b], 1);
             mbar_init(&xempty[b], kConsumerWarps);
-            mbar_init(&exch[b], C);
+            mbar_init(&exch[b], 1);
             mbar_init(&mfull[b], 1);
         }
         fence_mbar_init();
     }
     if (MODE == kExpand) __syncthreads();
-    else cluster_sync_all();  // peers arrive on our barriers / write our smem
+    else cluster_sync_all();  // peers push into our smem / arrive on our barriers
+    pdl_trigger();            // the next launch may start its prologue
+    if (tid == 0) TRACE(1);
 
     const int u_beg = p.sched_off[cl], u_end = p.sched_off[cl + 1];
     const T* pool = reinterpret_cast<const T*>(p.pool);
@@ -281,7 +440,8 @@ __global__ void __launch_bounds__(kThreads, 1) mbgmv_kernel(const __grid_constan
         // ============================ resolver ============================
         // Resolves unit i (items -> segments -> adapter page tables -> the
         // page ids of every row slice this CTA will stream) one unit ahead of
-        // the streamer, so the streaming loop issues copies from smem only.
+        // the streamer.  Reads only the batch descriptor and page tables, so
+        // under PDL it overlaps the previous launch.
         for (int i = 0; u_beg + i < u_end; ++i) {
             const int ub = i & 1;
             if (i >= 2) mbar_wait(&xempty[ub], ((i >> 1) - 1) & 1);
@@ -315,8 +475,7 @@ __global__ void __launch_bounds__(kThreads, 1) mbgmv_kernel(const __grid_constan
                     M.tok_item[it.tok_slot + t] = lane;
                 }
             }
-            // inclusive prefix sums over items -> row offsets
-            int pa = ra, pb = rr;
+            int pa = ra, pb = rr;  // inclusive prefix sums over items -> row offsets
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
                 const int xa = __shfl_up_sync(0xffffffffu, pa, o);
@@ -347,7 +506,6 @@ __global__ void __launch_bounds__(kThreads, 1) mbgmv_kernel(const __grid_constan
                 M.EF = tot_vf;
             }
             __syncwarp();
-            // page ids of every row slice (independent loads, one per lane)
             if (MODE != kExpand) {
                 for (int q = lane; q < RA; q += 32) {
                     const ItemMeta& it = M.it[M.rowA_item[q]];
@@ -364,19 +522,20 @@ __global__ void __launch_bounds__(kThreads, 1) mbgmv_kernel(const __grid_constan
                 }
             }
             __syncwarp();
+            if (lane == 0 && i < 4) TRACE(2 + i * 8);
             if (lane == 0) mbar_arrive(&mfull[ub]);
         }
     } else if (warp == kConsumerWarps) {
         // ============================ streamer ============================
-        int slot = 0;
-        uint32_t lap = 0;
+        pdl_wait();  // pages, x and y may be produced by the previous launch
+        Ring rg;
         for (int i = 0; u_beg + i < u_end; ++i) {
             const int ub = i & 1;
             mbar_wait(&mfull[ub], (i >> 1) & 1);
+            if (lane == 0 && i < 4) TRACE(3 + i * 8);
             const UnitMeta& M = meta[ub];
             const int RA = M.RA, RB = M.RB, toks = M.toks;
-            // ---- x rows of the unit (the same arrive publishes the meta)
-            if (MODE != kExpand) {
+            if (MODE != kExpand) {  // x rows of the unit; the same arrive publishes the meta
                 if (lane == 0) mbar_arrive_expect_tx(&xfull[ub], uint32_t(toks * KS * ES));
                 __syncwarp();
                 if (lane < toks) {
@@ -387,20 +546,19 @@ __global__ void __launch_bounds__(kThreads, 1) mbgmv_kernel(const __grid_constan
             } else {
                 if (lane == 0) mbar_arrive(&xfull[ub]);
             }
-            // ---- A rows (K slice c), then B rows (D slice c)
-            for (int phase = 0; phase < 2; ++phase) {
+            for (int phase = 0; phase < 2; ++phase) {  // A rows (K slice c), then B rows (D slice c)
                 if (phase == 0 && MODE == kExpand) continue;
                 if (phase == 1 && MODE == kShrink) continue;
                 const int R = phase == 0 ? RA : RB;
                 const uint32_t row_bytes = uint32_t((phase == 0 ? KS : DS) * ES);
                 for (int base = 0; base < R; base += kRowsPerSlot) {
                     const int nrow = min(kRowsPerSlot, R - base);
-                    mbar_wait(&empty[slot], (lap & 1) ^ 1);
-                    if (lane == 0) mbar_arrive_expect_tx(&full[slot], uint32_t(nrow) * row_bytes);
+                    mbar_wait(&empty[rg.slot], (rg.lap & 1) ^ 1);
+                    if (lane == 0) mbar_arrive_expect_tx(&full[rg.slot], uint32_t(nrow) * row_bytes);
                     __syncwarp();
                     if (lane < nrow) {
                         const int row = base + lane;
-                        unsigned char* dst = ring + (size_t(slot) * kRowsPerSlot + lane) * rowb;
+                        unsigned char* dst = ring + (size_t(rg.slot) * kRowsPerSlot + lane) * rowb;
                         if (phase == 0) {
                             int64_t k = int64_t(c) * KS;
                             const int64_t kend = k + KS;
@@ -408,93 +566,63 @@ __global__ void __launch_bounds__(kThreads, 1) mbgmv_kernel(const __grid_constan
                             while (k < kend) {  // a slice may span pages (TP q/k/v rows)
                                 const int32_t page = M.pa[row][ch++];
                                 const int64_t len = min(P - k % P, kend - k);
-                                bulk_g2s(dst, pool + int64_t(page) * P + k % P, uint32_t(len * ES), &full[slot]);
+                                bulk_g2s(dst, pool + int64_t(page) * P + k % P, uint32_t(len * ES), &full[rg.slot]);
                                 dst += len * ES;
                                 k += len;
                             }
                         } else {
-                            bulk_g2s(dst, pool + int64_t(M.pb[row]) * P + int64_t(c) * DS, row_bytes, &full[slot]);
+                            bulk_g2s(dst, pool + int64_t(M.pb[row]) * P + int64_t(c) * DS, row_bytes, &full[rg.slot]);
                         }
                     }
-                    if (++slot == ns) { slot = 0; ++lap; }
+                    rg.advance(ns);
                 }
             }
+            if (lane == 0 && i < 4) TRACE(4 + i * 8);
         }
     } else {
         // ============================ consumers ===========================
-        int slot = 0;
-        uint32_t lap = 0;
-        const int nvec_k = int(KS / VE);
+        Ring rg;
+        const int nvec_k = int(KS * ES / 16);
         const int cvs = int(DS / VE);
-        const int nwc = (cvs + 31) / 32;                    // warps covering the columns
-        const int ntg = kConsumerWarps / (nwc > 0 ? nwc : 1); // token groups
-        const int wc = warp % (nwc > 0 ? nwc : 1);
-        const int tg = warp / (nwc > 0 ? nwc : 1);
-        const int cv = wc * 32 + lane;
+        const int cv = warp * 32 + lane;
+        const bool active = cv < cvs;  // expand: this thread's 16-byte column vector
         for (int i = 0; u_beg + i < u_end; ++i) {
             const int ub = i & 1;
             mbar_wait(&xfull[ub], (i >> 1) & 1);
+            if (tid == 0 && i < 4) TRACE(5 + i * 8);
             const UnitMeta& M = meta[ub];
             if (MODE != kExpand) {
                 // ------------------------------ shrink ------------------------------
-                const T* xr = xrows + size_t(ub) * kTokCap * KS;
                 float* xb = xbuf + size_t(ub) * C * kVCap;
+                if (tid == 0) mbar_arrive_expect_tx(&exch[ub], uint32_t(C * M.E * 4));
+                const T* xr = xrows + size_t(ub) * kTokCap * KS;
                 for (int base = 0; base < M.RA; base += kRowsPerSlot) {
-                    mbar_wait(&full[slot], lap & 1);
+                    mbar_wait(&full[rg.slot], rg.lap & 1);
                     const int row = base + warp;
                     if (row < M.RA) {
                         const ItemMeta& it = M.it[M.rowA_item[row]];
                         const int j = row - it.rowA;
-                        const uint4* arow = reinterpret_cast<const uint4*>(ring + (size_t(slot) * kRowsPerSlot + warp) * rowb);
-                        float acc[kTokCap];
-#pragma unroll
-                        for (int t = 0; t < kTokCap; ++t) acc[t] = 0.f;
-                        for (int q = lane; q < nvec_k; q += 32) {
-                            float a[VE];
-                            V::to_f32(arow[q], a);
-#pragma unroll
-                            for (int t = 0; t < kTokCap; ++t) {
-                                if (t < it.nt) {
-                                    float xv[VE];
-                                    V::to_f32(reinterpret_cast<const uint4*>(xr + size_t(it.ts + t) * KS)[q], xv);
-#pragma unroll
-                                    for (int e = 0; e < VE; ++e) acc[t] = fmaf(xv[e], a[e], acc[t]);
-                                }
-                            }
-                        }
-#pragma unroll
-                        for (int t = 0; t < kTokCap; ++t) {
-                            if (t < it.nt) {
-                                float s = acc[t];
-#pragma unroll
-                                for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-                                acc[t] = s;
-                            }
-                        }
-                        // lane (t, cc) pushes token t's partial into CTA cc's slot [c]
-                        for (int w = lane; w < it.nt * C; w += 32) {
-                            const int t = w / C, cc = w % C;
-                            float s = 0.f;
-#pragma unroll
-                            for (int tt = 0; tt < kTokCap; ++tt)
-                                if (tt == t) s = acc[tt];
-                            const float* dst = xb + size_t(c) * kVCap + it.v_off + t * it.ra + j;
-                            st_dsmem(dst, uint32_t(cc), s);
+                        const uint4* arow =
+                            reinterpret_cast<const uint4*>(ring + (size_t(rg.slot) * kRowsPerSlot + warp) * rowb);
+                        switch (it.nt) {
+#define SLORA_SHRINK_CASE(N) \
+    case N: shrink_row<T, N>(arow, xr, KS, nvec_k, it, j, xb, &exch[ub], C, c, lane); break;
+                            SLORA_SHRINK_CASE(1) SLORA_SHRINK_CASE(2) SLORA_SHRINK_CASE(3) SLORA_SHRINK_CASE(4)
+                            SLORA_SHRINK_CASE(5) SLORA_SHRINK_CASE(6) SLORA_SHRINK_CASE(7) SLORA_SHRINK_CASE(8)
+#undef SLORA_SHRINK_CASE
+                            default: break;
                         }
                     }
                     __syncwarp();
-                    if (lane == 0) mbar_arrive(&empty[slot]);
-                    if (++slot == ns) { slot = 0; ++lap; }
+                    if (lane == 0) mbar_arrive(&empty[rg.slot]);
+                    rg.advance(ns);
                 }
-                fence_cluster();
-                consumer_sync();
-                if (tid == 0)
-                    for (int cc = 0; cc < C; ++cc) mbar_arrive_remote(&exch[ub], uint32_t(cc));
-                mbar_wait_cluster(&exch[ub], (i >> 1) & 1);
-                // combine the C partials in fixed order
+                if (tid == 0 && i < 4) TRACE(6 + i * 8);
+                mbar_wait(&exch[ub], (i >> 1) & 1);  // all C partials landed (st.async complete_tx)
+                if (tid == 0 && i < 4) TRACE(7 + i * 8);
                 for (int e = tid; e < M.E; e += kConsumerWarps * 32) {
                     float s = 0.f;
-                    for (int cc = 0; cc < C; ++cc) s += xb[size_t(cc) * kVCap + e];
+                    for (int cc = 0; cc < C; ++cc) s += xb[size_t(cc) * kVCap + e];  // fixed order
                     if (MODE == kFused) {
                         vfull[e] = s;
                     } else if (e % C == c) {
@@ -533,69 +661,43 @@ __global__ void __launch_bounds__(kThreads, 1) mbgmv_kernel(const __grid_constan
             }
             if (MODE != kShrink) {
                 // ------------------------------ expand ------------------------------
-                // token slots owned by this thread: t % ntg == tg (bit mask)
-                uint32_t own = 0;
-                if (cv < cvs)
-                    for (int t = tg; t < M.toks; t += ntg) own |= 1u << t;
-                uint4 yv[kTokCap];
-                float acc[kTokCap][VE];
-#pragma unroll
-                for (int t = 0; t < kTokCap; ++t) {
-#pragma unroll
-                    for (int e = 0; e < VE; ++e) acc[t][e] = 0.f;
-                    if (own >> t & 1u) {
-                        const ItemMeta& it = M.it[M.tok_item[t]];
-                        const T* y = reinterpret_cast<const T*>(p.y[it.proj]);
-                        yv[t] = *reinterpret_cast<const uint4*>(y + int64_t(M.tok[t]) * p.ldy[it.proj] + c * DS +
-                                                                int64_t(cv) * VE);
+                int row = 0;
+                const int64_t cDS = int64_t(c) * DS;
+                for (int ii = 0; ii < M.n_items; ++ii) {
+                    const ItemMeta& it = M.it[ii];
+                    switch (it.nt) {
+#define SLORA_EXPAND_CASE(N)                                                                              \
+    case N:                                                                                               \
+        expand_item<T, N>(p, M, it, ring, rowb, full, empty, rg, ns, row, vfull, active, cv, cDS, lane); \
+        break;
+                        SLORA_EXPAND_CASE(1) SLORA_EXPAND_CASE(2) SLORA_EXPAND_CASE(3) SLORA_EXPAND_CASE(4)
+                        SLORA_EXPAND_CASE(5) SLORA_EXPAND_CASE(6) SLORA_EXPAND_CASE(7) SLORA_EXPAND_CASE(8)
+#undef SLORA_EXPAND_CASE
+                        default: break;
                     }
                 }
-                for (int base = 0; base < M.RB; base += kRowsPerSlot) {
-                    mbar_wait(&full[slot], lap & 1);
-                    if (own) {
-                        const int nr = min(kRowsPerSlot, M.RB - base);
-                        for (int q = 0; q < nr; ++q) {
-                            const int row = base + q;
-                            const ItemMeta& it = M.it[M.rowB_item[row]];
-                            const uint32_t m = own & (((1u << it.nt) - 1u) << it.ts);
-                            if (!m) continue;
-                            const int j = row - it.rowB;
-                            float b[VE];
-                            V::to_f32(reinterpret_cast<const uint4*>(ring + (size_t(slot) * kRowsPerSlot + q) * rowb)[cv], b);
-                            const float* vcol = vfull + it.vf_off + j - it.ts * it.r;
-#pragma unroll
-                            for (int t = 0; t < kTokCap; ++t) {
-                                if (m >> t & 1u) {
-                                    const float vj = vcol[t * it.r];
-#pragma unroll
-                                    for (int e = 0; e < VE; ++e) acc[t][e] = fmaf(vj, b[e], acc[t][e]);
-                                }
-                            }
-                        }
-                    }
+                if (row > 0) {  // release the unit's last B slot
                     __syncwarp();
-                    if (lane == 0) mbar_arrive(&empty[slot]);
-                    if (++slot == ns) { slot = 0; ++lap; }
-                }
-#pragma unroll
-                for (int t = 0; t < kTokCap; ++t) {
-                    if (own >> t & 1u) {
-                        const ItemMeta& it = M.it[M.tok_item[t]];
-                        T* y = reinterpret_cast<T*>(p.y[it.proj]);
-                        float yf[VE];
-                        V::to_f32(yv[t], yf);
-#pragma unroll
-                        for (int e = 0; e < VE; ++e) yf[e] = yf[e] + it.scale * acc[t][e];
-                        *reinterpret_cast<uint4*>(y + int64_t(M.tok[t]) * p.ldy[it.proj] + c * DS + int64_t(cv) * VE) =
-                            V::from_f32(yf);
-                    }
+                    if (lane == 0) mbar_arrive(&empty[rg.slot]);
+                    rg.advance(ns);
                 }
             }
+            if (tid == 0 && i < 4) TRACE(8 + i * 8);
             __syncwarp();
             if (lane == 0) mbar_arrive(&xempty[ub]);
         }
     }
+    if (tid == 0) TRACE(40);
     if (MODE != kExpand) cluster_sync_all();  // no CTA leaves while peers may touch its smem
+    if (tid == 0) TRACE(41);
+}
+
+static bool pdl_enabled() {
+    static const bool on = [] {
+        const char* s = getenv("SLORA_PDL");
+        return !(s && atoi(s) == 0);
+    }();
+    return on;
 }
 
 template <typename T, int MODE>
@@ -623,14 +725,19 @@ static cudaError_t launch_t(const LoraParams& p, cudaStream_t s, size_t smem) {
     cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     int na = 0;
     if (MODE != kExpand) {
-        attr[0].id = cudaLaunchAttributeClusterDimension;
-        attr[0].val.clusterDim.x = unsigned(p.C);
-        attr[0].val.clusterDim.y = 1;
-        attr[0].val.clusterDim.z = 1;
-        na = 1;
+        attr[na].id = cudaLaunchAttributeClusterDimension;
+        attr[na].val.clusterDim.x = unsigned(p.C);
+        attr[na].val.clusterDim.y = 1;
+        attr[na].val.clusterDim.z = 1;
+        ++na;
+    }
+    if (pdl_enabled()) {  // programmatic dependent launch: prologue overlaps the previous kernel
+        attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
     }
     cfg.attrs = attr;
     cfg.numAttrs = na;

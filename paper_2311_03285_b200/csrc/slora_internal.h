@@ -79,6 +79,7 @@ struct LoraParams {
     int64_t ldx;
     void* y[4];
     int64_t ldy[4];
+    long long* trace;            // debug: per-CTA event timestamps (nullptr = off)
     float* v_out;
     const float* v_in;
     int32_t v_blocks;

@@ -88,6 +88,7 @@ SIGNATURES = {
     "slora_lora_shrink": [_VP, _VP, _I32, _U32, _VP, _I64, _VP, _VP],
     "slora_lora_expand": [_VP, _VP, _I32, _U32, _VP, _I32, ctypes.POINTER(_VP), _PI64, _VP],
     "slora_sync": [_VP, _VP],
+    "slora_debug_trace": [_VP, _PI64, _I32],
 }
 
 _lib = None
@@ -253,6 +254,12 @@ class Pool:
 
     def sync(self, stream=None) -> None:
         _check(lib().slora_sync(self.h, _stream(stream)))
+
+    def debug_trace(self) -> np.ndarray:
+        """[16 CTAs, 64 events] globaltimer ns of the last traced launches."""
+        out = np.zeros(1024, np.int64)
+        _check(lib().slora_debug_trace(self.h, out.ctypes.data_as(_PI64), 1024))
+        return out.reshape(16, 64)
 
 
 class Batch:
