@@ -133,8 +133,16 @@ KernelCfg make_kernel_cfg(int mode, int64_t K, int64_t D, int64_t P, int es, int
         if (mode != kShrink && (D % C || ((D / C) * es) % 16 || (D / C) * es > 4096)) return false;
         return true;
     };
+    // prefer the largest split whose slices stay >= 2 KB: bulk copies of 2 KB
+    // and up stream at full HBM rate (measured), and more CTAs per unit
+    // spread few units over more SMs
+    auto big = [&](int C) {
+        return (mode == kExpand || (K / C) * es >= 2048) && (mode == kShrink || (D / C) * es >= 2048);
+    };
     int C = 0;
     if (forced > 0 && forced <= 16 && valid(forced)) C = forced;
+    for (int c = 16; c >= 1 && !C; --c)
+        if (valid(c) && big(c)) C = c;
     for (int c = 1; c <= 16 && !C; ++c)
         if (valid(c)) C = c;
     if (!C) return k;
@@ -201,6 +209,7 @@ struct slora_batch {
     int64_t NR = 0;
     int64_t weight_bytes_per_proj = 0;
     std::vector<DevSeg> segs;
+    std::vector<const int32_t*> seg_tab;  // device page table of each segment's adapter
     std::vector<int32_t> tok_idx;
     std::vector<DevUnit> units[5];
     std::vector<DevItem> items[5];
@@ -658,10 +667,15 @@ void build_units(slora_batch* b, int nproj) {
         for (int pi = 0; pi < nproj; ++pi)
             for (int t0 = 0; t0 < s.n_tok; t0 += tmax) {
                 DevItem it{};
+                it.tab = b->seg_tab.empty() ? nullptr : b->seg_tab[size_t(si)];
+                it.vrow = s.vrow_off + int64_t(t0) * s.rank;
+                it.rank = s.rank;
                 it.seg = si;
                 it.pi = pi;
                 it.t0 = t0;
                 it.nt = std::min(tmax, s.n_tok - t0);
+                it.tok_off = s.tok_off + t0;
+                it.scale = s.scale;
                 all.push_back({it, s.rank});
             }
     }
@@ -793,6 +807,7 @@ extern "C" slora_status slora_batch_prepare(slora_batch_t b, const int64_t* tok_
         toks[size_t(s)].push_back(i);
     }
     b->segs.clear();
+    b->seg_tab.clear();
     b->tok_idx.clear();
     b->T = T;
     b->adapted = 0;
@@ -812,6 +827,7 @@ extern "C" slora_status slora_batch_prepare(slora_batch_t b, const int64_t* tok_
         b->weight_bytes_per_proj += int64_t(ad.rank) * 2 * p->P * p->es;
         for (int32_t t : toks[s]) b->tok_idx.push_back(t);
         b->segs.push_back(sg);
+        b->seg_tab.push_back(ad.dev_tab);
     }
     for (int np = 1; np <= 4; ++np) build_units(b, np);
     for (int kc = 0; kc < 4; ++kc)

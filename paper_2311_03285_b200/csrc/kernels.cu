@@ -196,8 +196,8 @@ struct ItemMeta {
     int32_t vf_off;      // first v entry in full-rank units (expand)
     int32_t proj, arp;   // projection id, pages per stored A row
     float scale;
-    int32_t seg, t0;
-    int32_t pad;
+    int32_t pi;          // projection index in the call's mask order
+    int64_t vrow;        // v row offset (segment vrow_off + t0 * rank)
 };
 struct UnitMeta {
     int32_t n_items, RA, RB, toks, E, EF, pad0, pad1;
@@ -331,9 +331,16 @@ template <typename T, int NT>
 __device__ __forceinline__ void expand_item(const LoraParams& p, const UnitMeta& M, const ItemMeta& it,
                                             const unsigned char* ring, size_t rowb, uint64_t* full, uint64_t* empty,
                                             Ring& rg, int ns, int& row, const float* vfull, bool active, int cv,
-                                            int64_t cDS, int lane) {
+                                            int64_t cDS, int lane, int tg, int ntg) {
     using V = Vec<T>;
     constexpr int VE = V::VE;
+    // tokens of this item owned by this thread: t % ntg == tg (ntg power of 2)
+    uint32_t own = 0;
+    if (active)
+#pragma unroll
+        for (int t = 0; t < NT; ++t)
+            if ((t & (ntg - 1)) == tg) own |= 1u << t;
+    active = own != 0;
     float acc[NT][VE];
 #pragma unroll
     for (int t = 0; t < NT; ++t)
@@ -348,8 +355,9 @@ __device__ __forceinline__ void expand_item(const LoraParams& p, const UnitMeta&
     if (kPrefetchY && active) {
 #pragma unroll
         for (int t = 0; t < NT; ++t)
-            yv[kPrefetchY ? t : 0] =
-                *reinterpret_cast<const uint4*>(y + int64_t(M.tok[it.ts + t]) * ldy + cDS + int64_t(cv) * VE);
+            if (own >> t & 1u)
+                yv[kPrefetchY ? t : 0] =
+                    *reinterpret_cast<const uint4*>(y + int64_t(M.tok[it.ts + t]) * ldy + cDS + int64_t(cv) * VE);
     }
     for (int j = 0; j < it.r; ++j, ++row) {
         if ((row & (kRowsPerSlot - 1)) == 0) {
@@ -367,15 +375,18 @@ __device__ __forceinline__ void expand_item(const LoraParams& p, const UnitMeta&
             const float* vc = vfull + it.vf_off + j;
 #pragma unroll
             for (int t = 0; t < NT; ++t) {
-                const float vj = vc[t * it.r];
+                if (own >> t & 1u) {
+                    const float vj = vc[t * it.r];
 #pragma unroll
-                for (int e = 0; e < VE; ++e) acc[t][e] = fmaf(vj, b[e], acc[t][e]);
+                    for (int e = 0; e < VE; ++e) acc[t][e] = fmaf(vj, b[e], acc[t][e]);
+                }
             }
         }
     }
     if (active) {
 #pragma unroll
         for (int t = 0; t < NT; ++t) {
+            if (!(own >> t & 1u)) continue;
             float yf[VE];
             uint4* yp = reinterpret_cast<uint4*>(y + int64_t(M.tok[it.ts + t]) * ldy + cDS + int64_t(cv) * VE);
             V::to_f32(kPrefetchY ? yv[kPrefetchY ? t : 0] : *yp, yf);
@@ -451,27 +462,26 @@ __global__ void __launch_bounds__(kThreads, 1) mbgmv_kernel(const __grid_constan
             ItemMeta im{};
             if (lane < U.n_items) {
                 const DevItem it = p.items[U.item_begin + lane];
-                const DevSeg sg = p.segs[it.seg];
                 const int proj = p.proj_ids[it.pi];
                 const int div = (MODE == kExpand) ? 1 : p.a_div[proj];
-                im.tab = p.slot_tab[sg.slot] + int64_t((p.layer * 4 + proj) * 2) * sg.rank;
-                im.ra = sg.rank / div;
-                im.r = sg.rank;
+                im.tab = it.tab + int64_t((p.layer * 4 + proj) * 2) * it.rank;
+                im.ra = it.rank / div;
+                im.r = it.rank;
                 im.ts = it.tok_slot;
                 im.nt = it.nt;
                 im.v_off = it.v_off / div;
                 im.vf_off = it.v_off;
                 im.proj = proj;
                 im.arp = p.a_row_pages[proj];
-                im.scale = sg.scale;
-                im.seg = it.seg;
-                im.t0 = it.t0;
+                im.scale = it.scale;
+                im.pi = it.pi;
+                im.vrow = it.vrow;
                 ra = im.ra;
                 rr = im.r;
                 ve = im.nt * im.ra;
                 vf = im.nt * im.r;
                 for (int t = 0; t < it.nt; ++t) {
-                    M.tok[it.tok_slot + t] = p.tok_idx[sg.tok_off + it.t0 + t];
+                    M.tok[it.tok_slot + t] = p.tok_idx[it.tok_off + t];
                     M.tok_item[it.tok_slot + t] = lane;
                 }
             }
@@ -527,14 +537,52 @@ __global__ void __launch_bounds__(kThreads, 1) mbgmv_kernel(const __grid_constan
         }
     } else if (warp == kConsumerWarps) {
         // ============================ streamer ============================
-        pdl_wait();  // pages, x and y may be produced by the previous launch
+        // Adapter pages are written only by the loader's scatter kernel, which
+        // never triggers its dependents early, so pages may be streamed before
+        // griddepcontrol.wait; x and y (and v) are touched only after it.
         Ring rg;
+        bool waited = false;
         for (int i = 0; u_beg + i < u_end; ++i) {
             const int ub = i & 1;
             mbar_wait(&mfull[ub], (i >> 1) & 1);
             if (lane == 0 && i < 4) TRACE(3 + i * 8);
             const UnitMeta& M = meta[ub];
             const int RA = M.RA, RB = M.RB, toks = M.toks;
+            auto issue_slot = [&](int phase, int base) {
+                const int R = phase == 0 ? RA : RB;
+                const uint32_t row_bytes = uint32_t((phase == 0 ? KS : DS) * ES);
+                const int nrow = min(kRowsPerSlot, R - base);
+                mbar_wait(&empty[rg.slot], (rg.lap & 1) ^ 1);
+                if (lane == 0) mbar_arrive_expect_tx(&full[rg.slot], uint32_t(nrow) * row_bytes);
+                __syncwarp();
+                if (lane < nrow) {
+                    const int row = base + lane;
+                    unsigned char* dst = ring + (size_t(rg.slot) * kRowsPerSlot + lane) * rowb;
+                    if (phase == 0) {
+                        int64_t k = int64_t(c) * KS;
+                        const int64_t kend = k + KS;
+                        int ch = 0;
+                        while (k < kend) {  // a slice may span pages (TP q/k/v rows)
+                            const int32_t page = M.pa[row][ch++];
+                            const int64_t len = min(P - k % P, kend - k);
+                            bulk_g2s(dst, pool + int64_t(page) * P + k % P, uint32_t(len * ES), &full[rg.slot]);
+                            dst += len * ES;
+                            k += len;
+                        }
+                    } else {
+                        bulk_g2s(dst, pool + int64_t(M.pb[row]) * P + int64_t(c) * DS, row_bytes, &full[rg.slot]);
+                    }
+                }
+                rg.advance(ns);
+            };
+            const int first_phase = MODE == kExpand ? 1 : 0;
+            int pre = 0;  // slots of the first phase issued before the PDL wait
+            if (!waited) {
+                const int R0 = first_phase == 0 ? RA : RB;
+                for (int base = 0; base < R0 && pre < ns; base += kRowsPerSlot, ++pre) issue_slot(first_phase, base);
+                pdl_wait();
+                waited = true;
+            }
             if (MODE != kExpand) {  // x rows of the unit; the same arrive publishes the meta
                 if (lane == 0) mbar_arrive_expect_tx(&xfull[ub], uint32_t(toks * KS * ES));
                 __syncwarp();
@@ -546,36 +594,11 @@ __global__ void __launch_bounds__(kThreads, 1) mbgmv_kernel(const __grid_constan
             } else {
                 if (lane == 0) mbar_arrive(&xfull[ub]);
             }
-            for (int phase = 0; phase < 2; ++phase) {  // A rows (K slice c), then B rows (D slice c)
-                if (phase == 0 && MODE == kExpand) continue;
+            for (int phase = first_phase; phase < 2; ++phase) {  // A rows (K slice c), then B rows (D slice c)
                 if (phase == 1 && MODE == kShrink) continue;
                 const int R = phase == 0 ? RA : RB;
-                const uint32_t row_bytes = uint32_t((phase == 0 ? KS : DS) * ES);
-                for (int base = 0; base < R; base += kRowsPerSlot) {
-                    const int nrow = min(kRowsPerSlot, R - base);
-                    mbar_wait(&empty[rg.slot], (rg.lap & 1) ^ 1);
-                    if (lane == 0) mbar_arrive_expect_tx(&full[rg.slot], uint32_t(nrow) * row_bytes);
-                    __syncwarp();
-                    if (lane < nrow) {
-                        const int row = base + lane;
-                        unsigned char* dst = ring + (size_t(rg.slot) * kRowsPerSlot + lane) * rowb;
-                        if (phase == 0) {
-                            int64_t k = int64_t(c) * KS;
-                            const int64_t kend = k + KS;
-                            int ch = 0;
-                            while (k < kend) {  // a slice may span pages (TP q/k/v rows)
-                                const int32_t page = M.pa[row][ch++];
-                                const int64_t len = min(P - k % P, kend - k);
-                                bulk_g2s(dst, pool + int64_t(page) * P + k % P, uint32_t(len * ES), &full[rg.slot]);
-                                dst += len * ES;
-                                k += len;
-                            }
-                        } else {
-                            bulk_g2s(dst, pool + int64_t(M.pb[row]) * P + int64_t(c) * DS, row_bytes, &full[rg.slot]);
-                        }
-                    }
-                    rg.advance(ns);
-                }
+                for (int base = (phase == first_phase ? pre : 0) * kRowsPerSlot; base < R; base += kRowsPerSlot)
+                    issue_slot(phase, base);
             }
             if (lane == 0 && i < 4) TRACE(4 + i * 8);
         }
@@ -583,9 +606,15 @@ __global__ void __launch_bounds__(kThreads, 1) mbgmv_kernel(const __grid_constan
         // ============================ consumers ===========================
         Ring rg;
         const int nvec_k = int(KS * ES / 16);
+        // expand: nwc warps cover the D slice's 16-byte column vectors; the
+        // remaining warps split the item's tokens (token t -> group t % ntg)
         const int cvs = int(DS / VE);
-        const int cv = warp * 32 + lane;
-        const bool active = cv < cvs;  // expand: this thread's 16-byte column vector
+        const int nwc = max(1, (cvs + 31) / 32);
+        int ntg = 1;
+        while (ntg * 2 * nwc <= kConsumerWarps) ntg *= 2;
+        const int wc = warp % nwc, tg = warp / nwc;
+        const int cv = wc * 32 + lane;
+        const bool active = cv < cvs && tg < ntg;
         for (int i = 0; u_beg + i < u_end; ++i) {
             const int ub = i & 1;
             mbar_wait(&xfull[ub], (i >> 1) & 1);
@@ -630,12 +659,8 @@ __global__ void __launch_bounds__(kThreads, 1) mbgmv_kernel(const __grid_constan
                         int ii = 0;
                         while (ii + 1 < M.n_items && M.it[ii + 1].v_off <= e) ++ii;
                         const ItemMeta& it = M.it[ii];
-                        const DevSeg sg = p.segs[it.seg];
                         const int div = it.r / it.ra;
-                        int pi = 0;
-                        for (int q = 0; q < p.nproj; ++q)
-                            if (p.proj_ids[q] == it.proj) pi = q;
-                        const int64_t base = int64_t(pi) * (p.NR / div) + (sg.vrow_off + int64_t(it.t0) * it.r) / div;
+                        const int64_t base = int64_t(it.pi) * (p.NR / div) + it.vrow / div;
                         p.v_out[base + (e - it.v_off)] = s;
                     }
                 }
@@ -648,13 +673,9 @@ __global__ void __launch_bounds__(kThreads, 1) mbgmv_kernel(const __grid_constan
                     int ii = 0;
                     while (ii + 1 < M.n_items && M.it[ii + 1].vf_off <= e) ++ii;
                     const ItemMeta& it = M.it[ii];
-                    const DevSeg sg = p.segs[it.seg];
-                    int pi = 0;
-                    for (int q = 0; q < p.nproj; ++q)
-                        if (p.proj_ids[q] == it.proj) pi = q;
                     const int r = it.r, rb = r / vb;
                     const int le = e - it.vf_off, t = le / r, j = le % r;
-                    const int64_t base = int64_t(pi) * (p.NR / vb) + (sg.vrow_off + int64_t(it.t0) * r) / vb;
+                    const int64_t base = int64_t(it.pi) * (p.NR / vb) + it.vrow / vb;
                     vfull[e] = p.v_in[int64_t(j / rb) * stride + base + int64_t(t) * rb + (j % rb)];
                 }
                 consumer_sync();
@@ -668,7 +689,7 @@ __global__ void __launch_bounds__(kThreads, 1) mbgmv_kernel(const __grid_constan
                     switch (it.nt) {
 #define SLORA_EXPAND_CASE(N)                                                                              \
     case N:                                                                                               \
-        expand_item<T, N>(p, M, it, ring, rowb, full, empty, rg, ns, row, vfull, active, cv, cDS, lane); \
+        expand_item<T, N>(p, M, it, ring, rowb, full, empty, rg, ns, row, vfull, active, cv, cDS, lane, tg, ntg); \
         break;
                         SLORA_EXPAND_CASE(1) SLORA_EXPAND_CASE(2) SLORA_EXPAND_CASE(3) SLORA_EXPAND_CASE(4)
                         SLORA_EXPAND_CASE(5) SLORA_EXPAND_CASE(6) SLORA_EXPAND_CASE(7) SLORA_EXPAND_CASE(8)

@@ -25,16 +25,23 @@ static_assert(sizeof(DevSeg) == 32, "DevSeg layout");
 // chunk).  Items are packed into units (<= kRowCap A/B rows, <= kTokCap token
 // slots, <= kVCap v entries); a cluster of C CTAs processes a unit, CTA c
 // owning the c-th 1/C slice of K (shrink) and of D (expand).
+// Self-contained: the kernel resolves an item with one load (no segment or
+// slot-table indirection).
 struct DevItem {
-    int32_t seg;
+    const int32_t* tab;  // the adapter's device page table (layer/proj offset added in-kernel)
+    int64_t vrow;      // v row offset of the chunk: segment vrow_off + t0 * rank
+    int32_t rank;
     int32_t pi;        // index of the projection in the call's mask order
     int32_t t0, nt;    // token chunk [t0, t0+nt) of the segment
-    int32_t row_off;   // first row of this item within the unit (full rank units)
+    int32_t tok_off;   // index in tok_idx of the chunk's first token
     int32_t tok_slot;  // first token slot within the unit
     int32_t v_off;     // first v entry within the unit (full rank units)
-    int32_t pad;
+    int32_t row_off;   // first row of this item within the unit (full rank units)
+    float scale;
+    int32_t seg;
+    int32_t pad[2];
 };
-static_assert(sizeof(DevItem) == 32, "DevItem layout");
+static_assert(sizeof(DevItem) == 64, "DevItem layout");
 
 struct DevUnit {
     int32_t item_begin, n_items;
@@ -51,7 +58,7 @@ constexpr int kConsumerWarps = 8;
 constexpr int kThreads = (kConsumerWarps + 2) * 32;  // + streamer warp + resolver warp
 constexpr int kMaxChunks = 4;    // pages one CTA's K slice of an A row may span
 constexpr int kRowsPerSlot = 8;  // page-slice rows per ring slot
-constexpr int kMaxSlots = 16;
+constexpr int kMaxSlots = 32;
 
 enum Mode : int { kFused = 0, kShrink = 1, kExpand = 2 };
 enum DType : int { kF32 = 0, kF16 = 1, kBF16 = 2 };
