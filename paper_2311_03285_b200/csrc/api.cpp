@@ -300,8 +300,8 @@ extern "C" slora_status slora_pool_create(const slora_pool_config* cfg, slora_po
         p->kcfg[3] = make_kernel_cfg(kExpand, P, P, P, es, dt);
         const char* tr = getenv("SLORA_TRACE");
         if (tr && atoi(tr) == 1) {
-            if ((e = cudaMalloc(&p->trace_dev, 1024 * sizeof(long long)))) return cleanup(e, "cudaMalloc trace");
-            cudaMemset(p->trace_dev, 0, 1024 * sizeof(long long));
+            if ((e = cudaMalloc(&p->trace_dev, 4096 * sizeof(long long)))) return cleanup(e, "cudaMalloc trace");
+            cudaMemset(p->trace_dev, 0, 4096 * sizeof(long long));
         }
         if (cfg->tp_size == 1 && !p->kcfg[0].ok) {
             slora_status s = fail(SLORA_ERR_SHAPE, "no valid MBGMV split for hidden %lld", (long long)H);
@@ -942,6 +942,11 @@ void fill_common(slora_pool* p, slora_batch* b, int kc, int32_t layer, uint32_t 
     q.K = int32_t(k.K);
     q.D = int32_t(k.D);
     q.ns = k.ns;
+    static const int l2pf = [] {
+        const char* s = getenv("SLORA_L2PF");
+        return s ? atoi(s) : 1;
+    }();
+    q.l2_prefetch = l2pf;
     q.NR = b->NR;
     const int N = p->N();
     for (int pj = 0; pj < 4; ++pj) {
@@ -1056,6 +1061,6 @@ extern "C" slora_status slora_debug_trace(slora_pool_t p, int64_t* out, int32_t 
     if (!p->trace_dev) return fail(SLORA_ERR_INVALID_ARG, "tracing is off (set SLORA_TRACE=1 before pool create)");
     CUDA_TRY(cudaSetDevice(p->cfg.device));
     CUDA_TRY(cudaDeviceSynchronize());
-    CUDA_TRY(cudaMemcpy(out, p->trace_dev, sizeof(int64_t) * size_t(std::min(n, 1024)), cudaMemcpyDeviceToHost));
+    CUDA_TRY(cudaMemcpy(out, p->trace_dev, sizeof(int64_t) * size_t(std::min(n, 4096)), cudaMemcpyDeviceToHost));
     return ok();
 }

@@ -101,6 +101,9 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
         "l"(src), "r"(bytes), "r"(smem_u32(bar))
         : "memory");
 }
+__device__ __forceinline__ void prefetch_l2(const void* src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ uint32_t cluster_ctarank() {
     uint32_t r;
     asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
@@ -133,7 +136,11 @@ __device__ __forceinline__ long long gtimer() {
 }
 #define TRACE(ev)                                                                       \
     do {                                                                                \
-        if (p.trace && blockIdx.x < 16 && (ev) < 64) p.trace[blockIdx.x * 64 + (ev)] = gtimer(); \
+        if (p.trace && blockIdx.x < 16 && (ev) < 256) p.trace[blockIdx.x * 256 + (ev)] = gtimer(); \
+    } while (0)
+#define TRACE_SLOT(base, seq)              \
+    do {                                   \
+        if ((seq) < 64) TRACE((base) + (seq)); \
     } while (0)
 
 // ---------------------------------------------------- element conversions
@@ -363,10 +370,12 @@ __device__ __forceinline__ void expand_item(const LoraParams& p, const UnitMeta&
         if ((row & (kRowsPerSlot - 1)) == 0) {
             if (row > 0) {
                 __syncwarp();
+                if (threadIdx.x == 0) TRACE_SLOT(192, int(rg.lap) * ns + rg.slot);
                 if (lane == 0) mbar_arrive(&empty[rg.slot]);
                 rg.advance(ns);
             }
             mbar_wait(&full[rg.slot], rg.lap & 1);
+            if (threadIdx.x == 0) TRACE_SLOT(128, int(rg.lap) * ns + rg.slot);
         }
         if (active) {
             float b[VE];
@@ -534,6 +543,22 @@ __global__ void __launch_bounds__(kThreads, 1) mbgmv_kernel(const __grid_constan
             __syncwarp();
             if (lane == 0 && i < 4) TRACE(2 + i * 8);
             if (lane == 0) mbar_arrive(&mfull[ub]);
+            // Pull the unit's pages into L2 ahead of the streamer: whole pages,
+            // each CTA of the cluster taking every C-th row, so the ring's bulk
+            // copies hit L2 (more bytes in flight than shared memory holds).
+            if (p.l2_prefetch) {
+                const uint32_t page_bytes = uint32_t(P * ES);
+                if (MODE != kExpand)
+                    for (int q = c + lane * C; q < M.RA; q += 32 * C) {
+                        const ItemMeta& it = M.it[M.rowA_item[q]];
+                        const int j = q - it.rowA;
+                        for (int ch = 0; ch < it.arp; ++ch)
+                            prefetch_l2(pool + int64_t(it.tab[j * it.arp + ch]) * P, page_bytes);
+                    }
+                if (MODE != kShrink)
+                    for (int q = c + lane * C; q < M.RB; q += 32 * C)
+                        prefetch_l2(pool + int64_t(M.pb[q]) * P, page_bytes);
+            }
         }
     } else if (warp == kConsumerWarps) {
         // ============================ streamer ============================
@@ -573,6 +598,7 @@ __global__ void __launch_bounds__(kThreads, 1) mbgmv_kernel(const __grid_constan
                         bulk_g2s(dst, pool + int64_t(M.pb[row]) * P + int64_t(c) * DS, row_bytes, &full[rg.slot]);
                     }
                 }
+                if (lane == 0) TRACE_SLOT(64, int(rg.lap) * ns + rg.slot);
                 rg.advance(ns);
             };
             const int first_phase = MODE == kExpand ? 1 : 0;
@@ -627,6 +653,7 @@ __global__ void __launch_bounds__(kThreads, 1) mbgmv_kernel(const __grid_constan
                 const T* xr = xrows + size_t(ub) * kTokCap * KS;
                 for (int base = 0; base < M.RA; base += kRowsPerSlot) {
                     mbar_wait(&full[rg.slot], rg.lap & 1);
+                    if (tid == 0) TRACE_SLOT(128, int(rg.lap) * ns + rg.slot);
                     const int row = base + warp;
                     if (row < M.RA) {
                         const ItemMeta& it = M.it[M.rowA_item[row]];
@@ -643,6 +670,7 @@ __global__ void __launch_bounds__(kThreads, 1) mbgmv_kernel(const __grid_constan
                         }
                     }
                     __syncwarp();
+                    if (tid == 0) TRACE_SLOT(192, int(rg.lap) * ns + rg.slot);
                     if (lane == 0) mbar_arrive(&empty[rg.slot]);
                     rg.advance(ns);
                 }

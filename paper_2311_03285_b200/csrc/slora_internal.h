@@ -82,6 +82,7 @@ struct LoraParams {
     int32_t a_div[4];             // A rank columns stored = r / a_div[p]
     int32_t a_row_pages[4];       // pages per stored A row
     int32_t ns;                   // ring slots
+    int32_t l2_prefetch;          // resolver pulls each unit's pages into L2 ahead of the ring
     const void* x;
     int64_t ldx;
     void* y[4];

@@ -257,9 +257,9 @@ class Pool:
 
     def debug_trace(self) -> np.ndarray:
         """[16 CTAs, 64 events] globaltimer ns of the last traced launches."""
-        out = np.zeros(1024, np.int64)
-        _check(lib().slora_debug_trace(self.h, out.ctypes.data_as(_PI64), 1024))
-        return out.reshape(16, 64)
+        out = np.zeros(4096, np.int64)
+        _check(lib().slora_debug_trace(self.h, out.ctypes.data_as(_PI64), 4096))
+        return out.reshape(16, 256)
 
 
 class Batch:
