@@ -663,7 +663,10 @@ void build_units(slora_batch* b, int nproj) {
     std::vector<It> all;
     for (int si = 0; si < int(b->segs.size()); ++si) {
         const DevSeg& s = b->segs[size_t(si)];
-        const int tmax = std::max(1, std::min(kTokCap, kVCap / s.rank));
+        // at most kItemTokCap tokens per item: a Zipf-head adapter with many
+        // decode tokens is split into several items (its pages are re-read,
+        // but the FMA work spreads over clusters instead of one straggler)
+        const int tmax = std::max(1, std::min(std::min(kTokCap, kItemTokCap), kVCap / s.rank));
         for (int pi = 0; pi < nproj; ++pi)
             for (int t0 = 0; t0 < s.n_tok; t0 += tmax) {
                 DevItem it{};
@@ -944,9 +947,14 @@ void fill_common(slora_pool* p, slora_batch* b, int kc, int32_t layer, uint32_t 
     q.ns = k.ns;
     static const int l2pf = [] {
         const char* s = getenv("SLORA_L2PF");
-        return s ? atoi(s) : 1;
+        return s ? atoi(s) : 0;
     }();
     q.l2_prefetch = l2pf;
+    static const int dbg = [] {
+        const char* s = getenv("SLORA_DBG");
+        return s ? atoi(s) : 0;
+    }();
+    q.dbg = dbg;
     q.NR = b->NR;
     const int N = p->N();
     for (int pj = 0; pj < 4; ++pj) {

@@ -649,13 +649,13 @@ __global__ void __launch_bounds__(kThreads, 1) mbgmv_kernel(const __grid_constan
             if (MODE != kExpand) {
                 // ------------------------------ shrink ------------------------------
                 float* xb = xbuf + size_t(ub) * C * kVCap;
-                if (tid == 0) mbar_arrive_expect_tx(&exch[ub], uint32_t(C * M.E * 4));
+                if (tid == 0) mbar_arrive_expect_tx(&exch[ub], (p.dbg & 1) ? 0u : uint32_t(C * M.E * 4));
                 const T* xr = xrows + size_t(ub) * kTokCap * KS;
                 for (int base = 0; base < M.RA; base += kRowsPerSlot) {
                     mbar_wait(&full[rg.slot], rg.lap & 1);
                     if (tid == 0) TRACE_SLOT(128, int(rg.lap) * ns + rg.slot);
                     const int row = base + warp;
-                    if (row < M.RA) {
+                    if (row < M.RA && !(p.dbg & 1)) {
                         const ItemMeta& it = M.it[M.rowA_item[row]];
                         const int j = row - it.rowA;
                         const uint4* arow =
@@ -717,7 +717,8 @@ __global__ void __launch_bounds__(kThreads, 1) mbgmv_kernel(const __grid_constan
                     switch (it.nt) {
 #define SLORA_EXPAND_CASE(N)                                                                              \
     case N:                                                                                               \
-        expand_item<T, N>(p, M, it, ring, rowb, full, empty, rg, ns, row, vfull, active, cv, cDS, lane, tg, ntg); \
+        expand_item<T, N>(p, M, it, ring, rowb, full, empty, rg, ns, row, vfull, active && !(p.dbg & 2), cv, cDS, \
+                          lane, tg, ntg);                                                                   \
         break;
                         SLORA_EXPAND_CASE(1) SLORA_EXPAND_CASE(2) SLORA_EXPAND_CASE(3) SLORA_EXPAND_CASE(4)
                         SLORA_EXPAND_CASE(5) SLORA_EXPAND_CASE(6) SLORA_EXPAND_CASE(7) SLORA_EXPAND_CASE(8)

@@ -53,6 +53,7 @@ static_assert(sizeof(DevUnit) == 32, "DevUnit layout");
 constexpr int kMaxItemsPerUnit = 16;
 constexpr int kRowCap = 64;      // rows (sum of ranks) per unit; max rank 64 on this path
 constexpr int kTokCap = 8;       // token slots per unit
+constexpr int kItemTokCap = 4;   // tokens per item (larger segments are chunked)
 constexpr int kVCap = 512;       // v entries per unit
 constexpr int kConsumerWarps = 8;
 constexpr int kThreads = (kConsumerWarps + 2) * 32;  // + streamer warp + resolver warp
@@ -83,6 +84,7 @@ struct LoraParams {
     int32_t a_row_pages[4];       // pages per stored A row
     int32_t ns;                   // ring slots
     int32_t l2_prefetch;          // resolver pulls each unit's pages into L2 ahead of the ring
+    int32_t dbg;                  // debug: bit0 skip shrink math, bit1 skip expand math
     const void* x;
     int64_t ldx;
     void* y[4];
