@@ -108,55 +108,38 @@ uint64_t splitmix64(uint64_t& st) {
 
 int esize_of(slora_dtype d) { return d == SLORA_F32 ? 4 : 2; }
 
-// Kernel configuration for one (mode, K, D).  C = the smallest split (cluster
-// size) whose per-CTA slices are whole 16-byte vectors and at most 4 KB (one
-// warp's worth of 16-byte vectors per slice row x 8 warps), so the producer
-// streams the largest slices and the most SMs stay usable (small clusters
-// pack GPCs best).  SLORA_SPLIT overrides.  ns = ring slots filling smem.
+// Kernel configuration for one (mode, K, D): shrink rows are whole stored A
+// rows (K elements, <= one ring slot); expand pieces cover `dchunk` output
+// columns (<= 256 16-byte vectors: one per consumer thread; measured: bulk
+// copies of >= 2 KB stream at full rate).  ns = ring slots filling smem.
+// SLORA_DCHUNK overrides the expand width.
 KernelCfg make_kernel_cfg(int mode, int64_t K, int64_t D, int64_t P, int es, int dtype) {
-
+    (void)P;
     KernelCfg k;
     k.mode = mode;
     k.K = K;
     k.D = D;
+    if (mode != kExpand && (K * es > kSlotBytes || (K * es) % 16)) return k;
     static int forced = [] {
-        const char* s = getenv("SLORA_SPLIT");
+        const char* s = getenv("SLORA_DCHUNK");
         return s ? atoi(s) : 0;
     }();
-    auto valid = [&](int C) {
-        if (mode != kExpand && (K % C || ((K / C) * es) % 16 || (K / C) * es > 4096)) return false;
-        if (mode != kExpand)
-            for (int c = 0; c < C; ++c) {  // pages one CTA's K slice spans
-                const int64_t k0 = c * (K / C), k1 = k0 + K / C - 1;
-                if (k1 / P - k0 / P + 1 > kMaxChunks) return false;
-            }
-        if (mode != kShrink && (D % C || ((D / C) * es) % 16 || (D / C) * es > 4096)) return false;
-        return true;
-    };
-    // prefer the largest split whose slices stay >= 2 KB: bulk copies of 2 KB
-    // and up stream at full HBM rate (measured), and more CTAs per unit
-    // spread few units over more SMs
-    auto big = [&](int C) {
-        return (mode == kExpand || (K / C) * es >= 2048) && (mode == kShrink || (D / C) * es >= 2048);
-    };
-    int C = 0;
-    if (forced > 0 && forced <= 16 && valid(forced)) C = forced;
-    for (int c = 16; c >= 1 && !C; --c)
-        if (valid(c) && big(c)) C = c;
-    for (int c = 1; c <= 16 && !C; ++c)
-        if (valid(c)) C = c;
-    if (!C) return k;
-    k.C = C;
+    if (mode != kShrink) {
+        int64_t dc = std::min<int64_t>(D, 4096 / es * 1);  // <= 4 KB per B row slice
+        if (forced > 0 && D % forced == 0 && (forced * es) % 16 == 0 && forced * es <= kSlotBytes) dc = forced;
+        while (dc > 1 && (D % dc || (dc * es) % 16)) --dc;
+        if ((dc * es) % 16 || dc / (16 / es) > kConsumerWarps * 32) return k;
+        k.dchunk = dc;
+    }
     const size_t budget = size_t(227) * 1024;
-    const size_t base = lora_smem_bytes(mode, C, K, D, 0, es);
-    const size_t per_slot = lora_smem_bytes(mode, C, K, D, 1, es) - base;
-    int ns = int((budget - base) / per_slot);
+    const size_t base = lora_smem_bytes(mode, K, k.dchunk, 0, es);
+    int ns = int((budget - base) / kSlotBytes);
     ns = std::min(ns, kMaxSlots);
     if (ns < 2) return k;
     k.ns = ns;
-    k.smem = lora_smem_bytes(mode, C, K, D, ns, es);
-    k.n_clusters = lora_max_clusters(mode, dtype, C, k.smem);
-    k.ok = k.n_clusters > 0;
+    k.smem = lora_smem_bytes(mode, K, k.dchunk, ns, es);
+    k.grid = lora_max_ctas(mode, dtype, k.smem);
+    k.ok = k.grid > 0;
     return k;
 }
 }  // namespace
@@ -185,6 +168,13 @@ struct slora_pool {
     // 2 shrink o (K=H/N), 3 expand (D=H/N)
     KernelCfg kcfg[4];
     long long* trace_dev = nullptr;   // SLORA_TRACE=1: kernel event timestamps
+    // rotating per-launch slots: ticket/exit/item-done counters (zeroed, and
+    // re-zeroed by each launch's last CTA) and the fused v workspace
+    int32_t* sync_dev = nullptr;
+    int64_t sync_stride = 0;          // ints per slot
+    float* ws_dev = nullptr;
+    int64_t ws_stride = 0;            // floats per slot
+    uint64_t launch_seq = 0;
 
     int64_t free_pages() const { return int64_t(free_stack.size()); }
     int N() const { return cfg.tp_size; }
@@ -211,16 +201,20 @@ struct slora_batch {
     std::vector<DevSeg> segs;
     std::vector<const int32_t*> seg_tab;  // device page table of each segment's adapter
     std::vector<int32_t> tok_idx;
-    std::vector<DevUnit> units[5];
-    std::vector<DevItem> items[5];
-    // LPT schedules: [kernel cfg][nproj] -> per-cluster unit lists
-    std::vector<int32_t> sched_off[4][5], sched[4][5];
-    // device descriptor blob
-    size_t off_segs = 0, off_tok = 0, off_units[5] = {}, off_items[5] = {};
-    size_t off_sched_off[4][5] = {}, off_sched[4][5] = {};
-    size_t blob_cap = 0;
-    void* blob_host = nullptr;
-    void* blob_dev = nullptr;
+    // per (kernel cfg, nproj) work descriptors, built on first use after a
+    // prepare and uploaded into the batch's device arena
+    struct Call {
+        bool built = false;
+        uint32_t mask = 0;
+        std::vector<DevItem> items;
+        std::vector<DevPiece> pieces;
+        size_t off_items = 0, off_pieces = 0;
+    } calls[4][5];
+    size_t off_tok = 0;
+    // device arena (bump allocated per prepare) + its pinned staging mirror
+    size_t arena_cap = 0, arena_used = 0;
+    void* arena_host = nullptr;
+    void* arena_dev = nullptr;
     cudaEvent_t upload_ev = nullptr;
     bool upload_pending = false;
 };
@@ -327,6 +321,9 @@ extern "C" slora_status slora_pool_destroy(slora_pool_t p) {
             cudaEventDestroy(p->stage_ev[b]);
         }
         cudaEventDestroy(p->release_ev);
+        if (p->sync_dev) cudaFree(p->sync_dev);
+        if (p->ws_dev) cudaFree(p->ws_dev);
+        if (p->trace_dev) cudaFree(p->trace_dev);
     }
     delete p;
     return ok();
@@ -468,7 +465,7 @@ extern "C" slora_status slora_adapter_load(slora_pool_t p, int64_t id, int32_t r
                                            float scale, void* stream, int32_t* slot_out) {
     if (check_pool(p)) return SLORA_ERR_INVALID_ARG;
     if (rank < 1) return fail(SLORA_ERR_INVALID_ARG, "rank < 1");
-    if (rank > kRowCap) return fail(SLORA_ERR_SHAPE, "rank %d > %d (max rank of the MBGMV path)", rank, kRowCap);
+    if (rank > kMaxRank) return fail(SLORA_ERR_SHAPE, "rank %d > %d (max rank of the MBGMV path)", rank, kMaxRank);
     if (rank % p->N()) return fail(SLORA_ERR_INDIVISIBLE, "rank %d %% tp_size %d", rank, p->N());
     if (p->dev && !host_w) return fail(SLORA_ERR_INVALID_ARG, "host_w is NULL");
     if (!p->dev && host_w) return fail(SLORA_ERR_NO_DEVICE, "bookkeeping-only pool takes host_w = NULL");
@@ -648,113 +645,6 @@ extern "C" slora_status slora_gather_pages(slora_pool_t p, const int32_t* pages,
 }
 
 // ------------------------------------------------------------------- batch
-namespace {
-// Items = (segment x projection x token chunk); units = items packed by
-// first-fit decreasing on rank under the kernel's caps (kRowCap rows,
-// kTokCap token slots, kVCap v entries, kMaxItemsPerUnit items): an r = 64
-// item fills a unit alone, eight r = 8 items share one -- rank-heterogeneous
-// balancing without padding to a maximum rank.
-void build_units(slora_batch* b, int nproj) {
-    auto& units = b->units[nproj];
-    auto& items = b->items[nproj];
-    units.clear();
-    items.clear();
-    struct It { DevItem it; int rank; };
-    std::vector<It> all;
-    for (int si = 0; si < int(b->segs.size()); ++si) {
-        const DevSeg& s = b->segs[size_t(si)];
-        // at most kItemTokCap tokens per item: a Zipf-head adapter with many
-        // decode tokens is split into several items (its pages are re-read,
-        // but the FMA work spreads over clusters instead of one straggler)
-        const int tmax = std::max(1, std::min(std::min(kTokCap, kItemTokCap), kVCap / s.rank));
-        for (int pi = 0; pi < nproj; ++pi)
-            for (int t0 = 0; t0 < s.n_tok; t0 += tmax) {
-                DevItem it{};
-                it.tab = b->seg_tab.empty() ? nullptr : b->seg_tab[size_t(si)];
-                it.vrow = s.vrow_off + int64_t(t0) * s.rank;
-                it.rank = s.rank;
-                it.seg = si;
-                it.pi = pi;
-                it.t0 = t0;
-                it.nt = std::min(tmax, s.n_tok - t0);
-                it.tok_off = s.tok_off + t0;
-                it.scale = s.scale;
-                all.push_back({it, s.rank});
-            }
-    }
-    std::stable_sort(all.begin(), all.end(), [](const It& a, const It& c) { return a.rank > c.rank; });
-    struct Bin { std::vector<DevItem> its; int rows = 0, toks = 0, v = 0; };
-    std::vector<Bin> bins;
-    for (const It& x : all) {
-        const int r = x.rank, nt = x.it.nt;
-        Bin* target = nullptr;
-        for (Bin& bn : bins)
-            if (bn.rows + r <= kRowCap && bn.toks + nt <= kTokCap && bn.v + nt * r <= kVCap &&
-                int(bn.its.size()) < kMaxItemsPerUnit) {
-                target = &bn;
-                break;
-            }
-        if (!target) {
-            bins.emplace_back();
-            target = &bins.back();
-        }
-        DevItem it = x.it;
-        it.row_off = target->rows;
-        it.tok_slot = target->toks;
-        it.v_off = target->v;
-        target->rows += r;
-        target->toks += nt;
-        target->v += nt * r;
-        target->its.push_back(it);
-    }
-    for (Bin& bn : bins) {
-        DevUnit u{};
-        u.item_begin = int32_t(items.size());
-        u.n_items = int32_t(bn.its.size());
-        u.rows = bn.rows;
-        u.toks = bn.toks;
-        u.ventries = bn.v;
-        for (auto& it : bn.its) items.push_back(it);
-        units.push_back(u);
-    }
-}
-
-// LPT static schedule of units over the kernel's persistent clusters: units
-// by decreasing cost, each to the least-loaded cluster.  Cost = bytes one
-// cluster CTA streams for the unit + a fixed per-unit overhead.
-void build_schedule(slora_batch* b, const KernelCfg& k, int es, int nproj, std::vector<int32_t>& off,
-                    std::vector<int32_t>& sched) {
-    off.clear();
-    sched.clear();
-    const auto& units = b->units[nproj];
-    if (!k.ok || units.empty()) {
-        off.assign(1, 0);
-        return;
-    }
-    const int G = std::max(1, std::min<int>(k.n_clusters, int(units.size())));
-    const double KSb = k.mode == kExpand ? 0.0 : double(k.K / k.C) * es;
-    const double DSb = k.mode == kShrink ? 0.0 : double(k.D / k.C) * es;
-    std::vector<std::pair<double, int>> cost;
-    for (int u = 0; u < int(units.size()); ++u) {
-        const DevUnit& U = units[size_t(u)];
-        cost.push_back({U.rows * (KSb + DSb) + U.toks * KSb + 8192.0, u});
-    }
-    std::stable_sort(cost.begin(), cost.end(), [](auto& a, auto& c) { return a.first > c.first; });
-    std::vector<double> load(size_t(G), 0.0);
-    std::vector<std::vector<int32_t>> lists(static_cast<size_t>(G));
-    for (auto& cu : cost) {
-        size_t g = size_t(std::min_element(load.begin(), load.end()) - load.begin());
-        load[g] += cu.first;
-        lists[g].push_back(cu.second);
-    }
-    off.push_back(0);
-    for (auto& l : lists) {
-        for (int32_t u : l) sched.push_back(u);
-        off.push_back(int32_t(sched.size()));
-    }
-}
-}  // namespace
-
 extern "C" slora_status slora_batch_create(slora_pool_t p, slora_batch_t* out) {
     if (check_pool(p) || !out) return fail(SLORA_ERR_INVALID_ARG, "null argument");
     slora_batch* b = new slora_batch();
@@ -774,13 +664,88 @@ extern "C" slora_status slora_batch_destroy(slora_batch_t b) {
     if (!b) return fail(SLORA_ERR_INVALID_ARG, "null batch");
     if (b->pool->dev) {
         if (b->upload_pending) cudaEventSynchronize(b->upload_ev);
-        if (b->blob_dev) cudaFree(b->blob_dev);
-        if (b->blob_host) cudaFreeHost(b->blob_host);
+        if (b->arena_dev) cudaFree(b->arena_dev);
+        if (b->arena_host) cudaFreeHost(b->arena_host);
         cudaEventDestroy(b->upload_ev);
     }
     delete b;
     return ok();
 }
+
+namespace {
+// Copy `n` bytes into the batch's pinned arena and enqueue their H2D copy into
+// the device arena; returns the device offset.  The arena is bump-allocated
+// per prepare and sized by prepare (grown there, never mid-batch).
+size_t arena_put(slora_batch* b, const void* src, size_t n, cudaStream_t s, cudaError_t& err) {
+    const size_t off = b->arena_used;
+    const size_t n_al = (n + 255) & ~size_t(255);
+    if (off + n_al > b->arena_cap) {
+        err = cudaErrorMemoryAllocation;
+        return 0;
+    }
+    if (n) {
+        memcpy(static_cast<uint8_t*>(b->arena_host) + off, src, n);
+        err = cudaMemcpyAsync(static_cast<uint8_t*>(b->arena_dev) + off, static_cast<uint8_t*>(b->arena_host) + off,
+                              n, cudaMemcpyHostToDevice, s);
+        if (!err) err = cudaEventRecord(b->upload_ev, s);
+        b->upload_pending = true;
+    }
+    b->arena_used = off + n_al;
+    return off;
+}
+
+// Items = (segment x projection of the call x token chunk of <= kItemTokCap
+// tokens); pieces: each item's stored A rows in groups of kShrinkRows (shrink,
+// full K), and its output columns in chunks of kc.dchunk (expand).  Pieces are
+// ordered shrink-before-expand, larger items first (the ticket counter hands
+// them out in this order).
+void build_call(slora_batch* b, const KernelCfg& k, int N, int nproj, uint32_t mask, slora_batch::Call& call) {
+    call.items.clear();
+    call.pieces.clear();
+    int proj_ids[4], np = 0;
+    for (int pj = 0; pj < 4; ++pj)
+        if (mask & (1u << pj)) proj_ids[np++] = pj;
+    (void)nproj;
+    struct Ord { int item; int64_t cost; };
+    std::vector<Ord> order;
+    for (int si = 0; si < int(b->segs.size()); ++si) {
+        const DevSeg& s = b->segs[size_t(si)];
+        for (int pi = 0; pi < np; ++pi) {
+            const int proj = proj_ids[pi];
+            const int div = (k.mode == kExpand) ? 1 : ((proj < 3) ? N : 1);
+            const int ra = s.rank / div;
+            for (int t0 = 0; t0 < s.n_tok; t0 += kItemTokCap) {
+                DevItem it{};
+                it.tab = b->seg_tab.empty() ? nullptr : b->seg_tab[size_t(si)];
+                it.vrow = s.vrow_off + int64_t(t0) * s.rank;
+                it.rank = s.rank;
+                it.seg = si;
+                it.pi = pi;
+                it.t0 = t0;
+                it.nt = std::min(kItemTokCap, s.n_tok - t0);
+                it.tok_off = s.tok_off + t0;
+                it.scale = s.scale;
+                it.n_sp = (k.mode == kExpand) ? 0 : (ra + kShrinkRows - 1) / kShrinkRows;
+                order.push_back({int(call.items.size()), int64_t(s.rank) * 1000 + it.nt});
+                call.items.push_back(it);
+            }
+        }
+    }
+    std::stable_sort(order.begin(), order.end(), [](const Ord& a, const Ord& c) { return a.cost > c.cost; });
+    if (k.mode != kExpand)
+        for (const Ord& o : order) {
+            const DevItem& it = call.items[size_t(o.item)];
+            const int proj = proj_ids[it.pi];
+            const int ra = it.rank / ((k.mode == kExpand) ? 1 : ((proj < 3) ? N : 1));
+            for (int r0 = 0; r0 < ra; r0 += kShrinkRows)
+                call.pieces.push_back({kPieceS, o.item, r0, std::min(kShrinkRows, ra - r0)});
+        }
+    if (k.mode != kShrink)
+        for (const Ord& o : order)
+            for (int64_t c0 = 0; c0 < k.D; c0 += k.dchunk)
+                call.pieces.push_back({kPieceE, o.item, int32_t(c0), int32_t(std::min<int64_t>(k.dchunk, k.D - c0))});
+}
+}  // namespace
 
 extern "C" slora_status slora_batch_prepare(slora_batch_t b, const int64_t* tok_adapter, int32_t T, void* stream) {
     if (!b) return fail(SLORA_ERR_INVALID_ARG, "null batch");
@@ -832,65 +797,57 @@ extern "C" slora_status slora_batch_prepare(slora_batch_t b, const int64_t* tok_
         b->segs.push_back(sg);
         b->seg_tab.push_back(ad.dev_tab);
     }
-    for (int np = 1; np <= 4; ++np) build_units(b, np);
-    for (int kc = 0; kc < 4; ++kc)
-        for (int np = 1; np <= 4; ++np) build_schedule(b, p->kcfg[kc], p->es, np, b->sched_off[kc][np], b->sched[kc][np]);
+    for (auto& row : b->calls)
+        for (auto& c : row) c.built = false;
     b->epoch = p->epoch;
     b->prepared = true;
-    if (!p->dev) return ok();
-
-    // ---- upload: [segs][tok_idx][units/items per nproj][schedules per cfg x nproj]
-    auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
-    size_t off = 0;
-    b->off_segs = off;
-    off = al(off + b->segs.size() * sizeof(DevSeg));
-    b->off_tok = off;
-    off = al(off + b->tok_idx.size() * sizeof(int32_t));
-    for (int np = 1; np <= 4; ++np) {
-        b->off_units[np] = off;
-        off = al(off + b->units[np].size() * sizeof(DevUnit));
-        b->off_items[np] = off;
-        off = al(off + b->items[np].size() * sizeof(DevItem));
+    if (!p->dev) {
+        // bookkeeping pools still build the descriptors (tested on CPU)
+        for (int np = 1; np <= 4; ++np) build_call(b, p->kcfg[0], p->N(), np, (1u << np) - 1, b->calls[0][np]);
+        return ok();
     }
-    for (int kc = 0; kc < 4; ++kc)
-        for (int np = 1; np <= 4; ++np) {
-            b->off_sched_off[kc][np] = off;
-            off = al(off + b->sched_off[kc][np].size() * sizeof(int32_t));
-            b->off_sched[kc][np] = off;
-            off = al(off + b->sched[kc][np].size() * sizeof(int32_t));
-        }
-    const size_t need = std::max<size_t>(off, 256);
+    // ---- device arena: tok_idx now, call descriptors on first use.  Sized
+    // for every call this prepare can see (items <= segs*4*chunks).
+    int64_t chunks = 0;
+    for (const DevSeg& s : b->segs) chunks += (s.n_tok + kItemTokCap - 1) / kItemTokCap;
+    const int64_t max_items = 4 * chunks;
+    const int64_t max_pieces_per_item = (kMaxRank + kShrinkRows - 1) / kShrinkRows + 64;
+    const size_t need = 256 + size_t(T) * 4 + 16 * (256 + size_t(max_items) * sizeof(DevItem) +
+                                                   size_t(max_items * max_pieces_per_item) * sizeof(DevPiece));
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     CUDA_TRY(cudaSetDevice(p->cfg.device));
-    if (b->upload_pending) CUDA_TRY(cudaEventSynchronize(b->upload_ev));  // pinned blob free again
-    if (need > b->blob_cap) {
-        if (b->blob_host) CUDA_TRY(cudaFreeHost(b->blob_host));
-        if (b->blob_dev) CUDA_TRY(cudaFreeAsync(b->blob_dev, s));
-        b->blob_host = nullptr;
-        b->blob_dev = nullptr;
+    if (b->upload_pending) CUDA_TRY(cudaEventSynchronize(b->upload_ev));  // pinned arena free again
+    b->upload_pending = false;
+    if (need > b->arena_cap) {
+        if (b->arena_host) CUDA_TRY(cudaFreeHost(b->arena_host));
+        if (b->arena_dev) CUDA_TRY(cudaFreeAsync(b->arena_dev, s));
+        b->arena_host = nullptr;
+        b->arena_dev = nullptr;
         const size_t cap = need * 2;
-        CUDA_TRY(cudaHostAlloc(&b->blob_host, cap, cudaHostAllocDefault));
-        CUDA_TRY(cudaMallocAsync(&b->blob_dev, cap, s));
-        b->blob_cap = cap;
+        CUDA_TRY(cudaHostAlloc(&b->arena_host, cap, cudaHostAllocDefault));
+        CUDA_TRY(cudaMallocAsync(&b->arena_dev, cap, s));
+        b->arena_cap = cap;
     }
-    uint8_t* h = static_cast<uint8_t*>(b->blob_host);
-    auto put = [&](size_t o, const void* src, size_t n) {
-        if (n) memcpy(h + o, src, n);
-    };
-    put(b->off_segs, b->segs.data(), b->segs.size() * sizeof(DevSeg));
-    put(b->off_tok, b->tok_idx.data(), b->tok_idx.size() * sizeof(int32_t));
-    for (int np = 1; np <= 4; ++np) {
-        put(b->off_units[np], b->units[np].data(), b->units[np].size() * sizeof(DevUnit));
-        put(b->off_items[np], b->items[np].data(), b->items[np].size() * sizeof(DevItem));
+    b->arena_used = 0;
+    cudaError_t e = cudaSuccess;
+    b->off_tok = arena_put(b, b->tok_idx.data(), b->tok_idx.size() * sizeof(int32_t), s, e);
+    if (e) return fail(SLORA_ERR_CUDA, "batch upload: %s", cudaGetErrorString(e));
+    // per-launch sync slots and fused workspace, sized for this batch
+    const int64_t sync_need = 2 + max_items + 32;
+    const int64_t ws_need = 4 * b->NR + 64;
+    if (sync_need > p->sync_stride) {
+        if (p->sync_dev) CUDA_TRY(cudaFreeAsync(p->sync_dev, s));
+        const int64_t st = sync_need * 2;
+        CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&p->sync_dev), sizeof(int32_t) * st * kLaunchSlots, s));
+        CUDA_TRY(cudaMemsetAsync(p->sync_dev, 0, sizeof(int32_t) * st * kLaunchSlots, s));
+        p->sync_stride = st;
     }
-    for (int kc = 0; kc < 4; ++kc)
-        for (int np = 1; np <= 4; ++np) {
-            put(b->off_sched_off[kc][np], b->sched_off[kc][np].data(), b->sched_off[kc][np].size() * sizeof(int32_t));
-            put(b->off_sched[kc][np], b->sched[kc][np].data(), b->sched[kc][np].size() * sizeof(int32_t));
-        }
-    CUDA_TRY(cudaMemcpyAsync(b->blob_dev, b->blob_host, need, cudaMemcpyHostToDevice, s));
-    CUDA_TRY(cudaEventRecord(b->upload_ev, s));
-    b->upload_pending = true;
+    if (ws_need > p->ws_stride) {
+        if (p->ws_dev) CUDA_TRY(cudaFreeAsync(p->ws_dev, s));
+        const int64_t st = ws_need * 2;
+        CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&p->ws_dev), sizeof(float) * st * kLaunchSlots, s));
+        p->ws_stride = st;
+    }
     return ok();
 }
 
@@ -922,37 +879,50 @@ bool aligned16(const void* ptr, int64_t ld, int es) {
     return !(reinterpret_cast<uintptr_t>(ptr) & 15) && (ld * es) % 16 == 0;
 }
 
-void fill_common(slora_pool* p, slora_batch* b, int kc, int32_t layer, uint32_t mask, LoraParams& q) {
-    memset(&q, 0, sizeof(q));
+// Resolve (building + uploading on first use) the call descriptor and fill the
+// launch parameters common to all modes.
+slora_status prepare_call(slora_pool* p, slora_batch* b, int kc, int32_t layer, uint32_t mask, void* stream,
+                          LoraParams& q) {
     const KernelCfg& k = p->kcfg[kc];
-    q.pool = p->cfg.device_buffer;
-    q.page_elems = p->P;
-    q.slot_tab = p->slot_tab_dev;
-    uint8_t* base = static_cast<uint8_t*>(b->blob_dev);
-    q.segs = reinterpret_cast<const DevSeg*>(base + b->off_segs);
-    q.tok_idx = reinterpret_cast<const int32_t*>(base + b->off_tok);
+    if (!k.ok) return fail(SLORA_ERR_SHAPE, "no valid kernel configuration for K=%lld D=%lld", (long long)k.K,
+                           (long long)k.D);
+    memset(&q, 0, sizeof(q));
     int np = 0;
     for (int pj = 0; pj < 4; ++pj)
         if (mask & (1u << pj)) q.proj_ids[np++] = pj;
     q.nproj = np;
-    q.units = reinterpret_cast<const DevUnit*>(base + b->off_units[np]);
-    q.items = reinterpret_cast<const DevItem*>(base + b->off_items[np]);
-    q.sched_off = reinterpret_cast<const int32_t*>(base + b->off_sched_off[kc][np]);
-    q.sched = reinterpret_cast<const int32_t*>(base + b->off_sched[kc][np]);
-    q.n_clusters = int32_t(b->sched_off[kc][np].size()) - 1;
+    // descriptors depend on the mask only through np and which projections
+    // are q/k/v vs o (the stored-row divisor under TP); key by (kc, np) and
+    // rebuild when the o-ness of the mask differs
+    slora_batch::Call& call = b->calls[kc][np];
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (!call.built || call.mask != mask) {
+        build_call(b, k, p->N(), np, mask, call);
+        cudaError_t e = cudaSuccess;
+        call.off_items = arena_put(b, call.items.data(), call.items.size() * sizeof(DevItem), s, e);
+        if (!e) call.off_pieces = arena_put(b, call.pieces.data(), call.pieces.size() * sizeof(DevPiece), s, e);
+        if (e) return fail(SLORA_ERR_CUDA, "call descriptor upload: %s", cudaGetErrorString(e));
+        call.built = true;
+        call.mask = mask;
+    }
+    uint8_t* base = static_cast<uint8_t*>(b->arena_dev);
+    q.pool = p->cfg.device_buffer;
+    q.page_elems = p->P;
+    q.tok_idx = reinterpret_cast<const int32_t*>(base + b->off_tok);
+    q.items = reinterpret_cast<const DevItem*>(base + call.off_items);
+    q.pieces = reinterpret_cast<const DevPiece*>(base + call.off_pieces);
+    q.n_pieces = int32_t(call.pieces.size());
+    q.n_items = int32_t(call.items.size());
+    if (q.n_items + 2 > p->sync_stride) return fail(SLORA_ERR_SHAPE, "sync area too small");
+    const uint64_t slot = p->launch_seq++ % kLaunchSlots;
+    q.sync = p->sync_dev + int64_t(slot) * p->sync_stride;
     q.layer = layer;
-    q.C = k.C;
     q.K = int32_t(k.K);
     q.D = int32_t(k.D);
     q.ns = k.ns;
-    static const int l2pf = [] {
-        const char* s = getenv("SLORA_L2PF");
-        return s ? atoi(s) : 0;
-    }();
-    q.l2_prefetch = l2pf;
     static const int dbg = [] {
-        const char* s = getenv("SLORA_DBG");
-        return s ? atoi(s) : 0;
+        const char* e = getenv("SLORA_DBG");
+        return e ? atoi(e) : 0;
     }();
     q.dbg = dbg;
     q.NR = b->NR;
@@ -961,16 +931,16 @@ void fill_common(slora_pool* p, slora_batch* b, int kc, int32_t layer, uint32_t 
         q.a_div[pj] = (pj < 3) ? N : 1;
         q.a_row_pages[pj] = (pj < 3) ? N : 1;
     }
+    if (k.mode == kFused) q.v = p->ws_dev + int64_t(slot) * p->ws_stride;
+    q.trace = p->trace_dev;
+    return SLORA_OK;
 }
 
 slora_status launch(slora_pool* p, int kc, LoraParams& q, void* stream) {
     const KernelCfg& k = p->kcfg[kc];
-    if (!k.ok) return fail(SLORA_ERR_SHAPE, "no valid kernel configuration for K=%lld D=%lld", (long long)k.K,
-                           (long long)k.D);
     CUDA_TRY(cudaSetDevice(p->cfg.device));
     const int dt = p->cfg.dtype == SLORA_F32 ? kF32 : (p->cfg.dtype == SLORA_F16 ? kF16 : kBF16);
-    q.trace = p->trace_dev;
-    CUDA_TRY(launch_lora(q, k.mode, dt, static_cast<cudaStream_t>(stream), k.smem));
+    CUDA_TRY(launch_lora(q, k.mode, dt, k.grid, static_cast<cudaStream_t>(stream), k.smem));
     return ok();
 }
 }  // namespace
@@ -989,7 +959,8 @@ extern "C" slora_status slora_lora_apply(slora_pool_t p, slora_batch_t b, int32_
             if (!y[pj] || !aligned16(y[pj], ldy[pj], p->es) || ldy[pj] < p->cfg.hidden)
                 return fail(SLORA_ERR_SHAPE, "y[%d] alignment/stride", pj);
     LoraParams q;
-    fill_common(p, b, 0, layer, mask, q);
+    st = prepare_call(p, b, 0, layer, mask, stream, q);
+    if (st) return st;
     q.x = x;
     q.ldx = ldx;
     for (int pj = 0; pj < 4; ++pj) {
@@ -1023,10 +994,11 @@ extern "C" slora_status slora_lora_shrink(slora_pool_t p, slora_batch_t b, int32
     if (!x || !v) return fail(SLORA_ERR_INVALID_ARG, "null x/v");
     if (!aligned16(x, ldx, p->es) || ldx < K) return fail(SLORA_ERR_SHAPE, "x alignment/stride");
     LoraParams q;
-    fill_common(p, b, kc, layer, mask, q);
+    st = prepare_call(p, b, kc, layer, mask, stream, q);
+    if (st) return st;
     q.x = x;
     q.ldx = ldx;
-    q.v_out = v;
+    q.v = v;
     return launch(p, kc, q, stream);
 }
 
@@ -1045,7 +1017,8 @@ extern "C" slora_status slora_lora_expand(slora_pool_t p, slora_batch_t b, int32
             if (!y[pj] || !aligned16(y[pj], ldy[pj], p->es) || ldy[pj] < p->P)
                 return fail(SLORA_ERR_SHAPE, "y[%d] alignment/stride", pj);
     LoraParams q;
-    fill_common(p, b, 3, layer, mask, q);
+    st = prepare_call(p, b, 3, layer, mask, stream, q);
+    if (st) return st;
     q.v_in = v;
     q.v_blocks = v_blocks;
     for (int pj = 0; pj < 4; ++pj) {

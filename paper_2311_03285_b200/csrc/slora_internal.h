@@ -11,7 +11,7 @@ namespace slora {
 // One segment = the tokens of one adapter in a batch (the kernels
 // "gather adapter weights with different ranks from the memory pool").
 struct DevSeg {
-    int32_t slot;      // adapter slot -> slot_tab[slot] = its device page table
+    int32_t slot;      // adapter slot
     int32_t rank;      // r (full, unsharded rank)
     int32_t n_tok;     // tokens of this adapter in the batch
     int32_t tok_off;   // first entry in tok_idx
@@ -21,12 +21,8 @@ struct DevSeg {
 };
 static_assert(sizeof(DevSeg) == 32, "DevSeg layout");
 
-// A work item = (segment, projection index within the call's mask, token
-// chunk).  Items are packed into units (<= kRowCap A/B rows, <= kTokCap token
-// slots, <= kVCap v entries); a cluster of C CTAs processes a unit, CTA c
-// owning the c-th 1/C slice of K (shrink) and of D (expand).
-// Self-contained: the kernel resolves an item with one load (no segment or
-// slot-table indirection).
+// A work item = (segment, projection of the call, token chunk of <=
+// kItemTokCap tokens).  Self-contained: the kernel resolves it with one load.
 struct DevItem {
     const int32_t* tab;  // the adapter's device page table (layer/proj offset added in-kernel)
     int64_t vrow;      // v row offset of the chunk: segment vrow_off + t0 * rank
@@ -34,64 +30,60 @@ struct DevItem {
     int32_t pi;        // index of the projection in the call's mask order
     int32_t t0, nt;    // token chunk [t0, t0+nt) of the segment
     int32_t tok_off;   // index in tok_idx of the chunk's first token
-    int32_t tok_slot;  // first token slot within the unit
-    int32_t v_off;     // first v entry within the unit (full rank units)
-    int32_t row_off;   // first row of this item within the unit (full rank units)
+    int32_t n_sp;      // number of shrink pieces of this item (fused dependency count)
     float scale;
     int32_t seg;
-    int32_t pad[2];
+    int32_t pad[4];
 };
 static_assert(sizeof(DevItem) == 64, "DevItem layout");
 
-struct DevUnit {
-    int32_t item_begin, n_items;
-    int32_t rows, toks, ventries;  // totals (full rank units)
-    int32_t pad[3];
+// A piece = the unit of dynamic scheduling.  kind 0 (shrink): rows
+// [a, a+b) of the item's stored A rows, full K.  kind 1 (expand): all B rows,
+// output columns [a, a+b).  Tickets hand out all shrink pieces before any
+// expand piece, so an expand piece only ever waits on earlier tickets.
+struct DevPiece {
+    int32_t kind, item, a, b;
 };
-static_assert(sizeof(DevUnit) == 32, "DevUnit layout");
+static_assert(sizeof(DevPiece) == 16, "DevPiece layout");
 
-constexpr int kMaxItemsPerUnit = 16;
-constexpr int kRowCap = 64;      // rows (sum of ranks) per unit; max rank 64 on this path
-constexpr int kTokCap = 8;       // token slots per unit
 constexpr int kItemTokCap = 4;   // tokens per item (larger segments are chunked)
-constexpr int kVCap = 512;       // v entries per unit
+constexpr int kMaxRank = 64;     // max rank of the MBGMV path
+constexpr int kShrinkRows = 16;  // A rows per shrink piece
 constexpr int kConsumerWarps = 8;
 constexpr int kThreads = (kConsumerWarps + 2) * 32;  // + streamer warp + resolver warp
-constexpr int kMaxChunks = 4;    // pages one CTA's K slice of an A row may span
-constexpr int kRowsPerSlot = 8;  // page-slice rows per ring slot
-constexpr int kMaxSlots = 32;
+constexpr int kMaxChunks = 8;    // pages one stored A row spans (TP q/k/v: N)
+constexpr int kSlotBytes = 32 * 1024;  // ring slot
+constexpr int kMaxSlots = 16;
+constexpr int kLaunchSlots = 8;  // rotating per-launch counter/workspace slots
 
 enum Mode : int { kFused = 0, kShrink = 1, kExpand = 2 };
 enum DType : int { kF32 = 0, kF16 = 1, kBF16 = 2 };
+enum PieceKind : int { kPieceS = 0, kPieceE = 1, kPieceStop = 2 };
 
 struct LoraParams {
     const void* pool;             // page buffer
     int64_t page_elems;           // P
-    const int32_t* const* slot_tab;
-    const DevSeg* segs;
     const int32_t* tok_idx;
-    const DevUnit* units;
     const DevItem* items;
-    const int32_t* sched_off;     // [n_clusters + 1] per-cluster unit lists (LPT)
-    const int32_t* sched;
-    int32_t n_clusters;
+    const DevPiece* pieces;
+    int32_t n_pieces;
+    int32_t n_items;
+    int32_t* sync;                // this launch's slot: [0] tickets, [1] exits, [2..] item done counts
     int32_t nproj;
     int32_t proj_ids[4];
     int32_t layer;
-    int32_t C;                    // K/D split = cluster size (fused / shrink)
-    int32_t K, D;                 // A-row length, B-row length (elements)
+    int32_t K, D;                 // stored A-row length, B-row length (elements)
     int32_t a_div[4];             // A rank columns stored = r / a_div[p]
     int32_t a_row_pages[4];       // pages per stored A row
     int32_t ns;                   // ring slots
-    int32_t l2_prefetch;          // resolver pulls each unit's pages into L2 ahead of the ring
     int32_t dbg;                  // debug: bit0 skip shrink math, bit1 skip expand math
     const void* x;
     int64_t ldx;
     void* y[4];
     int64_t ldy[4];
-    long long* trace;            // debug: per-CTA event timestamps (nullptr = off)
-    float* v_out;
-    const float* v_in;
+    long long* trace;             // debug: per-CTA event timestamps (nullptr = off)
+    float* v;                     // shrink output / fused workspace (C-ABI v layout, div as stored)
+    const float* v_in;            // expand input
     int32_t v_blocks;
     int64_t NR;                   // sum over adapted tokens of rank
 };
@@ -99,18 +91,18 @@ struct LoraParams {
 // Per-launch kernel configuration (chosen on the host, see api.cpp).
 struct KernelCfg {
     int mode = 0;
-    int C = 0, ns = 0;
+    int ns = 0;
     int64_t K = 0, D = 0;
+    int64_t dchunk = 0;           // expand piece width (elements)
     size_t smem = 0;
-    int n_clusters = 0;           // persistent clusters (grid = n_clusters * C)
+    int grid = 0;                 // persistent CTAs
     bool ok = false;
 };
 
 // smem bytes for a launch (host and device agree via smem_layout in kernels.cu)
-size_t lora_smem_bytes(int mode, int C, int64_t K, int64_t D, int ns, int esize);
-// number of persistent clusters that can be co-resident (occupancy API)
-int lora_max_clusters(int mode, int dtype, int C, size_t smem);
-cudaError_t launch_lora(const LoraParams& p, int mode, int dtype, cudaStream_t s, size_t smem);
+size_t lora_smem_bytes(int mode, int64_t K, int64_t dchunk, int ns, int esize);
+int lora_max_ctas(int mode, int dtype, size_t smem);
+cudaError_t launch_lora(const LoraParams& p, int mode, int dtype, int grid, cudaStream_t s, size_t smem);
 cudaError_t configure_lora_kernels(int device);
 
 // Adapter scatter: jobs describe how rows of a packed staging buffer land in
