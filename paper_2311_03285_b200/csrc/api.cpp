@@ -131,7 +131,7 @@ KernelCfg make_kernel_cfg(int mode, int64_t K, int64_t D, int64_t P, int es, int
         if ((dc * es) % 16 || dc / (16 / es) > kConsumerWarps * 32) return k;
         k.dchunk = dc;
     }
-    const size_t budget = size_t(227) * 1024;
+    const size_t budget = size_t(226) * 1024;
     const size_t base = lora_smem_bytes(mode, K, k.dchunk, 0, es);
     int ns = int((budget - base) / kSlotBytes);
     ns = std::min(ns, kMaxSlots);
