@@ -291,25 +291,29 @@ __device__ __forceinline__ void expand_piece(const LoraParams& p, const PieceMet
             if (own >> t & 1u)
                 yv[kPrefetchY ? t : 0] = *reinterpret_cast<const uint4*>(y + int64_t(M.tok[t]) * ldy + col);
     }
-    for (int j = 0; j < M.r; ++j) {
-        const int q = j % rps;
-        if (q == 0) {
-            if (j > 0) {
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&empty[rg.slot]);
-                rg.advance(ns);
-            }
-            mbar_wait(&full[rg.slot], rg.lap & 1);
+    const int r = M.r;
+    const uint32_t rowv = rowb / 16;  // 16-byte vectors per row slice
+    for (int j0 = 0; j0 < r; j0 += rps) {
+        if (j0 > 0) {
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[rg.slot]);
+            rg.advance(ns);
         }
+        mbar_wait(&full[rg.slot], rg.lap & 1);
         if (active) {
-            float b[VE];
-            V::to_f32(reinterpret_cast<const uint4*>(ring + size_t(rg.slot) * kSlotBytes + size_t(q) * rowb)[cv], b);
+            const uint4* sl = reinterpret_cast<const uint4*>(ring + size_t(rg.slot) * kSlotBytes) + cv;
+            const int nrow = min(rps, r - j0);
+            for (int q = 0; q < nrow; ++q) {
+                float b[VE];
+                V::to_f32(sl[q * rowv], b);
+                const float* vc = vbuf + j0 + q;
 #pragma unroll
-            for (int t = 0; t < NT; ++t) {
-                if (own >> t & 1u) {
-                    const float vj = vbuf[t * M.r + j];
+                for (int t = 0; t < NT; ++t) {
+                    if (own >> t & 1u) {
+                        const float vj = vc[t * r];
 #pragma unroll
-                    for (int e = 0; e < VE; ++e) acc[t][e] = fmaf(vj, b[e], acc[t][e]);
+                        for (int e = 0; e < VE; ++e) acc[t][e] = fmaf(vj, b[e], acc[t][e]);
+                    }
                 }
             }
         }
@@ -423,21 +427,27 @@ __global__ void __launch_bounds__(kThreads, 1) mbgmv_kernel(const __grid_constan
                 for (int q = lane; q < it.rank; q += 32) M.pages[q] = tab[it.rank + q];
             }
             __syncwarp();
+            if (lane == 0 && i < 48) TRACE(16 + i);
+            if (lane == 0 && i < 48 && p.trace && blockIdx.x < 16) p.trace[blockIdx.x * 256 + 208 + i] = ticket;
             if (lane == 0) mbar_arrive(&mfull[ub]);
         }
-    } else if (warp == kConsumerWarps) {
-        // ============================ streamer ============================
+    } else if (warp == kConsumerWarps || warp == kConsumerWarps + 2) {
+        // ============================ streamers ===========================
+        // Two warps issue alternate ring slots (bulk-copy issue costs ~90 ns
+        // per copy per warp, measured; two issuers double the rate).
         // Adapter pages are written only by the loader's scatter kernel, which
         // never triggers its dependents early, so the first piece's pages are
         // streamed before griddepcontrol.wait; x, y and v only after it.
+        const int sid = warp == kConsumerWarps ? 0 : 1;
         Ring rg;
+        uint32_t seq = 0;  // slot sequence number (shared numbering, both warps)
         bool waited = false;
         for (int i = 0;; ++i) {
             const int ub = i & 1;
             mbar_wait(&mfull[ub], (i >> 1) & 1);
             const PieceMeta& M = meta[ub];
             if (M.kind == kPieceStop) {
-                if (lane == 0) mbar_arrive(&xfull[ub]);
+                if (lane == 0 && sid == 0) mbar_arrive(&xfull[ub]);
                 break;
             }
             const bool S = M.kind == kPieceS;
@@ -445,6 +455,11 @@ __global__ void __launch_bounds__(kThreads, 1) mbgmv_kernel(const __grid_constan
             const uint32_t rowb = S ? arow_bytes : uint32_t(M.dcols * ES);
             const int rps = S ? rps_s : kSlotBytes / int(rowb);
             auto issue_slot = [&](int base) {
+                const bool mine = (seq++ & 1u) == uint32_t(sid);
+                if (!mine) {
+                    rg.advance(ns);
+                    return;
+                }
                 const int nrow = min(rps, R - base);
                 mbar_wait(&empty[rg.slot], (rg.lap & 1) ^ 1);
                 if (lane == 0) mbar_arrive_expect_tx(&full[rg.slot], uint32_t(nrow) * rowb);
@@ -474,18 +489,21 @@ __global__ void __launch_bounds__(kThreads, 1) mbgmv_kernel(const __grid_constan
                 pdl_wait();
                 waited = true;
             }
-            if (S) {  // x rows of the item's tokens; the same arrive publishes the meta
-                if (lane == 0) mbar_arrive_expect_tx(&xfull[ub], uint32_t(M.nt) * arow_bytes);
-                __syncwarp();
-                if (lane < M.nt) {
-                    const T* x = reinterpret_cast<const T*>(p.x);
-                    bulk_g2s(xrows + (size_t(ub) * kItemTokCap + lane) * K, x + int64_t(M.tok[lane]) * p.ldx,
-                             arow_bytes, &xfull[ub]);
+            if (sid == 0) {
+                if (S) {  // x rows of the item's tokens; the same arrive publishes the meta
+                    if (lane == 0) mbar_arrive_expect_tx(&xfull[ub], uint32_t(M.nt) * arow_bytes);
+                    __syncwarp();
+                    if (lane < M.nt) {
+                        const T* x = reinterpret_cast<const T*>(p.x);
+                        bulk_g2s(xrows + (size_t(ub) * kItemTokCap + lane) * K, x + int64_t(M.tok[lane]) * p.ldx,
+                                 arow_bytes, &xfull[ub]);
+                    }
+                } else {
+                    if (lane == 0) mbar_arrive(&xfull[ub]);
                 }
-            } else {
-                if (lane == 0) mbar_arrive(&xfull[ub]);
             }
             for (int base = pre * rps; base < R; base += rps) issue_slot(base);
+            if (lane == 0 && i < 48) TRACE(160 + i);
         }
     } else {
         // ============================ consumers ===========================
@@ -500,6 +518,7 @@ __global__ void __launch_bounds__(kThreads, 1) mbgmv_kernel(const __grid_constan
             mbar_wait(&xfull[ub], (i >> 1) & 1);
             const PieceMeta& M = meta[ub];
             if (M.kind == kPieceStop) break;
+            if (tid == 0 && i < 48) TRACE(64 + i);
             if (M.kind == kPieceS) {
                 // ------------------------------ shrink ------------------------------
                 const uint4* xr = reinterpret_cast<const uint4*>(xrows + size_t(ub) * kItemTokCap * K);
@@ -577,10 +596,12 @@ __global__ void __launch_bounds__(kThreads, 1) mbgmv_kernel(const __grid_constan
                 consumer_sync();  // vbuf reused by the next piece
             }
             __syncwarp();
+            if (tid == 0 && i < 48) TRACE(112 + i);
             if (lane == 0) mbar_arrive(&xempty[ub]);
         }
     }
     // ---- teardown: the last CTA out resets this launch slot's counters
+    if (tid == 0) TRACE(2);
     __syncthreads();
     if (tid == 0) {
         __threadfence();

@@ -50,7 +50,7 @@ constexpr int kItemTokCap = 4;   // tokens per item (larger segments are chunked
 constexpr int kMaxRank = 64;     // max rank of the MBGMV path
 constexpr int kShrinkRows = 16;  // A rows per shrink piece
 constexpr int kConsumerWarps = 8;
-constexpr int kThreads = (kConsumerWarps + 2) * 32;  // + streamer warp + resolver warp
+constexpr int kThreads = (kConsumerWarps + 3) * 32;  // + 2 streamer warps + resolver warp
 constexpr int kMaxChunks = 8;    // pages one stored A row spans (TP q/k/v: N)
 constexpr int kSlotBytes = 32 * 1024;  // ring slot
 constexpr int kMaxSlots = 16;
