@@ -50,6 +50,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-steps", type=int, default=0, help="untimed steps only (for ncu)")
+    ap.add_argument("--no-graph", action="store_true", help="eager launches instead of a CUDA graph replay")
     return ap.parse_args()
 
 
@@ -177,12 +178,35 @@ class Workload:
         self.flops_layer = sum(4 * 2 * r * 2 * self.H // tp for r in
                                [b.ranks[a] for a in b.token_adapter if a >= 0])
 
+    graph = None
+
+    def capture(self, stream):
+        """Capture the layer sequence (launches only) into a CUDA graph; the
+        per-step batch_prepare stays outside (host work + descriptor upload),
+        as in a serving loop that replays a decode graph every iteration."""
+        import torch
+        self.dbatch.prepare(self.batch.token_adapter, stream=stream)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        cs = torch.cuda.Stream()
+        with torch.cuda.graph(g, stream=cs):
+            self.layers(torch.cuda.current_stream())
+        torch.cuda.synchronize()
+        self.graph = g
+
     def step(self, stream, events=None, tpl=None):
         """One step: prepare + all layers.  events: list to append
         (start, end, kind) CUDA event pairs around each launch."""
-        import torch
         b = self.dbatch
         b.prepare(self.batch.token_adapter, stream=stream)
+        if self.graph is not None and events is None and tpl is None:
+            self.graph.replay()
+            return
+        self.layers(stream, events, tpl)
+
+    def layers(self, stream, events=None, tpl=None):
+        import torch
+        b = self.dbatch
         H, P = self.H, self.P
         for l in range(self.L):
             if self.N == 1:
@@ -233,6 +257,19 @@ def run_ours(args):
     for _ in range(warm):
         W.step(stream, tpl=tpl)
     torch.cuda.synchronize()
+    # host enqueue cost of one eager step (Python + ctypes + launches)
+    lc0 = launch_count()
+    th0 = time.perf_counter()
+    W.step(stream, tpl=tpl)
+    host_ms = (time.perf_counter() - th0) * 1e3
+    launches_per_step = launch_count() - lc0
+    torch.cuda.synchronize()
+    use_graph = ws == 1 and not args.no_graph
+    if use_graph:
+        W.capture(stream)
+        for _ in range(2):
+            W.step(stream)
+        torch.cuda.synchronize()
     if ws > 1:
         dist.barrier()
     clocks = ClockSampler(local)
@@ -308,8 +345,11 @@ def run_ours(args):
                       "projections": "q,k,v,o", "parallelism": f"tp{ws}",
                       "l2": "inputs larger than L2 (adapter pages of all layers ~%.2f GB rotate)" %
                             (layers * (W.bytes_qkv + W.bytes_o) / 1e9),
-                      "step": "batch_prepare + layers x (qkv apply, o apply)"},
-           "gpu_launches": int(launches), "clocks": ck}
+                      "step": "batch_prepare + layers x (qkv apply, o apply)",
+                      "launch": "CUDA graph replay of the layer launches (PDL edges); prepare per step"
+                      if use_graph else "eager launches"},
+           "gpu_launches": int(launches_per_step * args.steps if use_graph else launches),
+           "host_enqueue_ms_eager_step": round(host_ms, 3), "clocks": ck}
     if roofline:
         out["roofline"] = roofline
     if ws == 1 and not args.no_e2e:

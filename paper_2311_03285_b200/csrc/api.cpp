@@ -747,6 +747,10 @@ void build_call(slora_batch* b, const KernelCfg& k, int N, int nproj, uint32_t m
 }
 }  // namespace
 
+namespace {
+slora_status ensure_call(slora_pool* p, slora_batch* b, int kc, uint32_t mask, void* stream);
+}
+
 extern "C" slora_status slora_batch_prepare(slora_batch_t b, const int64_t* tok_adapter, int32_t T, void* stream) {
     if (!b) return fail(SLORA_ERR_INVALID_ARG, "null batch");
     if (T < 0 || (T > 0 && !tok_adapter)) return fail(SLORA_ERR_INVALID_ARG, "token map");
@@ -848,6 +852,20 @@ extern "C" slora_status slora_batch_prepare(slora_batch_t b, const int64_t* tok_
         CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&p->ws_dev), sizeof(float) * st * kLaunchSlots, s));
         p->ws_stride = st;
     }
+    // eager descriptors for the usual calls (q/k/v together, o alone)
+    slora_status st2 = SLORA_OK;
+    if (b->adapted > 0) {
+        if (p->N() == 1) {
+            if (!st2 && p->kcfg[0].ok) st2 = ensure_call(p, b, 0, 0x7, stream);
+            if (!st2 && p->kcfg[0].ok) st2 = ensure_call(p, b, 0, 0x8, stream);
+        } else {
+            if (!st2 && p->kcfg[1].ok) st2 = ensure_call(p, b, 1, 0x7, stream);
+            if (!st2 && p->kcfg[2].ok) st2 = ensure_call(p, b, 2, 0x8, stream);
+            if (!st2 && p->kcfg[3].ok) st2 = ensure_call(p, b, 3, 0x7, stream);
+            if (!st2 && p->kcfg[3].ok) st2 = ensure_call(p, b, 3, 0x8, stream);
+        }
+    }
+    if (st2) return st2;
     return ok();
 }
 
@@ -879,6 +897,26 @@ bool aligned16(const void* ptr, int64_t ld, int es) {
     return !(reinterpret_cast<uintptr_t>(ptr) & 15) && (ld * es) % 16 == 0;
 }
 
+// Build + upload the (kernel cfg, mask) call descriptor if this prepare has not
+// yet (prepare builds the usual q/k/v and o calls eagerly so that a captured
+// CUDA graph of the layer sequence contains kernel launches only).
+slora_status ensure_call(slora_pool* p, slora_batch* b, int kc, uint32_t mask, void* stream) {
+    int np = 0;
+    for (int pj = 0; pj < 4; ++pj) np += (mask >> pj) & 1;
+    slora_batch::Call& call = b->calls[kc][np];
+    if (call.built && call.mask == mask) return SLORA_OK;
+    if (!p->kcfg[kc].ok) return fail(SLORA_ERR_SHAPE, "no valid kernel configuration");
+    build_call(b, p->kcfg[kc], p->N(), np, mask, call);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    cudaError_t e = cudaSuccess;
+    call.off_items = arena_put(b, call.items.data(), call.items.size() * sizeof(DevItem), s, e);
+    if (!e) call.off_pieces = arena_put(b, call.pieces.data(), call.pieces.size() * sizeof(DevPiece), s, e);
+    if (e) return fail(SLORA_ERR_CUDA, "call descriptor upload: %s", cudaGetErrorString(e));
+    call.built = true;
+    call.mask = mask;
+    return SLORA_OK;
+}
+
 // Resolve (building + uploading on first use) the call descriptor and fill the
 // launch parameters common to all modes.
 slora_status prepare_call(slora_pool* p, slora_batch* b, int kc, int32_t layer, uint32_t mask, void* stream,
@@ -895,16 +933,8 @@ slora_status prepare_call(slora_pool* p, slora_batch* b, int kc, int32_t layer, 
     // are q/k/v vs o (the stored-row divisor under TP); key by (kc, np) and
     // rebuild when the o-ness of the mask differs
     slora_batch::Call& call = b->calls[kc][np];
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
-    if (!call.built || call.mask != mask) {
-        build_call(b, k, p->N(), np, mask, call);
-        cudaError_t e = cudaSuccess;
-        call.off_items = arena_put(b, call.items.data(), call.items.size() * sizeof(DevItem), s, e);
-        if (!e) call.off_pieces = arena_put(b, call.pieces.data(), call.pieces.size() * sizeof(DevPiece), s, e);
-        if (e) return fail(SLORA_ERR_CUDA, "call descriptor upload: %s", cudaGetErrorString(e));
-        call.built = true;
-        call.mask = mask;
-    }
+    slora_status cs = ensure_call(p, b, kc, mask, stream);
+    if (cs) return cs;
     uint8_t* base = static_cast<uint8_t*>(b->arena_dev);
     q.pool = p->cfg.device_buffer;
     q.page_elems = p->P;
