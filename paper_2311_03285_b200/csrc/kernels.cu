@@ -462,6 +462,11 @@ __global__ void __launch_bounds__(kThreads, 1) mbgmv_kernel(const __grid_constan
                 }
                 const int nrow = min(rps, R - base);
                 mbar_wait(&empty[rg.slot], (rg.lap & 1) ^ 1);
+                if (p.dbg & 4) {  // debug: no data movement (consumer-only throughput)
+                    if (lane == 0) mbar_arrive(&full[rg.slot]);
+                    rg.advance(ns);
+                    return;
+                }
                 if (lane == 0) mbar_arrive_expect_tx(&full[rg.slot], uint32_t(nrow) * rowb);
                 __syncwarp();
                 unsigned char* sbase = ring + size_t(rg.slot) * kSlotBytes;
@@ -491,9 +496,9 @@ __global__ void __launch_bounds__(kThreads, 1) mbgmv_kernel(const __grid_constan
             }
             if (sid == 0) {
                 if (S) {  // x rows of the item's tokens; the same arrive publishes the meta
-                    if (lane == 0) mbar_arrive_expect_tx(&xfull[ub], uint32_t(M.nt) * arow_bytes);
+                    if (lane == 0) mbar_arrive_expect_tx(&xfull[ub], (p.dbg & 4) ? 0u : uint32_t(M.nt) * arow_bytes);
                     __syncwarp();
-                    if (lane < M.nt) {
+                    if (lane < M.nt && !(p.dbg & 4)) {
                         const T* x = reinterpret_cast<const T*>(p.x);
                         bulk_g2s(xrows + (size_t(ub) * kItemTokCap + lane) * K, x + int64_t(M.tok[lane]) * p.ldx,
                                  arow_bytes, &xfull[ub]);
