@@ -223,7 +223,7 @@ slora_status slora_sync(slora_pool_t pool, void* stream);
 
 /* Debug: when the environment variable SLORA_TRACE=1 is set at pool creation,
  * the next kernel launches record per-CTA event timestamps (ns, %globaltimer)
- * for CTAs 0..15, 256 slots each.  Copies min(n, 4096) values to out_host
+ * for CTAs 0..15, 1024 slots each.  Copies min(n, 16384) values to out_host
  * (synchronizes the device); INVALID_ARG when tracing is off. */
 slora_status slora_debug_trace(slora_pool_t pool, int64_t* out_host, int32_t n);
 

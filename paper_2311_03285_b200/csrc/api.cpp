@@ -16,6 +16,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <queue>
 #include <string>
 #include <unordered_map>
 #include <vector>
@@ -135,6 +136,11 @@ KernelCfg make_kernel_cfg(int mode, int64_t K, int64_t D, int64_t P, int es, int
     const size_t base = lora_smem_bytes(mode, K, k.dchunk, 0, es);
     int ns = int((budget - base) / kSlotBytes);
     ns = std::min(ns, kMaxSlots);
+    static const int ns_cap = [] {  // experiment knob: cap the ring depth
+        const char* e = getenv("SLORA_NS");
+        return e ? atoi(e) : 0;
+    }();
+    if (ns_cap >= 2) ns = std::min(ns, ns_cap);
     if (ns < 2) return k;
     k.ns = ns;
     k.smem = lora_smem_bytes(mode, K, k.dchunk, ns, es);
@@ -168,8 +174,8 @@ struct slora_pool {
     // 2 shrink o (K=H/N), 3 expand (D=H/N)
     KernelCfg kcfg[4];
     long long* trace_dev = nullptr;   // SLORA_TRACE=1: kernel event timestamps
-    // rotating per-launch slots: ticket/exit/item-done counters (zeroed, and
-    // re-zeroed by each launch's last CTA) and the fused v workspace
+    // rotating per-launch slots: item-done counters (zeroed once; each item's
+    // last expand piece re-zeroes its counter) and the fused v workspace
     int32_t* sync_dev = nullptr;
     int64_t sync_stride = 0;          // ints per slot
     float* ws_dev = nullptr;
@@ -207,8 +213,9 @@ struct slora_batch {
         bool built = false;
         uint32_t mask = 0;
         std::vector<DevItem> items;
-        std::vector<DevPiece> pieces;
-        size_t off_items = 0, off_pieces = 0;
+        std::vector<DevPiece> pieces;   // grouped by CTA (schedule_pieces)
+        std::vector<int32_t> cta_off;   // grid + 1
+        size_t off_items = 0, off_pieces = 0, off_cta = 0;
     } calls[4][5];
     size_t off_tok = 0;
     // device arena (bump allocated per prepare) + its pinned staging mirror
@@ -294,8 +301,8 @@ extern "C" slora_status slora_pool_create(const slora_pool_config* cfg, slora_po
         p->kcfg[3] = make_kernel_cfg(kExpand, P, P, P, es, dt);
         const char* tr = getenv("SLORA_TRACE");
         if (tr && atoi(tr) == 1) {
-            if ((e = cudaMalloc(&p->trace_dev, 4096 * sizeof(long long)))) return cleanup(e, "cudaMalloc trace");
-            cudaMemset(p->trace_dev, 0, 4096 * sizeof(long long));
+            if ((e = cudaMalloc(&p->trace_dev, 16 * kTraceSlots * sizeof(long long)))) return cleanup(e, "cudaMalloc trace");
+            cudaMemset(p->trace_dev, 0, 16 * kTraceSlots * sizeof(long long));
         }
         if (cfg->tp_size == 1 && !p->kcfg[0].ok) {
             slora_status s = fail(SLORA_ERR_SHAPE, "no valid MBGMV split for hidden %lld", (long long)H);
@@ -694,11 +701,46 @@ size_t arena_put(slora_batch* b, const void* src, size_t n, cudaStream_t s, cuda
     return off;
 }
 
+// Static schedule: LPT (largest first onto the least-loaded CTA) over the
+// pieces' streamed bytes, shrink pieces first, then expand pieces on top of
+// the shrink loads; each CTA's list keeps shrink before expand (the kernel's
+// deadlock-freedom argument, kernels.cu header).  The per-piece constant
+// stands for the fixed cost of a piece (barriers, v exchange).
+void schedule_pieces(const std::vector<DevPiece>& in, const std::vector<int64_t>& cost, int grid,
+                     std::vector<DevPiece>& out, std::vector<int32_t>& cta_off) {
+    grid = std::max(1, grid);
+    std::vector<std::vector<int32_t>> lists(static_cast<size_t>(grid));
+    std::vector<int64_t> load(static_cast<size_t>(grid), 0);
+    using HE = std::pair<int64_t, int32_t>;  // (load, cta), min-heap
+    std::priority_queue<HE, std::vector<HE>, std::greater<HE>> heap;
+    for (int c = 0; c < grid; ++c) heap.push({0, c});
+    for (int kind = kPieceS; kind <= kPieceE; ++kind) {
+        std::vector<int32_t> idx;
+        for (int32_t i = 0; i < int32_t(in.size()); ++i)
+            if (in[size_t(i)].kind == kind) idx.push_back(i);
+        std::stable_sort(idx.begin(), idx.end(),
+                         [&](int32_t a, int32_t c) { return cost[size_t(a)] > cost[size_t(c)]; });
+        for (int32_t i : idx) {
+            HE h = heap.top();
+            heap.pop();
+            lists[size_t(h.second)].push_back(i);
+            h.first += cost[size_t(i)];
+            heap.push(h);
+        }
+    }
+    out.clear();
+    cta_off.assign(size_t(grid) + 1, 0);
+    for (int c = 0; c < grid; ++c) {
+        cta_off[size_t(c)] = int32_t(out.size());
+        for (int32_t i : lists[size_t(c)]) out.push_back(in[size_t(i)]);
+    }
+    cta_off[size_t(grid)] = int32_t(out.size());
+}
+
 // Items = (segment x projection of the call x token chunk of <= kItemTokCap
 // tokens); pieces: each item's stored A rows in groups of kShrinkRows (shrink,
-// full K), and its output columns in chunks of kc.dchunk (expand).  Pieces are
-// ordered shrink-before-expand, larger items first (the ticket counter hands
-// them out in this order).
+// full K), and its output columns in chunks of kc.dchunk (expand), scheduled
+// onto the kernel's persistent CTAs by schedule_pieces.
 void build_call(slora_batch* b, const KernelCfg& k, int N, int nproj, uint32_t mask, slora_batch::Call& call) {
     call.items.clear();
     call.pieces.clear();
@@ -706,8 +748,8 @@ void build_call(slora_batch* b, const KernelCfg& k, int N, int nproj, uint32_t m
     for (int pj = 0; pj < 4; ++pj)
         if (mask & (1u << pj)) proj_ids[np++] = pj;
     (void)nproj;
-    struct Ord { int item; int64_t cost; };
-    std::vector<Ord> order;
+    const int es = b->pool->es;
+    const int64_t n_ep = (k.mode == kShrink || k.dchunk <= 0) ? 0 : (k.D + k.dchunk - 1) / k.dchunk;
     for (int si = 0; si < int(b->segs.size()); ++si) {
         const DevSeg& s = b->segs[size_t(si)];
         for (int pi = 0; pi < np; ++pi) {
@@ -726,24 +768,32 @@ void build_call(slora_batch* b, const KernelCfg& k, int N, int nproj, uint32_t m
                 it.tok_off = s.tok_off + t0;
                 it.scale = s.scale;
                 it.n_sp = (k.mode == kExpand) ? 0 : (ra + kShrinkRows - 1) / kShrinkRows;
-                order.push_back({int(call.items.size()), int64_t(s.rank) * 1000 + it.nt});
+                it.n_ep = int32_t(n_ep);
                 call.items.push_back(it);
             }
         }
     }
-    std::stable_sort(order.begin(), order.end(), [](const Ord& a, const Ord& c) { return a.cost > c.cost; });
-    if (k.mode != kExpand)
-        for (const Ord& o : order) {
-            const DevItem& it = call.items[size_t(o.item)];
-            const int proj = proj_ids[it.pi];
-            const int ra = it.rank / ((k.mode == kExpand) ? 1 : ((proj < 3) ? N : 1));
-            for (int r0 = 0; r0 < ra; r0 += kShrinkRows)
-                call.pieces.push_back({kPieceS, o.item, r0, std::min(kShrinkRows, ra - r0)});
-        }
-    if (k.mode != kShrink)
-        for (const Ord& o : order)
-            for (int64_t c0 = 0; c0 < k.D; c0 += k.dchunk)
-                call.pieces.push_back({kPieceE, o.item, int32_t(c0), int32_t(std::min<int64_t>(k.dchunk, k.D - c0))});
+    std::vector<DevPiece> pieces;
+    std::vector<int64_t> cost;
+    const int64_t kPieceOverhead = 4096;
+    for (int32_t ii = 0; ii < int32_t(call.items.size()); ++ii) {
+        const DevItem& it = call.items[size_t(ii)];
+        const int proj = proj_ids[it.pi];
+        const int ra = it.rank / ((k.mode == kExpand) ? 1 : ((proj < 3) ? N : 1));
+        if (k.mode != kExpand)
+            for (int r0 = 0; r0 < ra; r0 += kShrinkRows) {
+                const int nr = std::min(kShrinkRows, ra - r0);
+                pieces.push_back({kPieceS, ii, r0, nr});
+                cost.push_back(int64_t(nr) * k.K * es + kPieceOverhead);
+            }
+        if (k.mode != kShrink)
+            for (int64_t c0 = 0; c0 < k.D; c0 += k.dchunk) {
+                const int64_t dc = std::min<int64_t>(k.dchunk, k.D - c0);
+                pieces.push_back({kPieceE, ii, int32_t(c0), int32_t(dc)});
+                cost.push_back(int64_t(it.rank) * dc * es + kPieceOverhead);
+            }
+    }
+    schedule_pieces(pieces, cost, k.grid, call.pieces, call.cta_off);
 }
 }  // namespace
 
@@ -816,7 +866,7 @@ extern "C" slora_status slora_batch_prepare(slora_batch_t b, const int64_t* tok_
     for (const DevSeg& s : b->segs) chunks += (s.n_tok + kItemTokCap - 1) / kItemTokCap;
     const int64_t max_items = 4 * chunks;
     const int64_t max_pieces_per_item = (kMaxRank + kShrinkRows - 1) / kShrinkRows + 64;
-    const size_t need = 256 + size_t(T) * 4 + 16 * (256 + size_t(max_items) * sizeof(DevItem) +
+    const size_t need = 256 + size_t(T) * 4 + 16 * (1024 + 4 * 1024 + size_t(max_items) * sizeof(DevItem) +
                                                    size_t(max_items * max_pieces_per_item) * sizeof(DevPiece));
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     CUDA_TRY(cudaSetDevice(p->cfg.device));
@@ -911,6 +961,7 @@ slora_status ensure_call(slora_pool* p, slora_batch* b, int kc, uint32_t mask, v
     cudaError_t e = cudaSuccess;
     call.off_items = arena_put(b, call.items.data(), call.items.size() * sizeof(DevItem), s, e);
     if (!e) call.off_pieces = arena_put(b, call.pieces.data(), call.pieces.size() * sizeof(DevPiece), s, e);
+    if (!e) call.off_cta = arena_put(b, call.cta_off.data(), call.cta_off.size() * sizeof(int32_t), s, e);
     if (e) return fail(SLORA_ERR_CUDA, "call descriptor upload: %s", cudaGetErrorString(e));
     call.built = true;
     call.mask = mask;
@@ -941,9 +992,10 @@ slora_status prepare_call(slora_pool* p, slora_batch* b, int kc, int32_t layer, 
     q.tok_idx = reinterpret_cast<const int32_t*>(base + b->off_tok);
     q.items = reinterpret_cast<const DevItem*>(base + call.off_items);
     q.pieces = reinterpret_cast<const DevPiece*>(base + call.off_pieces);
+    q.cta_off = reinterpret_cast<const int32_t*>(base + call.off_cta);
     q.n_pieces = int32_t(call.pieces.size());
     q.n_items = int32_t(call.items.size());
-    if (q.n_items + 2 > p->sync_stride) return fail(SLORA_ERR_SHAPE, "sync area too small");
+    if (q.n_items > p->sync_stride) return fail(SLORA_ERR_SHAPE, "sync area too small");
     const uint64_t slot = p->launch_seq++ % kLaunchSlots;
     q.sync = p->sync_dev + int64_t(slot) * p->sync_stride;
     q.layer = layer;
@@ -1072,6 +1124,6 @@ extern "C" slora_status slora_debug_trace(slora_pool_t p, int64_t* out, int32_t 
     if (!p->trace_dev) return fail(SLORA_ERR_INVALID_ARG, "tracing is off (set SLORA_TRACE=1 before pool create)");
     CUDA_TRY(cudaSetDevice(p->cfg.device));
     CUDA_TRY(cudaDeviceSynchronize());
-    CUDA_TRY(cudaMemcpy(out, p->trace_dev, sizeof(int64_t) * size_t(std::min(n, 4096)), cudaMemcpyDeviceToHost));
+    CUDA_TRY(cudaMemcpy(out, p->trace_dev, sizeof(int64_t) * size_t(std::min(n, 16 * kTraceSlots)), cudaMemcpyDeviceToHost));
     return ok();
 }

@@ -3,24 +3,27 @@
 // mbgmv_kernel<T, MODE>: MBGMV gather-shrink-expand over Unified Paging
 //   (Sec. 5.3; Eq. lora_factored).
 //
-//   Persistent (one CTA per SM), warp-specialized, dynamically scheduled.
+//   Persistent (one CTA per SM), warp-specialized, statically scheduled.
 //   The host cuts every (segment x projection x token chunk) item into
 //     shrink pieces  -- a group of kShrinkRows stored A rows over the full K:
 //                       v_j = <x_t, A_j> for the item's tokens (complete dot
 //                       products, no partial sums), and
 //     expand pieces  -- all r B rows over one chunk of output columns:
 //                       y_t[cols] += scale * sum_j v_j B_j[cols].
-//   A per-launch ticket counter hands out every shrink piece before any
-//   expand piece; an expand piece waits (per-item done counter, acquire) for
-//   its item's shrink pieces, so it only ever waits on earlier tickets (no
-//   deadlock with all CTAs resident).  In the fused mode the rank-r
-//   intermediate goes through a small per-launch workspace (<= nproj*NR fp32,
-//   a few KB, written and read within microseconds: it lives in L2, never
-//   streamed through HBM like the weights).
+//   and assigns them to CTAs (LPT on bytes, api.cpp); each CTA runs its
+//   shrink pieces before its expand pieces, and an expand piece waits
+//   (per-item done counter, acquire) for its item's shrink pieces, which
+//   never wait themselves (no deadlock with all CTAs resident).  In the fused
+//   mode the rank-r intermediate goes through a small per-launch workspace
+//   (<= nproj*NR fp32, a few KB, written and read within microseconds: it
+//   lives in L2, never streamed through HBM like the weights).  The counters
+//   reset themselves (the item's last expand piece), so a launch needs no
+//   teardown and no host memset.
 //
-//   warp 9 (resolver): takes tickets, resolves item -> adapter page table ->
-//     the page id of every row the piece streams, one piece ahead.
-//   warp 8 (streamer): streams the piece's pages (whole 8 KB A rows; 4 KB B
+//   warp 9 (resolver): loads the CTA's piece list + items (one per lane) and
+//     resolves each piece's page ids from the adapter page table, up to
+//     kMeta-1 pieces ahead of the consumers.
+//   warps 8, 10 (streamers): stream the piece's pages (whole 8 KB A rows; 4 KB B
 //     row slices) and x rows into an mbarrier ring with cp.async.bulk (TMA
 //     engine, SASS UBLKCP); weights of the first piece are fetched before
 //     griddepcontrol.wait (programmatic dependent launch), activations after.
@@ -69,7 +72,29 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                  : "memory");
 }
+// mbarrier wait.  SLORA_WAIT_MODE 0: try_wait (hardware-chosen suspend),
+// 1: try_wait with a suspend-time hint, 2: test_wait spin.
+#ifndef SLORA_WAIT_MODE
+#define SLORA_WAIT_MODE 0
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+#if SLORA_WAIT_MODE == 1
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity), "n"(1000000)
+        : "memory");
+#elif SLORA_WAIT_MODE == 2
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+#else
     asm volatile(
         "{\n\t.reg .pred p;\n"
         "WAIT_%=:\n\t"
@@ -77,6 +102,33 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
         "r"(parity)
         : "memory");
+#endif
+}
+// Back-off wait for the helper warps (streamers, resolver, prefetcher,
+// publisher): polls with test_wait and sleeps in between, so that idle
+// helpers do not flood the CTA's barrier unit with probes while the
+// consumers' own waits need it (measured: polling helpers slowed every
+// consumer barrier operation ~10x).
+#ifndef SLORA_HELPER_SLEEP_NS
+#define SLORA_HELPER_SLEEP_NS 128
+#endif
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+#if SLORA_HELPER_SLEEP_NS > 0
+    while (!mbar_test(bar, parity)) __nanosleep(SLORA_HELPER_SLEEP_NS);
+#else
+    mbar_wait(bar, parity);
+#endif
 }
 // 1-D bulk copy global -> own shared memory on the TMA engine (SASS UBLKCP),
 // completing `bytes` of transaction count on `bar`.
@@ -108,7 +160,7 @@ __device__ __forceinline__ long long gtimer() {
 }
 #define TRACE(ev)                                                                                  \
     do {                                                                                           \
-        if (p.trace && blockIdx.x < 16 && (ev) < 256) p.trace[blockIdx.x * 256 + (ev)] = gtimer(); \
+        if (p.trace && blockIdx.x < 16 && (ev) < kTraceSlots) p.trace[blockIdx.x * kTraceSlots + (ev)] = gtimer(); \
     } while (0)
 
 // ---------------------------------------------------- element conversions
@@ -193,7 +245,7 @@ __device__ __forceinline__ void dot16<float>(const uint4& a, const uint4& x, flo
 // ------------------------------------------------------------ smem layout
 constexpr int kMaxPiecePages = kMaxRank > kShrinkRows * kMaxChunks ? kMaxRank : kShrinkRows * kMaxChunks;
 struct PieceMeta {
-    int32_t kind, item, nt, r, ra, row0, nrows, dcol0, dcols, proj, arp, n_sp;
+    int32_t kind, item, nt, r, ra, row0, nrows, dcol0, dcols, proj, arp, n_sp, n_ep;
     float scale;
     int32_t pi;                   // projection index in the call's mask order
     int64_t vbase;                // v index of (token 0, rank row 0) of this item
@@ -203,21 +255,29 @@ struct PieceMeta {
 };
 
 struct SmemLayout {
-    size_t bars, meta, vbuf, xrows, ring, total;
+    size_t bars, meta, pubq, vbuf, red, xrows, ring, total;
 };
+constexpr int kPub = 4;        // shrink-done queue (consumers -> publisher warp)
+constexpr int kXBufs = 1;      // x row buffers (consumers copy x to registers and release at once)
+constexpr int kNumBars = 2 * kMaxSlots + 4 + 2 * kMeta + 4 + 2 * kPub;
+constexpr int kRedFloats = kConsumerWarps * kShrinkRows * kItemTokCap;  // per buffer
 __host__ __device__ inline size_t al128(size_t x) { return (x + 127) & ~size_t(127); }
 __host__ __device__ inline SmemLayout smem_layout(int mode, int64_t K, int64_t dchunk, int ns, int es) {
     (void)dchunk;
     SmemLayout L{};
     size_t off = 0;
     L.bars = off;
-    off = al128(off + sizeof(uint64_t) * (2 * kMaxSlots + 6));
+    off = al128(off + sizeof(uint64_t) * kNumBars);
     L.meta = off;
-    off = al128(off + 2 * sizeof(PieceMeta));
+    off = al128(off + kMeta * sizeof(PieceMeta));
+    L.pubq = off;
+    off = al128(off + kPub * sizeof(int32_t));
     L.vbuf = off;
-    off = al128(off + (mode != kShrink ? size_t(kItemTokCap) * kMaxRank * 4 : 0));
+    off = al128(off + (mode != kShrink ? size_t(2) * kItemTokCap * kMaxRank * 4 : 0));
+    L.red = off;
+    off = al128(off + (mode != kExpand ? size_t(2) * kRedFloats * 4 : 0));
     L.xrows = off;
-    off = al128(off + (mode != kExpand ? size_t(2) * kItemTokCap * K * es : 0));
+    off = al128(off + (mode != kExpand ? size_t(kXBufs) * kItemTokCap * K * es : 0));
     L.ring = off;
     off = al128(off + size_t(ns) * kSlotBytes);
     L.total = off;
@@ -235,25 +295,119 @@ struct Ring {
     }
 };
 
-// Shrink of one stored A row (full K) for NT tokens; returns the complete dot
-// products in out[] (all lanes).
-template <typename T, int NT>
-__device__ __forceinline__ void shrink_row(const uint4* arow, const uint4* xr, int xstride, int nvec, float (&out)[NT],
-                                           int lane) {
-    float a0[NT], a1[NT];
+// Sum VV (power of two) per-lane values across the warp by transposition:
+// VV-1 + 5-log2(VV) shuffles instead of 5*VV.  On return lane l holds the
+// warp total of value index (l >> (5 - LOG2VV)) & (VV - 1); the lanes whose
+// low 5-LOG2VV bits are zero are the writers.  Fixed order (deterministic).
+template <int VV, int LOG2VV>
+__device__ __forceinline__ float xreduce(float (&v)[VV], int lane) {
 #pragma unroll
-    for (int t = 0; t < NT; ++t) a0[t] = a1[t] = 0.f;
-    for (int q = lane; q < nvec; q += 32) {
-        const uint4 a = arow[q];
+    for (int step = 0; step < LOG2VV; ++step) {
+        const int o = 16 >> step;
+        const int half = VV >> (step + 1);
+        const bool up = (lane & o) != 0;
 #pragma unroll
-        for (int t = 0; t < NT; ++t) dot16<T>(a, xr[t * xstride + q], a0[t], a1[t]);
+        for (int j = 0; j < half; ++j) {
+            const float send = up ? v[j] : v[j + half];
+            const float keep = up ? v[j + half] : v[j];
+            v[j] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+        }
     }
+    float s = v[0];
 #pragma unroll
-    for (int t = 0; t < NT; ++t) {
-        float s = a0[t] + a1[t];
+    for (int o = 16 >> LOG2VV; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    return s;
+}
+
+// Shrink of one piece, K-split across the consumer warps: warp w owns the
+// 16-byte vectors [w*sl, (w+1)*sl) of every stored A row (sl = nvec/8; XV =
+// ceil(sl/32) per lane), holds the matching slice of the item's x rows in
+// registers (read from smem once per piece; the x buffer is released at
+// once), takes the slot's rows two at a time (all loads first), and reduces
+// the 2*NT partial dot products of a row pair across lanes by transposition;
+// the 8 warps' partials meet in smem (red) and each v entry is written once,
+// complete.  Warps do equal work per slot.
+template <typename T, int NT, int XV>
+__device__ __forceinline__ void shrink_piece(const LoraParams& p, const PieceMeta& M, const unsigned char* ring,
+                                             const uint4* xs, int nvec, uint32_t arow_bytes, int rps_s,
+                                             uint64_t* full, uint64_t* empty, Ring& rg, int ns, uint64_t* xempty,
+                                             float* red, int warp, int lane, int i) {
+    constexpr int NTP = NT == 3 ? 4 : NT;
+    constexpr int VV = 2 * NTP;
+    constexpr int LOG2VV = VV == 2 ? 1 : (VV == 4 ? 2 : 3);
+    const int sl = (nvec + kConsumerWarps - 1) / kConsumerWarps;
+    const int v0 = warp * sl, v1 = min(nvec, v0 + sl);
+    uint4 xv[NT][XV];
+    int li[XV];
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-        out[t] = s;
+    for (int k = 0; k < XV; ++k) {
+        const int idx = v0 + lane + 32 * k;
+        li[k] = min(idx, nvec - 1);  // clamped: x is zero there, so the product vanishes
+#pragma unroll
+        for (int t = 0; t < NT; ++t) xv[t][k] = idx < v1 ? xs[t * nvec + idx] : make_uint4(0, 0, 0, 0);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(xempty);  // x slice in registers: buffer free for the next shrink piece
+    const bool math = !(p.dbg & 1);
+    const int nrows = M.nrows;
+    const int nslots = (nrows + rps_s - 1) / rps_s;
+    const int wsh = 5 - LOG2VV;
+    const int vidx = (lane >> wsh) & (VV - 1);
+    const bool writer = (lane & ((1 << wsh) - 1)) == 0;
+    const int rsel = vidx / NTP, tw = vidx % NTP;
+    // slot by slot (no runtime divisions in the loop); within a slot, rows
+    // RQ at a time: all loads first, independent row-pair reductions
+    // (RQ = 2 for the widest rows: registers)
+    constexpr int RQ = XV >= 4 ? 2 : 4;
+    for (int k = 0, rbase = 0; k < nslots; ++k, rbase += rps_s) {
+        mbar_wait(&full[rg.slot], rg.lap & 1);
+        if (k == 0 && warp == 0 && lane == 0 && i < 48) TRACE(304 + i);
+        const int nrow = min(rps_s, nrows - rbase);
+        if (math) {
+            const unsigned char* sb = ring + size_t(rg.slot) * kSlotBytes;
+            for (int q0 = 0; q0 < nrow; q0 += RQ) {
+                uint4 av[RQ][XV];
+#pragma unroll
+                for (int j = 0; j < RQ; ++j) {
+                    const uint4* rp = reinterpret_cast<const uint4*>(sb + size_t(min(q0 + j, nrow - 1)) * arow_bytes);
+#pragma unroll
+                    for (int kk = 0; kk < XV; ++kk) av[j][kk] = rp[li[kk]];
+                }
+#pragma unroll
+                for (int h = 0; h < RQ / 2; ++h) {
+                    float c0[VV], c1[VV];
+#pragma unroll
+                    for (int j = 0; j < VV; ++j) c0[j] = c1[j] = 0.f;
+#pragma unroll
+                    for (int kk = 0; kk < XV; ++kk)
+#pragma unroll
+                        for (int t = 0; t < NT; ++t) {
+                            dot16<T>(av[2 * h][kk], xv[t][kk], c0[t], c1[t]);
+                            dot16<T>(av[2 * h + 1][kk], xv[t][kk], c0[NTP + t], c1[NTP + t]);
+                        }
+#pragma unroll
+                    for (int j = 0; j < VV; ++j) c0[j] += c1[j];
+                    const float sum = xreduce<VV, LOG2VV>(c0, lane);
+                    const int q = q0 + 2 * h + rsel;
+                    if (writer && tw < NT && q < nrow)
+                        red[(warp * kShrinkRows + rbase + q) * kItemTokCap + tw] = sum;
+                }
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[rg.slot]);
+        rg.advance(ns);
+    }
+    if (warp == 0 && lane == 0 && i < 48) TRACE(352 + i);
+    consumer_sync();  // all warps' partials of the piece are in red
+    if (warp == 0 && lane == 0 && i < 48) TRACE(400 + i);
+    const int tid = warp * 32 + lane;
+    if (tid < M.nrows * NT && math) {
+        const int q = tid / NT, t = tid % NT;
+        float s = 0.f;
+#pragma unroll
+        for (int w = 0; w < kConsumerWarps; ++w) s += red[(w * kShrinkRows + q) * kItemTokCap + t];
+        p.v[M.vbase + int64_t(t) * M.ra + M.row0 + q] = s;
     }
 }
 
@@ -300,19 +454,46 @@ __device__ __forceinline__ void expand_piece(const LoraParams& p, const PieceMet
             rg.advance(ns);
         }
         mbar_wait(&full[rg.slot], rg.lap & 1);
+        if (threadIdx.x == 0) {
+            const int sq = int(rg.lap) * ns + rg.slot;
+            if (sq < 240) TRACE(512 + sq);
+        }
         if (active) {
             const uint4* sl = reinterpret_cast<const uint4*>(ring + size_t(rg.slot) * kSlotBytes) + cv;
             const int nrow = min(rps, r - j0);
-            for (int q = 0; q < nrow; ++q) {
-                float b[VE];
-                V::to_f32(sl[q * rowv], b);
-                const float* vc = vbuf + j0 + q;
+            if ((nrow & 3) == 0) {  // the usual case (ranks are multiples of 4): 4 rows at a time, loads first
+                for (int q0 = 0; q0 < nrow; q0 += 4) {
+                    uint4 bv[4];
+                    float vv[4][NT];
 #pragma unroll
-                for (int t = 0; t < NT; ++t) {
-                    if (own >> t & 1u) {
-                        const float vj = vc[t * r];
+                    for (int q = 0; q < 4; ++q) {
+                        bv[q] = sl[(q0 + q) * rowv];
 #pragma unroll
-                        for (int e = 0; e < VE; ++e) acc[t][e] = fmaf(vj, b[e], acc[t][e]);
+                        for (int t = 0; t < NT; ++t) vv[q][t] = vbuf[t * r + j0 + q0 + q];
+                    }
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        float b[VE];
+                        V::to_f32(bv[q], b);
+#pragma unroll
+                        for (int t = 0; t < NT; ++t)
+                            if (own >> t & 1u)
+#pragma unroll
+                                for (int e = 0; e < VE; ++e) acc[t][e] = fmaf(vv[q][t], b[e], acc[t][e]);
+                    }
+                }
+            } else {
+                for (int q = 0; q < nrow; ++q) {
+                    float b[VE];
+                    V::to_f32(sl[q * rowv], b);
+                    const float* vc = vbuf + j0 + q;
+#pragma unroll
+                    for (int t = 0; t < NT; ++t) {
+                        if (own >> t & 1u) {
+                            const float vj = vc[t * r];
+#pragma unroll
+                            for (int e = 0; e < VE; ++e) acc[t][e] = fmaf(vj, b[e], acc[t][e]);
+                        }
                     }
                 }
             }
@@ -347,17 +528,24 @@ __global__ void __launch_bounds__(kThreads, 1) mbgmv_kernel(const __grid_constan
     const SmemLayout L = smem_layout(MODE, K, 0, p.ns, ES);
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.bars);
     uint64_t* empty = full + kMaxSlots;
-    uint64_t* xfull = empty + kMaxSlots;
+    uint64_t* xfull = empty + kMaxSlots;  // [2] x rows of the CTA's shrink pieces, alternating
     uint64_t* xempty = xfull + 2;
-    uint64_t* mfull = xempty + 2;
+    uint64_t* mfull = xempty + 2;         // [kMeta] resolved piece published
+    uint64_t* mempty = mfull + kMeta;     // [kMeta] piece retired by every role
+    uint64_t* vfull = mempty + kMeta;     // [2] expand v rows staged (prefetcher -> consumers)
+    uint64_t* vempty = vfull + 2;
+    uint64_t* pfull = vempty + 2;         // [kPub] shrink piece done (consumers -> publisher)
+    uint64_t* pempty = pfull + kPub;
     PieceMeta* meta = reinterpret_cast<PieceMeta*>(smem + L.meta);
-    float* vbuf = reinterpret_cast<float*>(smem + L.vbuf);
-    T* xrows = reinterpret_cast<T*>(smem + L.xrows);  // [2][kItemTokCap][K]
-    unsigned char* ring = smem + L.ring;              // [ns][kSlotBytes]
+    int32_t* pubq = reinterpret_cast<int32_t*>(smem + L.pubq);
+    float* vbuf = reinterpret_cast<float*>(smem + L.vbuf);  // [2][kItemTokCap * kMaxRank]
+    float* red = reinterpret_cast<float*>(smem + L.red);    // [2][kRedFloats]
+    T* xrows = reinterpret_cast<T*>(smem + L.xrows);        // [2][kItemTokCap][K]
+    unsigned char* ring = smem + L.ring;                    // [ns][kSlotBytes]
     const int ns = p.ns;
-    const uint32_t arow_bytes = uint32_t(K * ES);                 // shrink row (full K)
-    const int rps_s = max(1, kSlotBytes / int(arow_bytes));       // shrink rows per slot
-    __shared__ int s_last;
+    const uint32_t arow_bytes = uint32_t(K * ES);            // shrink row (full K)
+    const int rps_s = max(1, kSlotBytes / int(arow_bytes));  // shrink rows per slot
+    constexpr int kRoles = kConsumerWarps + 3;               // mempty arrivals: consumers, 2 streamers, prefetcher
 
     if (tid == 0) TRACE(0);
     if (tid == 0) {
@@ -368,7 +556,16 @@ __global__ void __launch_bounds__(kThreads, 1) mbgmv_kernel(const __grid_constan
         for (int b = 0; b < 2; ++b) {
             mbar_init(&xfull[b], 1);
             mbar_init(&xempty[b], kConsumerWarps);
+            mbar_init(&vfull[b], 1);
+            mbar_init(&vempty[b], kConsumerWarps);
+        }
+        for (int b = 0; b < kMeta; ++b) {
             mbar_init(&mfull[b], 1);
+            mbar_init(&mempty[b], kRoles);
+        }
+        for (int b = 0; b < kPub; ++b) {
+            mbar_init(&pfull[b], kConsumerWarps);
+            mbar_init(&pempty[b], 1);
         }
         fence_mbar_init();
     }
@@ -377,79 +574,91 @@ __global__ void __launch_bounds__(kThreads, 1) mbgmv_kernel(const __grid_constan
     const T* pool = reinterpret_cast<const T*>(p.pool);
     const int64_t P = p.page_elems;
 
-    if (warp == kConsumerWarps + 1) {
+    if (warp == kWarpResolver) {
         // ============================ resolver ============================
-        for (int i = 0;; ++i) {
-            const int ub = i & 1;
-            if (i >= 2) mbar_wait(&xempty[ub], ((i >> 1) - 1) & 1);
-            PieceMeta& M = meta[ub];
-            int ticket = 0;
-            if (lane == 0) ticket = atomicAdd(&p.sync[0], 1);
-            ticket = __shfl_sync(0xffffffffu, ticket, 0);
-            if (ticket >= p.n_pieces) {
-                if (lane == 0) {
-                    M.kind = kPieceStop;
-                    mbar_arrive(&mfull[ub]);
-                }
-                break;
+        // This CTA's pieces (host schedule) are loaded 32 at a time, one per
+        // lane, with their items; each piece then needs one dependent load
+        // (its page ids), kMeta-1 pieces ahead of the consumers.
+        const int pb = p.cta_off[blockIdx.x], pe = p.cta_off[blockIdx.x + 1];
+        int i = 0;
+        for (int base = pb; base < pe; base += 32) {
+            const int cnt = min(32, pe - base);
+            DevPiece pcl{};
+            DevItem itl{};
+            if (lane < cnt) {
+                pcl = p.pieces[base + lane];
+                itl = p.items[pcl.item];
             }
-            const DevPiece pc = p.pieces[ticket];
-            const DevItem it = p.items[pc.item];
-            const int proj = p.proj_ids[it.pi];
-            const int div = (MODE == kExpand) ? 1 : p.a_div[proj];
-            const int arp = (MODE == kExpand) ? 1 : p.a_row_pages[proj];
-            const int32_t* tab = it.tab + int64_t((p.layer * 4 + proj) * 2) * it.rank;
-            if (lane == 0) {
-                M.kind = pc.kind;
-                M.item = pc.item;
-                M.nt = it.nt;
-                M.r = it.rank;
-                M.ra = it.rank / div;
-                M.proj = proj;
-                M.arp = arp;
-                M.n_sp = it.n_sp;
-                M.scale = it.scale;
-                M.vbase = int64_t(it.pi) * (p.NR / div) + it.vrow / div;
-                M.pi = it.pi;
-                M.vrow = it.vrow;
-                if (pc.kind == kPieceS) {
-                    M.row0 = pc.a;
-                    M.nrows = pc.b;
+            for (int q = 0; q < cnt; ++q, ++i) {
+                const int m = i & (kMeta - 1);
+                if (i >= kMeta) mbar_wait_sleep(&mempty[m], ((i / kMeta) - 1) & 1);
+                PieceMeta& M = meta[m];
+                const int kind = __shfl_sync(0xffffffffu, pcl.kind, q);
+                const int pa = __shfl_sync(0xffffffffu, pcl.a, q);
+                const int pbn = __shfl_sync(0xffffffffu, pcl.b, q);
+                const int rank = __shfl_sync(0xffffffffu, itl.rank, q);
+                const int pi = __shfl_sync(0xffffffffu, itl.pi, q);
+                const int nt = __shfl_sync(0xffffffffu, itl.nt, q);
+                const int tok_off = __shfl_sync(0xffffffffu, itl.tok_off, q);
+                const int32_t* itab = reinterpret_cast<const int32_t*>(
+                    __shfl_sync(0xffffffffu, (unsigned long long)reinterpret_cast<uintptr_t>(itl.tab), q));
+                const int proj = p.proj_ids[pi];
+                const int div = (MODE == kExpand) ? 1 : p.a_div[proj];
+                const int arp = (MODE == kExpand) ? 1 : p.a_row_pages[proj];
+                const int32_t* tab = itab + int64_t((p.layer * 4 + proj) * 2) * rank;
+                if (lane < nt) M.tok[lane] = p.tok_idx[tok_off + lane];
+                if (kind == kPieceS) {
+                    for (int w = lane; w < pbn * arp; w += 32) M.pages[w] = tab[(pa + w / arp) * arp + w % arp];
                 } else {
-                    M.dcol0 = pc.a;
-                    M.dcols = pc.b;
+                    for (int w = lane; w < rank; w += 32) M.pages[w] = tab[rank + w];
                 }
+                if (lane == q) {
+                    M.kind = kind;
+                    M.item = pcl.item;
+                    M.nt = nt;
+                    M.r = rank;
+                    M.ra = rank / div;
+                    M.proj = proj;
+                    M.arp = arp;
+                    M.n_sp = itl.n_sp;
+                    M.n_ep = itl.n_ep;
+                    M.scale = itl.scale;
+                    M.vbase = int64_t(pi) * (p.NR / div) + itl.vrow / div;
+                    M.pi = pi;
+                    M.vrow = itl.vrow;
+                    M.row0 = M.dcol0 = pa;
+                    M.nrows = M.dcols = pbn;
+                }
+                __syncwarp();
+                if (lane == 0 && i < 48) TRACE(16 + i);
+                if (lane == 0 && i < 48 && p.trace && blockIdx.x < 16)  // piece code: kind, tokens, rows / rank
+                    p.trace[blockIdx.x * kTraceSlots + 208 + i] = kind * 1000000 + nt * 100000 + (kind == kPieceS ? pbn : rank);
+                if (lane == 0) mbar_arrive(&mfull[m]);
             }
-            if (lane < it.nt) M.tok[lane] = p.tok_idx[it.tok_off + lane];
-            if (pc.kind == kPieceS) {
-                for (int q = lane; q < pc.b * arp; q += 32) M.pages[q] = tab[(pc.a + q / arp) * arp + q % arp];
-            } else {
-                for (int q = lane; q < it.rank; q += 32) M.pages[q] = tab[it.rank + q];
-            }
-            __syncwarp();
-            if (lane == 0 && i < 48) TRACE(16 + i);
-            if (lane == 0 && i < 48 && p.trace && blockIdx.x < 16) p.trace[blockIdx.x * 256 + 208 + i] = ticket;
-            if (lane == 0) mbar_arrive(&mfull[ub]);
         }
-    } else if (warp == kConsumerWarps || warp == kConsumerWarps + 2) {
+        const int m = i & (kMeta - 1);
+        if (i >= kMeta) mbar_wait_sleep(&mempty[m], ((i / kMeta) - 1) & 1);
+        if (lane == 0) {
+            meta[m].kind = kPieceStop;
+            mbar_arrive(&mfull[m]);
+        }
+    } else if (warp == kWarpStreamer0 || warp == kWarpStreamer1) {
         // ============================ streamers ===========================
         // Two warps issue alternate ring slots (bulk-copy issue costs ~90 ns
         // per copy per warp, measured; two issuers double the rate).
         // Adapter pages are written only by the loader's scatter kernel, which
         // never triggers its dependents early, so the first piece's pages are
         // streamed before griddepcontrol.wait; x, y and v only after it.
-        const int sid = warp == kConsumerWarps ? 0 : 1;
+        const int sid = warp == kWarpStreamer0 ? 0 : 1;
         Ring rg;
         uint32_t seq = 0;  // slot sequence number (shared numbering, both warps)
         bool waited = false;
+        int xs = 0;        // shrink pieces seen (x buffer = xs & 1)
         for (int i = 0;; ++i) {
-            const int ub = i & 1;
-            mbar_wait(&mfull[ub], (i >> 1) & 1);
-            const PieceMeta& M = meta[ub];
-            if (M.kind == kPieceStop) {
-                if (lane == 0 && sid == 0) mbar_arrive(&xfull[ub]);
-                break;
-            }
+            const int m = i & (kMeta - 1);
+            mbar_wait_sleep(&mfull[m], (i / kMeta) & 1);
+            const PieceMeta& M = meta[m];
+            if (M.kind == kPieceStop) break;
             const bool S = M.kind == kPieceS;
             const int R = S ? M.nrows : M.r;
             const uint32_t rowb = S ? arow_bytes : uint32_t(M.dcols * ES);
@@ -461,11 +670,19 @@ __global__ void __launch_bounds__(kThreads, 1) mbgmv_kernel(const __grid_constan
                     return;
                 }
                 const int nrow = min(rps, R - base);
-                mbar_wait(&empty[rg.slot], (rg.lap & 1) ^ 1);
+                mbar_wait_sleep(&empty[rg.slot], (rg.lap & 1) ^ 1);
                 if (p.dbg & 4) {  // debug: no data movement (consumer-only throughput)
+                    if (lane == 0) {
+                        const int sq = int(rg.lap) * ns + rg.slot;
+                        if (sq < 240) TRACE(768 + sq);
+                    }
                     if (lane == 0) mbar_arrive(&full[rg.slot]);
                     rg.advance(ns);
                     return;
+                }
+                if (lane == 0) {
+                    const int sq = int(rg.lap) * ns + rg.slot;
+                    if (sq < 240) TRACE(768 + sq);
                 }
                 if (lane == 0) mbar_arrive_expect_tx(&full[rg.slot], uint32_t(nrow) * rowb);
                 __syncwarp();
@@ -473,12 +690,14 @@ __global__ void __launch_bounds__(kThreads, 1) mbgmv_kernel(const __grid_constan
                 if (S) {
                     // row q: K elements over arp pages of P (TP q/k/v rows span N pages)
                     const int nc = nrow * M.arp;
-                    for (int w = lane; w < nc; w += 32) {
-                        const int q = w / M.arp, ch = w % M.arp;
+                    const int sp = (p.dbg & 8) ? 2 : 1;  // debug: split each page copy in two
+                    for (int w = lane; w < nc * sp; w += 32) {
+                        const int ww = w / sp, h = w % sp;
+                        const int q = ww / M.arp, ch = ww % M.arp;
                         const int64_t k0 = int64_t(ch) * P;
-                        const int64_t len = min(P, K - k0);
-                        bulk_g2s(sbase + size_t(q) * rowb + k0 * ES,
-                                 pool + int64_t(M.pages[(base + q) * M.arp + ch]) * P, uint32_t(len * ES),
+                        const int64_t len = min(P, K - k0) / sp;
+                        bulk_g2s(sbase + size_t(q) * rowb + (k0 + h * len) * ES,
+                                 pool + int64_t(M.pages[(base + q) * M.arp + ch]) * P + h * len, uint32_t(len * ES),
                                  &full[rg.slot]);
                     }
                 } else {
@@ -494,92 +713,133 @@ __global__ void __launch_bounds__(kThreads, 1) mbgmv_kernel(const __grid_constan
                 pdl_wait();
                 waited = true;
             }
-            if (sid == 0) {
-                if (S) {  // x rows of the item's tokens; the same arrive publishes the meta
-                    if (lane == 0) mbar_arrive_expect_tx(&xfull[ub], (p.dbg & 4) ? 0u : uint32_t(M.nt) * arow_bytes);
+            if (S) {  // x rows of the item's tokens
+                const int xb = xs % kXBufs;
+                if (sid == 0) {
+                    if (xs >= kXBufs) mbar_wait_sleep(&xempty[xb], ((xs / kXBufs) - 1) & 1);
+                    const bool xcopy = !(p.dbg & (4 | 16));  // debug bit 16: no x rows
+                    if (lane == 0) mbar_arrive_expect_tx(&xfull[xb], xcopy ? uint32_t(M.nt) * arow_bytes : 0u);
                     __syncwarp();
-                    if (lane < M.nt && !(p.dbg & 4)) {
+                    if (lane < M.nt && xcopy) {
                         const T* x = reinterpret_cast<const T*>(p.x);
-                        bulk_g2s(xrows + (size_t(ub) * kItemTokCap + lane) * K, x + int64_t(M.tok[lane]) * p.ldx,
-                                 arow_bytes, &xfull[ub]);
+                        bulk_g2s(xrows + (size_t(xb) * kItemTokCap + lane) * K, x + int64_t(M.tok[lane]) * p.ldx,
+                                 arow_bytes, &xfull[xb]);
                     }
-                } else {
-                    if (lane == 0) mbar_arrive(&xfull[ub]);
                 }
+                ++xs;
             }
             for (int base = pre * rps; base < R; base += rps) issue_slot(base);
             if (lane == 0 && i < 48) TRACE(160 + i);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&mempty[m]);
+        }
+    } else if (warp == kWarpPrefetch) {
+        // ======================= expand-v prefetcher ======================
+        // Stages each expand piece's v rows (after its item's shrink pieces
+        // are published, fused mode) into vbuf while the consumers still work
+        // on earlier pieces.
+        int es = 0;
+        for (int i = 0;; ++i) {
+            const int m = i & (kMeta - 1);
+            mbar_wait_sleep(&mfull[m], (i / kMeta) & 1);
+            const PieceMeta& M = meta[m];
+            if (M.kind == kPieceStop) break;
+            if (M.kind == kPieceE) {
+                const int eb = es & 1;
+                if (es >= 2) mbar_wait_sleep(&vempty[eb], ((es >> 1) - 1) & 1);
+                float* vb = vbuf + eb * (kItemTokCap * kMaxRank);
+                if (es == 0) pdl_wait();
+                if (MODE == kFused) {
+                    if (lane == 0)
+                        while (ld_acquire(&p.sync[M.item]) < M.n_sp) __nanosleep(32);
+                    __syncwarp();
+                    for (int e = lane; e < M.nt * M.r; e += 32) vb[e] = __ldcg(p.v + M.vbase + e);
+                    __syncwarp();
+                    // the item's last expand piece to read v resets its counter for
+                    // the launch slot's next use (which starts after this grid ends)
+                    if (lane == 0 && atomicAdd(&p.sync[M.item], 1) == M.n_sp + M.n_ep - 1)
+                        atomicExch(&p.sync[M.item], 0);
+                } else {  // v from v_in: block layout of slora_lora_expand
+                    const int vbk = p.v_blocks, rb = M.r / vbk;
+                    const int64_t stride = int64_t(p.nproj) * (p.NR / vbk);
+                    const int64_t base = int64_t(M.pi) * (p.NR / vbk) + M.vrow / vbk;
+                    for (int e = lane; e < M.nt * M.r; e += 32) {
+                        const int t = e / M.r, j = e % M.r;
+                        vb[e] = p.v_in[int64_t(j / rb) * stride + base + int64_t(t) * rb + j % rb];
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&vfull[eb]);
+                ++es;
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&mempty[m]);
+        }
+    } else if (warp == kWarpPublish) {
+        // ========================== publisher =============================
+        // Releases each finished shrink piece to the item's expand pieces
+        // (red.release.gpu; cumulative over the consumers' v stores observed
+        // through the mbarrier), off the consumers' critical path.
+        for (int s = 0; MODE == kFused; ++s) {
+            const int b = s & (kPub - 1);
+            mbar_wait_sleep(&pfull[b], (s / kPub) & 1);
+            const int item = pubq[b];
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&pempty[b]);
+            if (item < 0) break;
+            if (lane == 0 && MODE == kFused) red_release_add(&p.sync[item], 1);
         }
     } else {
         // ============================ consumers ===========================
         Ring rg;
         const int nvec = int(arow_bytes / 16);
-        // shrink: slot k holds rps_s rows; warp groups take alternate slots
-        const int ngroups = max(1, kConsumerWarps / rps_s);
-        const int gwarps = kConsumerWarps / ngroups;
-        const int grp = warp / gwarps, gw = warp % gwarps;
+        int xs = 0, es = 0, ps = 0;
+        auto publish = [&](int item) {  // hand a finished shrink piece (or the stop mark) to the publisher
+            const int b = ps & (kPub - 1);
+            if (ps >= kPub) mbar_wait(&pempty[b], ((ps / kPub) - 1) & 1);
+            if (tid == 0) pubq[b] = item;
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&pfull[b]);
+            ++ps;
+        };
         for (int i = 0;; ++i) {
-            const int ub = i & 1;
-            mbar_wait(&xfull[ub], (i >> 1) & 1);
-            const PieceMeta& M = meta[ub];
+            const int m = i & (kMeta - 1);
+            mbar_wait(&mfull[m], (i / kMeta) & 1);
+            const PieceMeta& M = meta[m];
             if (M.kind == kPieceStop) break;
             if (tid == 0 && i < 48) TRACE(64 + i);
             if (M.kind == kPieceS) {
                 // ------------------------------ shrink ------------------------------
-                const uint4* xr = reinterpret_cast<const uint4*>(xrows + size_t(ub) * kItemTokCap * K);
-                const int xstride = nvec;
-                const int nslots = (M.nrows + rps_s - 1) / rps_s;
-                for (int k = 0; k < nslots; ++k) {
-                    mbar_wait(&full[rg.slot], rg.lap & 1);
-                    if ((k % ngroups) == grp && !(p.dbg & 1)) {
-                        const int nrow = min(rps_s, M.nrows - k * rps_s);
-                        for (int q = gw; q < nrow; q += gwarps) {
-                            const uint4* arow = reinterpret_cast<const uint4*>(ring + size_t(rg.slot) * kSlotBytes +
-                                                                              size_t(q) * arow_bytes);
-                            const int j = M.row0 + k * rps_s + q;
-                            float* vo = p.v + M.vbase + j;
-                            switch (M.nt) {
-#define SLORA_SHRINK_CASE(N)                                          \
-    case N: {                                                         \
-        float out[N];                                                 \
-        shrink_row<T, N>(arow, xr, xstride, nvec, out, lane);         \
-        _Pragma("unroll") for (int t = 0; t < N; ++t) if (lane == t) vo[t * M.ra] = out[t]; \
-    } break;
-                                SLORA_SHRINK_CASE(1) SLORA_SHRINK_CASE(2) SLORA_SHRINK_CASE(3) SLORA_SHRINK_CASE(4)
+                const int xb = xs % kXBufs;
+                mbar_wait(&xfull[xb], (xs / kXBufs) & 1);
+                if (tid == 0 && i < 48) TRACE(256 + i);
+                const uint4* xsm = reinterpret_cast<const uint4*>(xrows + size_t(xb) * kItemTokCap * K);
+                float* rd = red + (xs & 1) * kRedFloats;
+                const int xvn = ((nvec + kConsumerWarps - 1) / kConsumerWarps + 31) / 32;
+                switch (M.nt * 8 + (xvn <= 1 ? 1 : (xvn == 2 ? 2 : 4))) {
+#define SLORA_SHRINK_CASE(N, X)                                                                                  \
+    case N * 8 + X:                                                                                            \
+        shrink_piece<T, N, X>(p, M, ring, xsm, nvec, arow_bytes, rps_s, full, empty, rg, ns, &xempty[xb], rd,    \
+                              warp, lane, i);                                                                   \
+        break;
+#ifdef SLORA_FEW_VARIANTS
+                    SLORA_SHRINK_CASE(1, 2)
+#else
+                    SLORA_SHRINK_CASE(1, 1) SLORA_SHRINK_CASE(2, 1) SLORA_SHRINK_CASE(3, 1) SLORA_SHRINK_CASE(4, 1)
+                    SLORA_SHRINK_CASE(1, 2) SLORA_SHRINK_CASE(2, 2) SLORA_SHRINK_CASE(3, 2) SLORA_SHRINK_CASE(4, 2)
+                    SLORA_SHRINK_CASE(1, 4) SLORA_SHRINK_CASE(2, 4) SLORA_SHRINK_CASE(3, 4) SLORA_SHRINK_CASE(4, 4)
+#endif
 #undef SLORA_SHRINK_CASE
-                                default: break;
-                            }
-                        }
-                    }
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(&empty[rg.slot]);
-                    rg.advance(ns);
+                    default: break;
                 }
-                if (MODE == kFused) {  // publish this piece's v rows to the item's expand pieces
-                    consumer_sync();
-                    if (tid == 0) {
-                        __threadfence();
-                        red_release_add(&p.sync[2 + M.item], 1);
-                    }
-                }
+                ++xs;
+                if (MODE == kFused) publish(M.item);
             } else {
                 // ------------------------------ expand ------------------------------
-                if (MODE == kFused) {
-                    if (tid == 0)
-                        while (ld_acquire(&p.sync[2 + M.item]) < M.n_sp) __nanosleep(64);
-                    consumer_sync();
-                    for (int e = tid; e < M.nt * M.r; e += kConsumerWarps * 32)
-                        vbuf[e] = __ldcg(p.v + M.vbase + e);
-                } else {  // v from v_in: block layout of slora_lora_expand
-                    const int vb = p.v_blocks, rb = M.r / vb;
-                    const int64_t stride = int64_t(p.nproj) * (p.NR / vb);
-                    const int64_t base = int64_t(M.pi) * (p.NR / vb) + M.vrow / vb;
-                    for (int e = tid; e < M.nt * M.r; e += kConsumerWarps * 32) {
-                        const int t = e / M.r, j = e % M.r;
-                        vbuf[e] = p.v_in[int64_t(j / rb) * stride + base + int64_t(t) * rb + j % rb];
-                    }
-                }
-                consumer_sync();
+                const int eb = es & 1;
+                mbar_wait(&vfull[eb], (es >> 1) & 1);
+                if (tid == 0 && i < 48) TRACE(256 + i);
+                const float* vb = vbuf + eb * (kItemTokCap * kMaxRank);
                 const uint32_t rowb = uint32_t(M.dcols * ES);
                 const int rps = kSlotBytes / int(rowb);
                 const int cvs = M.dcols / VE;
@@ -592,35 +852,27 @@ __global__ void __launch_bounds__(kThreads, 1) mbgmv_kernel(const __grid_constan
                 switch (M.nt) {
 #define SLORA_EXPAND_CASE(N)                                                                                   \
     case N:                                                                                                    \
-        expand_piece<T, N>(p, M, ring, rowb, rps, full, empty, rg, ns, vbuf, active, cv, lane, tg, ntg); \
+        expand_piece<T, N>(p, M, ring, rowb, rps, full, empty, rg, ns, vb, active, cv, lane, tg, ntg); \
         break;
+#ifdef SLORA_FEW_VARIANTS
+                    SLORA_EXPAND_CASE(1)
+#else
                     SLORA_EXPAND_CASE(1) SLORA_EXPAND_CASE(2) SLORA_EXPAND_CASE(3) SLORA_EXPAND_CASE(4)
+#endif
 #undef SLORA_EXPAND_CASE
                     default: break;
                 }
-                consumer_sync();  // vbuf reused by the next piece
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&vempty[eb]);
+                ++es;
             }
             __syncwarp();
             if (tid == 0 && i < 48) TRACE(112 + i);
-            if (lane == 0) mbar_arrive(&xempty[ub]);
+            if (lane == 0) mbar_arrive(&mempty[m]);
         }
+        if (MODE == kFused) publish(-1);
     }
-    // ---- teardown: the last CTA out resets this launch slot's counters
     if (tid == 0) TRACE(2);
-    __syncthreads();
-    if (tid == 0) {
-        __threadfence();
-        s_last = atomicAdd(&p.sync[1], 1) == int(gridDim.x) - 1;
-    }
-    __syncthreads();
-    if (s_last) {
-        for (int e = tid; e < p.n_items; e += blockDim.x) p.sync[2 + e] = 0;
-        if (tid == 0) {
-            p.sync[0] = 0;
-            p.sync[1] = 0;
-        }
-        __threadfence();
-    }
 }
 
 static bool pdl_enabled() {

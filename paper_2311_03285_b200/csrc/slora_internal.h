@@ -33,14 +33,17 @@ struct DevItem {
     int32_t n_sp;      // number of shrink pieces of this item (fused dependency count)
     float scale;
     int32_t seg;
-    int32_t pad[4];
+    int32_t n_ep;      // number of expand pieces of this item (fused: the last one resets the counter)
+    int32_t pad[3];
 };
 static_assert(sizeof(DevItem) == 64, "DevItem layout");
 
-// A piece = the unit of dynamic scheduling.  kind 0 (shrink): rows
-// [a, a+b) of the item's stored A rows, full K.  kind 1 (expand): all B rows,
-// output columns [a, a+b).  Tickets hand out all shrink pieces before any
-// expand piece, so an expand piece only ever waits on earlier tickets.
+// A piece = the unit of scheduling.  kind 0 (shrink): rows [a, a+b) of the
+// item's stored A rows, full K.  kind 1 (expand): all B rows, output columns
+// [a, a+b).  The host assigns pieces to the persistent CTAs (LPT on bytes,
+// api.cpp schedule_pieces); every CTA runs all its shrink pieces before any
+// expand piece, so an expand piece only ever waits on shrink pieces, which
+// never wait (no deadlock with all CTAs resident).
 struct DevPiece {
     int32_t kind, item, a, b;
 };
@@ -50,11 +53,18 @@ constexpr int kItemTokCap = 4;   // tokens per item (larger segments are chunked
 constexpr int kMaxRank = 64;     // max rank of the MBGMV path
 constexpr int kShrinkRows = 16;  // A rows per shrink piece
 constexpr int kConsumerWarps = 8;
-constexpr int kThreads = (kConsumerWarps + 3) * 32;  // + 2 streamer warps + resolver warp
+// warp roles: 0-7 consumers, then streamer 0, resolver, streamer 1, expand-v
+// prefetcher, shrink publisher
+constexpr int kWarpStreamer0 = kConsumerWarps, kWarpResolver = kConsumerWarps + 1,
+              kWarpStreamer1 = kConsumerWarps + 2, kWarpPrefetch = kConsumerWarps + 3,
+              kWarpPublish = kConsumerWarps + 4;
+constexpr int kThreads = (kConsumerWarps + 5) * 32;
 constexpr int kMaxChunks = 8;    // pages one stored A row spans (TP q/k/v: N)
 constexpr int kSlotBytes = 32 * 1024;  // ring slot
 constexpr int kMaxSlots = 16;
-constexpr int kLaunchSlots = 8;  // rotating per-launch counter/workspace slots
+constexpr int kMeta = 4;         // resolved-piece ring (resolver runs up to kMeta-1 pieces ahead)
+constexpr int kLaunchSlots = 8;
+constexpr int kTraceSlots = 1024;  // debug trace: globaltimer events per traced CTA (16 CTAs)  // rotating per-launch counter/workspace slots
 
 enum Mode : int { kFused = 0, kShrink = 1, kExpand = 2 };
 enum DType : int { kF32 = 0, kF16 = 1, kBF16 = 2 };
@@ -65,10 +75,11 @@ struct LoraParams {
     int64_t page_elems;           // P
     const int32_t* tok_idx;
     const DevItem* items;
-    const DevPiece* pieces;
+    const DevPiece* pieces;       // grouped by CTA: CTA b runs pieces [cta_off[b], cta_off[b+1])
+    const int32_t* cta_off;       // grid + 1 entries
     int32_t n_pieces;
     int32_t n_items;
-    int32_t* sync;                // this launch's slot: [0] tickets, [1] exits, [2..] item done counts
+    int32_t* sync;                // this launch's slot: per-item done counters (self-resetting)
     int32_t nproj;
     int32_t proj_ids[4];
     int32_t layer;

@@ -15,7 +15,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libslora.so")
+LIB_PATH = os.environ.get("SLORA_LIB") or os.path.join(_HERE, "libslora.so")  # SLORA_LIB: alternate build (experiments)
 
 DTYPES = {"f32": 0, "f16": 1, "bf16": 2}
 ESIZE = {"f32": 4, "f16": 2, "bf16": 2}
@@ -256,10 +256,10 @@ class Pool:
         _check(lib().slora_sync(self.h, _stream(stream)))
 
     def debug_trace(self) -> np.ndarray:
-        """[16 CTAs, 64 events] globaltimer ns of the last traced launches."""
-        out = np.zeros(4096, np.int64)
-        _check(lib().slora_debug_trace(self.h, out.ctypes.data_as(_PI64), 4096))
-        return out.reshape(16, 256)
+        """[16 CTAs, 1024 events] globaltimer ns of the last traced launches."""
+        out = np.zeros(16 * 1024, np.int64)
+        _check(lib().slora_debug_trace(self.h, out.ctypes.data_as(_PI64), 16 * 1024))
+        return out.reshape(16, 1024)
 
 
 class Batch:
