@@ -328,7 +328,7 @@ def run_ours(args):
         roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
                     "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": traffic,
                     "peak_source": f"{peak_kind} copy bandwidth (MEASURED_PEAKS.json hbm_gbs)",
-                    "kernel": f"mbgmv_kernel<{cfg.dtype}, kFused> (MBGMV cluster gather-shrink-expand)",
+                    "kernel": f"mbgmv_kernel<{cfg.dtype}, kFused> (persistent warp-specialized gather-shrink-expand)",
                     "alg_bytes_per_launch": {"qkv": W.bytes_qkv, "o": W.bytes_o},
                     "avg_launch_us_in_step": round(1e3 * ms / (2 * layers), 2),
                     "serialized_launch_us": {"qkv": round(1e3 * float(np.mean(dur["qkv"])), 2),
