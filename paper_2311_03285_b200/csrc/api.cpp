@@ -120,7 +120,7 @@ KernelCfg make_kernel_cfg(int mode, int64_t K, int64_t D, int64_t P, int es, int
     k.mode = mode;
     k.K = K;
     k.D = D;
-    if (mode != kExpand && (K * es > kSlotBytes || (K * es) % 16)) return k;
+    if (mode != kExpand && (K * es + 16 > kSlotBytes || (K * es) % 16)) return k;
     static int forced = [] {
         const char* s = getenv("SLORA_DCHUNK");
         return s ? atoi(s) : 0;
@@ -134,7 +134,7 @@ KernelCfg make_kernel_cfg(int mode, int64_t K, int64_t D, int64_t P, int es, int
     }
     const size_t budget = size_t(226) * 1024;
     const size_t base = lora_smem_bytes(mode, K, k.dchunk, 0, es);
-    int ns = int((budget - base) / kSlotBytes);
+    int ns = int((budget - base) / lora_slot_stride(mode, K, es));
     ns = std::min(ns, kMaxSlots);
     static const int ns_cap = [] {  // experiment knob: cap the ring depth
         const char* e = getenv("SLORA_NS");
@@ -299,6 +299,12 @@ extern "C" slora_status slora_pool_create(const slora_pool_config* cfg, slora_po
         p->kcfg[1] = make_kernel_cfg(kShrink, H, P, P, es, dt);
         p->kcfg[2] = make_kernel_cfg(kShrink, cfg->tp_size > 1 ? P : H, P, P, es, dt);
         p->kcfg[3] = make_kernel_cfg(kExpand, P, P, P, es, dt);
+        if (const char* vb = getenv("SLORA_VERBOSE"); vb && atoi(vb) > 0)
+            for (int c = 0; c < 4; ++c)
+                fprintf(stderr, "slora: kcfg[%d] mode=%d K=%lld D=%lld dchunk=%lld ns=%d smem=%zu grid=%d ok=%d\n", c,
+                        p->kcfg[c].mode, (long long)p->kcfg[c].K, (long long)p->kcfg[c].D,
+                        (long long)p->kcfg[c].dchunk, p->kcfg[c].ns, p->kcfg[c].smem, p->kcfg[c].grid,
+                        int(p->kcfg[c].ok));
         const char* tr = getenv("SLORA_TRACE");
         if (tr && atoi(tr) == 1) {
             if ((e = cudaMalloc(&p->trace_dev, 16 * kTraceSlots * sizeof(long long)))) return cleanup(e, "cudaMalloc trace");

@@ -258,10 +258,23 @@ struct SmemLayout {
     size_t bars, meta, pubq, vbuf, red, xrows, ring, total;
 };
 constexpr int kPub = 4;        // shrink-done queue (consumers -> publisher warp)
-constexpr int kXBufs = 1;      // x row buffers (consumers copy x to registers and release at once)
 constexpr int kNumBars = 2 * kMaxSlots + 4 + 2 * kMeta + 4 + 2 * kPub;
 constexpr int kRedFloats = kConsumerWarps * kShrinkRows * kItemTokCap;  // per buffer
 __host__ __device__ inline size_t al128(size_t x) { return (x + 127) & ~size_t(127); }
+// Shrink rows sit in a slot at a stride of (row bytes + 16) and the slot
+// stride is offset by 16 B per row of the previous slot (mod 128), so that 8
+// consecutive A rows -- the 8 row addresses of an ldmatrix -- hit 8 distinct
+// 16-byte bank groups (conflict-free tensor-core operand loads).
+__host__ __device__ inline int shrink_rows_per_slot(int64_t K, int es) {
+    return int((kSlotBytes + 128) / (K * es + 16));  // rows * (K*es + 16) <= kSlotBytes + 128 < slot_stride
+}
+// x row buffers: two (the next shrink piece's x loads while this one
+// computes) unless the rows are wide (16 KB: one, to keep the ring deep)
+__host__ __device__ inline int x_buffers(int64_t K, int es) { return K * es <= 8192 ? 2 : 1; }
+__host__ __device__ inline size_t slot_stride(int mode, int64_t K, int es) {
+    const int rps = mode == kExpand ? 0 : shrink_rows_per_slot(K, es);
+    return size_t(kSlotBytes) + 256 + size_t((16 * rps) & 127);
+}
 __host__ __device__ inline SmemLayout smem_layout(int mode, int64_t K, int64_t dchunk, int ns, int es) {
     (void)dchunk;
     SmemLayout L{};
@@ -271,21 +284,22 @@ __host__ __device__ inline SmemLayout smem_layout(int mode, int64_t K, int64_t d
     L.meta = off;
     off = al128(off + kMeta * sizeof(PieceMeta));
     L.pubq = off;
-    off = al128(off + kPub * sizeof(int32_t));
+    off = al128(off + kPub * sizeof(int32_t) + 64);  // + 16 zero bytes at +64 (padding-row ldmatrix source)
     L.vbuf = off;
     off = al128(off + (mode != kShrink ? size_t(2) * kItemTokCap * kMaxRank * 4 : 0));
     L.red = off;
     off = al128(off + (mode != kExpand ? size_t(2) * kRedFloats * 4 : 0));
     L.xrows = off;
-    off = al128(off + (mode != kExpand ? size_t(kXBufs) * kItemTokCap * K * es : 0));
+    off = al128(off + (mode != kExpand ? size_t(x_buffers(K, es)) * kItemTokCap * (K * es + 16) : 0));  // x rows, staggered
     L.ring = off;
-    off = al128(off + size_t(ns) * kSlotBytes);
+    off = al128(off + size_t(ns) * slot_stride(mode, K, es));
     L.total = off;
     return L;
 }
 size_t lora_smem_bytes(int mode, int64_t K, int64_t dchunk, int ns, int esize) {
     return smem_layout(mode, K, dchunk, ns, esize).total;
 }
+size_t lora_slot_stride(int mode, int64_t K, int esize) { return slot_stride(mode, K, esize); }
 
 struct Ring {
     int slot = 0;
@@ -329,7 +343,7 @@ __device__ __forceinline__ float xreduce(float (&v)[VV], int lane) {
 // complete.  Warps do equal work per slot.
 template <typename T, int NT, int XV>
 __device__ __forceinline__ void shrink_piece(const LoraParams& p, const PieceMeta& M, const unsigned char* ring,
-                                             const uint4* xs, int nvec, uint32_t arow_bytes, int rps_s,
+                                             size_t SS, const uint4* xs, int nvec, uint32_t srow, int rps_s,
                                              uint64_t* full, uint64_t* empty, Ring& rg, int ns, uint64_t* xempty,
                                              float* red, int warp, int lane, int i) {
     constexpr int NTP = NT == 3 ? 4 : NT;
@@ -344,7 +358,7 @@ __device__ __forceinline__ void shrink_piece(const LoraParams& p, const PieceMet
         const int idx = v0 + lane + 32 * k;
         li[k] = min(idx, nvec - 1);  // clamped: x is zero there, so the product vanishes
 #pragma unroll
-        for (int t = 0; t < NT; ++t) xv[t][k] = idx < v1 ? xs[t * nvec + idx] : make_uint4(0, 0, 0, 0);
+        for (int t = 0; t < NT; ++t) xv[t][k] = idx < v1 ? xs[t * int(srow / 16) + idx] : make_uint4(0, 0, 0, 0);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(xempty);  // x slice in registers: buffer free for the next shrink piece
@@ -364,12 +378,12 @@ __device__ __forceinline__ void shrink_piece(const LoraParams& p, const PieceMet
         if (k == 0 && warp == 0 && lane == 0 && i < 48) TRACE(304 + i);
         const int nrow = min(rps_s, nrows - rbase);
         if (math) {
-            const unsigned char* sb = ring + size_t(rg.slot) * kSlotBytes;
+            const unsigned char* sb = ring + size_t(rg.slot) * SS;
             for (int q0 = 0; q0 < nrow; q0 += RQ) {
                 uint4 av[RQ][XV];
 #pragma unroll
                 for (int j = 0; j < RQ; ++j) {
-                    const uint4* rp = reinterpret_cast<const uint4*>(sb + size_t(min(q0 + j, nrow - 1)) * arow_bytes);
+                    const uint4* rp = reinterpret_cast<const uint4*>(sb + size_t(min(q0 + j, nrow - 1)) * srow);
 #pragma unroll
                     for (int kk = 0; kk < XV; ++kk) av[j][kk] = rp[li[kk]];
                 }
@@ -411,11 +425,132 @@ __device__ __forceinline__ void shrink_piece(const LoraParams& p, const PieceMet
     }
 }
 
+// ------------------------------------------------ tensor-core shrink (HMMA)
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+                 : "r"(addr));
+}
+template <typename T> struct MmaOp {  // fp32: never used (no TF32 for fp32 inputs)
+    __device__ static void run(float (&)[4], uint32_t, uint32_t, uint32_t, uint32_t) {}
+};
+template <> struct MmaOp<__half> {
+    __device__ static void run(float (&d)[4], uint32_t a0, uint32_t a2, uint32_t b0, uint32_t b1) {
+        asm volatile(
+            "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
+            "{%0, %1, %2, %3};"
+            : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+            : "r"(a0), "r"(0u), "r"(a2), "r"(0u), "r"(b0), "r"(b1));
+    }
+};
+template <> struct MmaOp<__nv_bfloat16> {
+    __device__ static void run(float (&d)[4], uint32_t a0, uint32_t a2, uint32_t b0, uint32_t b1) {
+        asm volatile(
+            "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
+            "{%0, %1, %2, %3};"
+            : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+            : "r"(a0), "r"(0u), "r"(a2), "r"(0u), "r"(b0), "r"(b1));
+    }
+};
+
+// Shrink of one piece on the tensor cores (fp16/bf16): D[token][row] over
+// the warp's K-slice with mma.m16n8k16 (M = tokens, rows 8-15 of A are the
+// zero register; N = 8 stored A rows; K = 16), fragments loaded with ldmatrix
+// from the staggered x rows and A rows (conflict-free).  Rows go 8 at a time
+// (the slots holding them are waited for, then released); the 8 warps'
+// partials meet in smem (red) as on the CUDA-core path.  Exact products,
+// fp32 accumulation in a fixed order (deterministic).  Requires K % 256 == 0
+// and a power-of-two rows-per-slot.
+template <typename T>
+__device__ __forceinline__ void shrink_piece_mma(const LoraParams& p, const PieceMeta& M, const unsigned char* ring,
+                                                 size_t SS, const unsigned char* xs, uint32_t zero16, int K,
+                                                 uint32_t srow, int lg_rps, uint64_t* full, uint64_t* empty, Ring& rg,
+                                                 int ns, uint64_t* xempty, float* red, int warp, int lane, int i) {
+    constexpr int ES = sizeof(T);
+    const int kslice = K / kConsumerWarps;  // elements of K per warp (multiple of 16)
+    const int k0w = warp * kslice;
+    const int mi = lane >> 3, rr = lane & 7;  // ldmatrix: this lane addresses row rr of matrix mi
+    const int g = lane >> 2, c = lane & 3;    // mma fragment coordinates
+    const int nt = M.nt, nrows = M.nrows;
+    // x operand rows: tokens >= nt read 16 zero bytes (and do not advance)
+    const bool xreal = rr < nt;
+    const uint32_t xbase = xreal ? smem_u32(xs) + uint32_t(rr) * srow + uint32_t(k0w + mi * 8) * ES : zero16;
+    const uint32_t xadv = xreal ? 32u * ES : 0u;  // two k-steps per ldmatrix.x4
+    const bool math = !(p.dbg & 1);
+    const int rps = 1 << lg_rps;
+    const int nslots = (nrows + rps - 1) >> lg_rps;
+    const int s0 = rg.slot;
+    const uint32_t l0 = rg.lap;
+    const uint32_t ring_u32 = smem_u32(ring);
+    int waited = 0, released = 0;
+    bool xfree = false;
+    for (int gb = 0; gb < nrows; gb += 8) {
+        const int ge = min(gb + 8, nrows);
+        const int need = (ge - 1) >> lg_rps;  // last slot this group reads
+        for (; waited <= need; ++waited) {
+            int a = s0 + waited;
+            uint32_t lap = l0;
+            if (a >= ns) { a -= ns; ++lap; }
+            mbar_wait(&full[a], lap & 1);
+        }
+        if (gb == 0 && warp == 0 && lane == 0 && i < 48) TRACE(304 + i);
+        if (math) {
+            // A-row operand: this lane addresses stored row min(gb + rr, ge - 1) (padding rows repeat a real
+            // row; their columns of D are discarded)
+            const int row = min(gb + rr, ge - 1);
+            int a = s0 + (row >> lg_rps);
+            if (a >= ns) a -= ns;
+            const uint32_t bbase = ring_u32 + uint32_t(a) * uint32_t(SS) + uint32_t(row & (rps - 1)) * srow +
+                                   uint32_t(k0w + mi * 8) * ES;
+            float d[4] = {0.f, 0.f, 0.f, 0.f};
+            const int npair = kslice >> 5;  // k-step pairs
+#pragma unroll 4
+            for (int kp = 0; kp < npair; ++kp) {
+                uint32_t xa0, xa1, xa2, xa3, b0, b1, b2, b3;
+                ldsm_x4(xbase + uint32_t(kp) * xadv, xa0, xa1, xa2, xa3);
+                ldsm_x4(bbase + uint32_t(kp) * (32u * ES), b0, b1, b2, b3);
+                MmaOp<T>::run(d, xa0, xa1, b0, b1);
+                MmaOp<T>::run(d, xa2, xa3, b2, b3);
+            }
+            // d0, d1: token g, rows gb + 2c, gb + 2c + 1 (d2, d3: tokens g + 8, zero)
+            if (g < nt) {
+                if (gb + 2 * c < nrows) red[(warp * kShrinkRows + gb + 2 * c) * kItemTokCap + g] = d[0];
+                if (gb + 2 * c + 1 < nrows) red[(warp * kShrinkRows + gb + 2 * c + 1) * kItemTokCap + g] = d[1];
+            }
+        }
+        if (ge >= nrows && !xfree) {  // the last group: x rows no longer needed
+            __syncwarp();
+            if (lane == 0) mbar_arrive(xempty);
+            xfree = true;
+        }
+        // release the slots wholly consumed by this group
+        const int fin = (ge >= nrows) ? nslots : (ge >> lg_rps);
+        __syncwarp();
+        for (; released < fin; ++released) {
+            int a = s0 + released;
+            if (a >= ns) a -= ns;
+            if (lane == 0) mbar_arrive(&empty[a]);
+        }
+    }
+    for (int j = 0; j < nslots; ++j) rg.advance(ns);
+    if (warp == 0 && lane == 0 && i < 48) TRACE(352 + i);
+    consumer_sync();  // all warps' partials of the piece are in red
+    if (warp == 0 && lane == 0 && i < 48) TRACE(400 + i);
+    const int tid = warp * 32 + lane;
+    if (tid < nrows * nt && math) {
+        const int q = tid / nt, t = tid % nt;
+        float sum = 0.f;
+#pragma unroll
+        for (int w = 0; w < kConsumerWarps; ++w) sum += red[(w * kShrinkRows + q) * kItemTokCap + t];
+        p.v[M.vbase + int64_t(t) * M.ra + M.row0 + q] = sum;
+    }
+}
+
 // Expand of one piece (all B rows of the item over this piece's columns)
 // for NT tokens: y_t += scale * v_t B over this thread's 16-byte column
 // vector; walks ring slots every `rps` rows.
 template <typename T, int NT>
-__device__ __forceinline__ void expand_piece(const LoraParams& p, const PieceMeta& M, const unsigned char* ring,
+__device__ __forceinline__ void expand_piece(const LoraParams& p, const PieceMeta& M, const unsigned char* ring, size_t SS,
                                              uint32_t rowb, int rps, uint64_t* full, uint64_t* empty, Ring& rg,
                                              int ns, const float* vbuf, bool active, int cv, int lane, int tg,
                                              int ntg) {
@@ -459,7 +594,7 @@ __device__ __forceinline__ void expand_piece(const LoraParams& p, const PieceMet
             if (sq < 240) TRACE(512 + sq);
         }
         if (active) {
-            const uint4* sl = reinterpret_cast<const uint4*>(ring + size_t(rg.slot) * kSlotBytes) + cv;
+            const uint4* sl = reinterpret_cast<const uint4*>(ring + size_t(rg.slot) * SS) + cv;
             const int nrow = min(rps, r - j0);
             if ((nrow & 3) == 0) {  // the usual case (ranks are multiples of 4): 4 rows at a time, loads first
                 for (int q0 = 0; q0 < nrow; q0 += 4) {
@@ -469,7 +604,8 @@ __device__ __forceinline__ void expand_piece(const LoraParams& p, const PieceMet
                     for (int q = 0; q < 4; ++q) {
                         bv[q] = sl[(q0 + q) * rowv];
 #pragma unroll
-                        for (int t = 0; t < NT; ++t) vv[q][t] = vbuf[t * r + j0 + q0 + q];
+                        for (int t = 0; t < NT; ++t)  // tokens this thread does not own: v = 0 (branch-free FMAs)
+                            vv[q][t] = (own >> t & 1u) ? vbuf[t * r + j0 + q0 + q] : 0.f;
                     }
 #pragma unroll
                     for (int q = 0; q < 4; ++q) {
@@ -477,9 +613,8 @@ __device__ __forceinline__ void expand_piece(const LoraParams& p, const PieceMet
                         V::to_f32(bv[q], b);
 #pragma unroll
                         for (int t = 0; t < NT; ++t)
-                            if (own >> t & 1u)
 #pragma unroll
-                                for (int e = 0; e < VE; ++e) acc[t][e] = fmaf(vv[q][t], b[e], acc[t][e]);
+                            for (int e = 0; e < VE; ++e) acc[t][e] = fmaf(vv[q][t], b[e], acc[t][e]);
                     }
                 }
             } else {
@@ -544,7 +679,10 @@ __global__ void __launch_bounds__(kThreads, 1) mbgmv_kernel(const __grid_constan
     unsigned char* ring = smem + L.ring;                    // [ns][kSlotBytes]
     const int ns = p.ns;
     const uint32_t arow_bytes = uint32_t(K * ES);            // shrink row (full K)
-    const int rps_s = max(1, kSlotBytes / int(arow_bytes));  // shrink rows per slot
+    const uint32_t srow = arow_bytes + 16;                    // its smem stride (staggered; x rows too)
+    const int rps_s = shrink_rows_per_slot(K, ES);            // shrink rows per slot
+    const size_t SS = slot_stride(MODE, K, ES);               // ring slot stride
+    const int nxb = x_buffers(K, ES);                         // x row buffers
     constexpr int kRoles = kConsumerWarps + 3;               // mempty arrivals: consumers, 2 streamers, prefetcher
 
     if (tid == 0) TRACE(0);
@@ -567,6 +705,7 @@ __global__ void __launch_bounds__(kThreads, 1) mbgmv_kernel(const __grid_constan
             mbar_init(&pfull[b], kConsumerWarps);
             mbar_init(&pempty[b], 1);
         }
+        *reinterpret_cast<uint4*>(smem + L.pubq + 64) = make_uint4(0, 0, 0, 0);
         fence_mbar_init();
     }
     __syncthreads();
@@ -686,7 +825,7 @@ __global__ void __launch_bounds__(kThreads, 1) mbgmv_kernel(const __grid_constan
                 }
                 if (lane == 0) mbar_arrive_expect_tx(&full[rg.slot], uint32_t(nrow) * rowb);
                 __syncwarp();
-                unsigned char* sbase = ring + size_t(rg.slot) * kSlotBytes;
+                unsigned char* sbase = ring + size_t(rg.slot) * SS;
                 if (S) {
                     // row q: K elements over arp pages of P (TP q/k/v rows span N pages)
                     const int nc = nrow * M.arp;
@@ -696,7 +835,7 @@ __global__ void __launch_bounds__(kThreads, 1) mbgmv_kernel(const __grid_constan
                         const int q = ww / M.arp, ch = ww % M.arp;
                         const int64_t k0 = int64_t(ch) * P;
                         const int64_t len = min(P, K - k0) / sp;
-                        bulk_g2s(sbase + size_t(q) * rowb + (k0 + h * len) * ES,
+                        bulk_g2s(sbase + size_t(q) * srow + (k0 + h * len) * ES,
                                  pool + int64_t(M.pages[(base + q) * M.arp + ch]) * P + h * len, uint32_t(len * ES),
                                  &full[rg.slot]);
                     }
@@ -714,15 +853,16 @@ __global__ void __launch_bounds__(kThreads, 1) mbgmv_kernel(const __grid_constan
                 waited = true;
             }
             if (S) {  // x rows of the item's tokens
-                const int xb = xs % kXBufs;
+                const int xb = xs % nxb;
                 if (sid == 0) {
-                    if (xs >= kXBufs) mbar_wait_sleep(&xempty[xb], ((xs / kXBufs) - 1) & 1);
+                    if (xs >= nxb) mbar_wait_sleep(&xempty[xb], ((xs / nxb) - 1) & 1);
                     const bool xcopy = !(p.dbg & (4 | 16));  // debug bit 16: no x rows
                     if (lane == 0) mbar_arrive_expect_tx(&xfull[xb], xcopy ? uint32_t(M.nt) * arow_bytes : 0u);
                     __syncwarp();
                     if (lane < M.nt && xcopy) {
                         const T* x = reinterpret_cast<const T*>(p.x);
-                        bulk_g2s(xrows + (size_t(xb) * kItemTokCap + lane) * K, x + int64_t(M.tok[lane]) * p.ldx,
+                        bulk_g2s(reinterpret_cast<unsigned char*>(xrows) + (size_t(xb) * kItemTokCap + lane) * srow,
+                                 x + int64_t(M.tok[lane]) * p.ldx,
                                  arow_bytes, &xfull[xb]);
                     }
                 }
@@ -793,6 +933,13 @@ __global__ void __launch_bounds__(kThreads, 1) mbgmv_kernel(const __grid_constan
         // ============================ consumers ===========================
         Ring rg;
         const int nvec = int(arow_bytes / 16);
+        // tensor-core shrink for 16-bit types when the shapes allow (fp32 keeps
+        // the CUDA-core path: no TF32); SLORA_DBG bit 32 forces CUDA cores
+        int lg_rps = 0;
+        while ((2 << lg_rps) <= rps_s) ++lg_rps;
+        const bool use_mma = ES == 2 && (K % 256) == 0 && (1 << lg_rps) == rps_s && (8 >> lg_rps) <= ns &&
+                             !(p.dbg & 32);
+        const uint32_t zero16 = smem_u32(smem + L.pubq + 64);
         int xs = 0, es = 0, ps = 0;
         auto publish = [&](int item) {  // hand a finished shrink piece (or the stop mark) to the publisher
             const int b = ps & (kPub - 1);
@@ -810,16 +957,21 @@ __global__ void __launch_bounds__(kThreads, 1) mbgmv_kernel(const __grid_constan
             if (tid == 0 && i < 48) TRACE(64 + i);
             if (M.kind == kPieceS) {
                 // ------------------------------ shrink ------------------------------
-                const int xb = xs % kXBufs;
-                mbar_wait(&xfull[xb], (xs / kXBufs) & 1);
+                const int xb = xs % nxb;
+                mbar_wait(&xfull[xb], (xs / nxb) & 1);
                 if (tid == 0 && i < 48) TRACE(256 + i);
-                const uint4* xsm = reinterpret_cast<const uint4*>(xrows + size_t(xb) * kItemTokCap * K);
+                const uint4* xsm = reinterpret_cast<const uint4*>(reinterpret_cast<const unsigned char*>(xrows) +
+                                                                  size_t(xb) * kItemTokCap * srow);
                 float* rd = red + (xs & 1) * kRedFloats;
                 const int xvn = ((nvec + kConsumerWarps - 1) / kConsumerWarps + 31) / 32;
+                if (use_mma) {
+                    shrink_piece_mma<T>(p, M, ring, SS, reinterpret_cast<const unsigned char*>(xsm), zero16, int(K),
+                                        srow, lg_rps, full, empty, rg, ns, &xempty[xb], rd, warp, lane, i);
+                } else
                 switch (M.nt * 8 + (xvn <= 1 ? 1 : (xvn == 2 ? 2 : 4))) {
 #define SLORA_SHRINK_CASE(N, X)                                                                                  \
     case N * 8 + X:                                                                                            \
-        shrink_piece<T, N, X>(p, M, ring, xsm, nvec, arow_bytes, rps_s, full, empty, rg, ns, &xempty[xb], rd,    \
+        shrink_piece<T, N, X>(p, M, ring, SS, xsm, nvec, srow, rps_s, full, empty, rg, ns, &xempty[xb], rd,      \
                               warp, lane, i);                                                                   \
         break;
 #ifdef SLORA_FEW_VARIANTS
@@ -852,7 +1004,7 @@ __global__ void __launch_bounds__(kThreads, 1) mbgmv_kernel(const __grid_constan
                 switch (M.nt) {
 #define SLORA_EXPAND_CASE(N)                                                                                   \
     case N:                                                                                                    \
-        expand_piece<T, N>(p, M, ring, rowb, rps, full, empty, rg, ns, vb, active, cv, lane, tg, ntg); \
+        expand_piece<T, N>(p, M, ring, SS, rowb, rps, full, empty, rg, ns, vb, active, cv, lane, tg, ntg); \
         break;
 #ifdef SLORA_FEW_VARIANTS
                     SLORA_EXPAND_CASE(1)

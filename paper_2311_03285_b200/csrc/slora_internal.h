@@ -112,6 +112,7 @@ struct KernelCfg {
 
 // smem bytes for a launch (host and device agree via smem_layout in kernels.cu)
 size_t lora_smem_bytes(int mode, int64_t K, int64_t dchunk, int ns, int esize);
+size_t lora_slot_stride(int mode, int64_t K, int esize);  // ring slot stride (bytes)
 int lora_max_ctas(int mode, int dtype, size_t smem);
 cudaError_t launch_lora(const LoraParams& p, int mode, int dtype, int grid, cudaStream_t s, size_t smem);
 cudaError_t configure_lora_kernels(int device);
