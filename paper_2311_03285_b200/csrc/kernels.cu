@@ -153,6 +153,9 @@ __device__ __forceinline__ void red_release_add(int* p, int v) {
     asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+__device__ __forceinline__ void prefetch_l1(const void* p) {
+    asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
+}
 __device__ __forceinline__ long long gtimer() {
     long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -268,6 +271,8 @@ __host__ __device__ inline size_t al128(size_t x) { return (x + 127) & ~size_t(1
 __host__ __device__ inline int shrink_rows_per_slot(int64_t K, int es) {
     return int((kSlotBytes + 128) / (K * es + 16));  // rows * (K*es + 16) <= kSlotBytes + 128 < slot_stride
 }
+// expand rows (B row slices of rowb bytes) also sit at a 16-byte stagger
+__host__ __device__ inline int expand_rows_per_slot(uint32_t rowb) { return int((kSlotBytes + 128) / (rowb + 16)); }
 // x row buffers: two (the next shrink piece's x loads while this one
 // computes) unless the rows are wide (16 KB: one, to keep the ring deep)
 __host__ __device__ inline int x_buffers(int64_t K, int es) { return K * es <= 8192 ? 2 : 1; }
@@ -546,6 +551,164 @@ __device__ __forceinline__ void shrink_piece_mma(const LoraParams& p, const Piec
     }
 }
 
+// Expand of one piece on the tensor cores (fp16/bf16): D[col][token] =
+// B^T v^T with mma.m16n8k16 (M = 16 output columns, A operand = B rows read
+// transposed by ldmatrix.trans from the staggered slot rows; N = 8 tokens,
+// B operand = v split into a 16-bit high and low part (two MMAs: v = hi + lo
+// to ~2^-22, so the expand keeps fp32-grade accuracy); K = 16 rank rows,
+// i.e. two slots of 8 rows).  The warp owns M.dcols/8 columns (m-tiles of
+// 16); D stays in registers over the whole piece and is added once into y
+// (y = y + scale*D, one rounding).  Requires dcols % 128 == 0, r % 8 == 0,
+// 8 rows per slot.
+template <typename T> struct MmaFull;
+template <> struct MmaFull<__half> {
+    __device__ static void run(float* d, uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
+                               uint32_t b1) {
+        asm volatile(
+            "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
+            "{%0, %1, %2, %3};"
+            : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+            : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+    }
+    __device__ static uint32_t pack(float lo, float hi) {
+        __half2 h = __floats2half2_rn(lo, hi);
+        return *reinterpret_cast<uint32_t*>(&h);
+    }
+    __device__ static float2 unpack(uint32_t u) { return __half22float2(*reinterpret_cast<__half2*>(&u)); }
+};
+template <> struct MmaFull<__nv_bfloat16> {
+    __device__ static void run(float* d, uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
+                               uint32_t b1) {
+        asm volatile(
+            "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
+            "{%0, %1, %2, %3};"
+            : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+            : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+    }
+    __device__ static uint32_t pack(float lo, float hi) {
+        __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
+        return *reinterpret_cast<uint32_t*>(&h);
+    }
+    __device__ static float2 unpack(uint32_t u) { return __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&u)); }
+};
+template <> struct MmaFull<float> {  // never used (fp32 keeps the CUDA-core expand)
+    __device__ static void run(float*, uint32_t, uint32_t, uint32_t, uint32_t, uint32_t, uint32_t) {}
+    __device__ static uint32_t pack(float, float) { return 0; }
+    __device__ static float2 unpack(uint32_t) { return make_float2(0.f, 0.f); }
+};
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+                 : "r"(addr));
+}
+
+constexpr int kMaxMT = 16;  // m-tiles (16 columns) per warp: dcols <= 2048
+template <typename T>
+__device__ __forceinline__ void expand_piece_mma(const LoraParams& p, const PieceMeta& M, const unsigned char* ring,
+                                                 size_t SS, uint32_t erow, uint64_t* full, uint64_t* empty, Ring& rg,
+                                                 int ns, const float* vbuf, int warp, int lane, int i) {
+    using MF = MmaFull<T>;
+    constexpr int ES = sizeof(T);
+    const int r = M.r, nt = M.nt;
+    const int g = lane >> 2, c = lane & 3;
+    const int mi = lane >> 3, rr = lane & 7;
+    const int nks = (r + 15) >> 4;  // k-steps of 16 rank rows (<= 4)
+    const bool math = !(p.dbg & 2);
+    // v operand (col layout, k = rank row, n = token), per k-step: b0b1 = v[tok g][16ks + 2c .. +1],
+    // b2b3 = v[tok g][16ks + 8 + 2c .. +1]; split v = hi + lo
+    auto vfrag = [&](int ks, int h, uint32_t& hi, uint32_t& lo) {
+        const int j = 16 * ks + 8 * h + 2 * c;
+        const float v0 = (g < nt && j < r) ? vbuf[g * r + j] : 0.f;
+        const float v1 = (g < nt && j + 1 < r) ? vbuf[g * r + j + 1] : 0.f;
+        hi = MF::pack(v0, v1);
+        const float2 hf = MF::unpack(hi);
+        lo = MF::pack(v0 - hf.x, v1 - hf.y);
+    };
+    const int mt = M.dcols >> 7;  // m-tiles per warp (dcols / 8 warps / 16)
+    const int col0 = warp * (mt << 4);
+    {  // pull this warp's y segments (nt rows x mt*32 bytes) into L1 now; the epilogue then hits L1
+        const int lines = (mt * 16 * ES + 127) >> 7;
+        const int t = lane / lines, l = lane % lines;
+        if (t < nt && math)
+            prefetch_l1(reinterpret_cast<const T*>(p.y[M.proj]) + int64_t(M.tok[t]) * p.ldy[M.proj] + M.dcol0 + col0 +
+                        l * (128 / ES));
+    }
+    float d[kMaxMT][4];
+#pragma unroll
+    for (int m = 0; m < kMaxMT; ++m) d[m][0] = d[m][1] = d[m][2] = d[m][3] = 0.f;
+    const uint32_t ring_u32 = smem_u32(ring);
+    // this lane's ldmatrix row: k-row (mi >= 2 ? 8 : 0) + rr of the k-step, column half (mi & 1)
+    const int krow = ((mi >> 1) << 3) + rr;
+    const uint32_t coff = uint32_t(col0 + ((mi & 1) << 3)) * ES;
+    for (int ks = 0; ks < nks; ++ks) {
+        // the k-step's rows 16ks..16ks+15 are the next two slots (the second only if r > 16ks + 8)
+        const bool two = r > 16 * ks + 8;
+        const int sa = rg.slot;
+        const uint32_t la = rg.lap;
+        int sb = sa + 1;
+        uint32_t lb = la;
+        if (sb == ns) { sb = 0; ++lb; }
+        mbar_wait(&full[sa], la & 1);
+        if (two) mbar_wait(&full[sb], lb & 1);
+        if (math) {
+            uint32_t h0, h1, l0, l1;
+            vfrag(ks, 0, h0, l0);
+            vfrag(ks, 1, h1, l1);
+            // rows 8-15 of a half k-step (r % 16 == 8) re-read rows 0-7 (finite); their v is zero
+            const int srow_slot = (krow >= 8 && two) ? sb : sa;
+            const uint32_t base = ring_u32 + uint32_t(srow_slot) * uint32_t(SS) + uint32_t(krow & 7) * erow + coff;
+#pragma unroll
+            for (int m = 0; m < kMaxMT; ++m) {
+                if (m < mt) {
+                    uint32_t a0, a1, a2, a3;
+                    ldsm_x4_t(base + uint32_t(m) * (16u * ES), a0, a1, a2, a3);
+                    MF::run(d[m], a0, a1, a2, a3, h0, h1);
+                    MF::run(d[m], a0, a1, a2, a3, l0, l1);
+                }
+            }
+        }
+        __syncwarp();
+        if (lane == 0) {
+            mbar_arrive(&empty[sa]);
+            if (two) mbar_arrive(&empty[sb]);
+        }
+        rg.advance(ns);
+        if (two) rg.advance(ns);
+    }
+    if (warp == 0 && lane == 0 && i < 48) TRACE(352 + i);
+    if (!math) return;
+    // y[tok][dcol0 + col] += scale * D: d0 (col g, tok 2c), d1 (col g, tok 2c+1), d2/d3 (col g+8)
+    T* y = reinterpret_cast<T*>(p.y[M.proj]);
+    const int64_t ldy = p.ldy[M.proj];
+    const float sc = M.scale;
+    // all of a token's y loads first, then the stores (no load waits behind a store)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int t = 2 * c + h;
+        if (t < nt) {
+            T* yr = y + int64_t(M.tok[t]) * ldy + M.dcol0 + col0 + g;
+#pragma unroll
+            for (int m0 = 0; m0 < kMaxMT; m0 += 4) {
+                if (m0 < mt) {
+                    T yv[4][2];
+#pragma unroll
+                    for (int m = 0; m < 4; ++m)
+                        if (m0 + m < mt) {
+                            yv[m][0] = yr[(m0 + m) * 16];
+                            yv[m][1] = yr[(m0 + m) * 16 + 8];
+                        }
+#pragma unroll
+                    for (int m = 0; m < 4; ++m)
+                        if (m0 + m < mt) {
+                            yr[(m0 + m) * 16] = T(float(yv[m][0]) + sc * d[m0 + m][h]);
+                            yr[(m0 + m) * 16 + 8] = T(float(yv[m][1]) + sc * d[m0 + m][2 + h]);
+                        }
+                }
+            }
+        }
+    }
+}
+
 // Expand of one piece (all B rows of the item over this piece's columns)
 // for NT tokens: y_t += scale * v_t B over this thread's 16-byte column
 // vector; walks ring slots every `rps` rows.
@@ -579,9 +742,13 @@ __device__ __forceinline__ void expand_piece(const LoraParams& p, const PieceMet
         for (int t = 0; t < NT; ++t)
             if (own >> t & 1u)
                 yv[kPrefetchY ? t : 0] = *reinterpret_cast<const uint4*>(y + int64_t(M.tok[t]) * ldy + col);
+    } else if (active) {  // larger token counts: into L1 (registers are short), read after the rows
+#pragma unroll
+        for (int t = 0; t < NT; ++t)
+            if ((own >> t & 1u) && (cv & 7) == 0) prefetch_l1(y + int64_t(M.tok[t]) * ldy + col);
     }
     const int r = M.r;
-    const uint32_t rowv = rowb / 16;  // 16-byte vectors per row slice
+    const uint32_t rowv = (rowb + 16) / 16;  // 16-byte vectors per (staggered) row slice
     for (int j0 = 0; j0 < r; j0 += rps) {
         if (j0 > 0) {
             __syncwarp();
@@ -801,7 +968,7 @@ __global__ void __launch_bounds__(kThreads, 1) mbgmv_kernel(const __grid_constan
             const bool S = M.kind == kPieceS;
             const int R = S ? M.nrows : M.r;
             const uint32_t rowb = S ? arow_bytes : uint32_t(M.dcols * ES);
-            const int rps = S ? rps_s : kSlotBytes / int(rowb);
+            const int rps = S ? rps_s : expand_rows_per_slot(rowb);
             auto issue_slot = [&](int base) {
                 const bool mine = (seq++ & 1u) == uint32_t(sid);
                 if (!mine) {
@@ -841,7 +1008,7 @@ __global__ void __launch_bounds__(kThreads, 1) mbgmv_kernel(const __grid_constan
                     }
                 } else {
                     for (int q = lane; q < nrow; q += 32)
-                        bulk_g2s(sbase + size_t(q) * rowb, pool + int64_t(M.pages[base + q]) * P + M.dcol0, rowb,
+                        bulk_g2s(sbase + size_t(q) * (rowb + 16), pool + int64_t(M.pages[base + q]) * P + M.dcol0, rowb,
                                  &full[rg.slot]);
                 }
                 rg.advance(ns);
@@ -993,7 +1160,7 @@ __global__ void __launch_bounds__(kThreads, 1) mbgmv_kernel(const __grid_constan
                 if (tid == 0 && i < 48) TRACE(256 + i);
                 const float* vb = vbuf + eb * (kItemTokCap * kMaxRank);
                 const uint32_t rowb = uint32_t(M.dcols * ES);
-                const int rps = kSlotBytes / int(rowb);
+                const int rps = expand_rows_per_slot(rowb);
                 const int cvs = M.dcols / VE;
                 const int nwc = max(1, (cvs + 31) / 32);
                 int ntg = 1;
@@ -1001,6 +1168,14 @@ __global__ void __launch_bounds__(kThreads, 1) mbgmv_kernel(const __grid_constan
                 const int wc = warp % nwc, tg = warp / nwc;
                 const int cv = wc * 32 + lane;
                 const bool active = cv < cvs && tg < ntg && !(p.dbg & 2);
+                // tensor-core expand: opt-in (SLORA_DBG bit 128).  Measured slower than the CUDA-core axpys
+                // at decode token counts, and using it for some items only would make a token's rounding
+                // depend on how its segment is chunked (breaks the batch-permutation bit-identity).
+                const bool use_emma = ES == 2 && (p.dbg & 128) && (M.dcols & 127) == 0 && (M.dcols >> 7) <= kMaxMT &&
+                                      (M.r & 7) == 0 && M.r <= 64 && expand_rows_per_slot(rowb) == 8;
+                if (use_emma)
+                    expand_piece_mma<T>(p, M, ring, SS, rowb + 16, full, empty, rg, ns, vb, warp, lane, i);
+                else
                 switch (M.nt) {
 #define SLORA_EXPAND_CASE(N)                                                                                   \
     case N:                                                                                                    \
