@@ -24,6 +24,8 @@
 #include "../../include/slora.h"
 #include "slora_internal.h"
 
+#include <cudaTypedefs.h>
+
 namespace slora {
 int64_t launch_count();
 }
@@ -215,8 +217,14 @@ struct slora_batch {
         std::vector<DevItem> items;
         std::vector<DevPiece> pieces;   // grouped by CTA (schedule_pieces)
         std::vector<int32_t> cta_off;   // grid + 1
-        size_t off_items = 0, off_pieces = 0, off_cta = 0;
+        std::vector<MgUnit> mg_s, mg_e; // MBGMM shrink / expand units (fused calls with long runs)
+        size_t off_items = 0, off_pieces = 0, off_cta = 0, off_mg_s = 0, off_mg_e = 0;
     } calls[4][5];
+    // per segment: token ranges [begin, end) of the segment's token list that
+    // are MBGMM runs (>= theta consecutive x rows; fused 16-bit calls only)
+    std::vector<std::vector<std::pair<int32_t, int32_t>>> runs;
+    int32_t n_runs = 0;
+    int64_t mg_units_max = 0;  // units of one 4-projection fused call (arena sizing)
     size_t off_tok = 0;
     // device arena (bump allocated per prepare) + its pinned staging mirror
     size_t arena_cap = 0, arena_used = 0;
@@ -280,6 +288,7 @@ extern "C" slora_status slora_pool_create(const slora_pool_config* cfg, slora_po
         cudaError_t e;
         if ((e = cudaSetDevice(cfg->device))) return cleanup(e, "cudaSetDevice");
         if ((e = configure_lora_kernels(cfg->device))) return cleanup(e, "configure kernels");
+        if ((e = configure_mbgmm_kernels())) return cleanup(e, "configure MBGMM kernels");
         if ((e = cudaMalloc(&p->slot_tab_dev, sizeof(int32_t*) * size_t(cfg->max_adapters))))
             return cleanup(e, "cudaMalloc slot table");
         if ((e = cudaMemset(p->slot_tab_dev, 0, sizeof(int32_t*) * size_t(cfg->max_adapters))))
@@ -756,27 +765,62 @@ void build_call(slora_batch* b, const KernelCfg& k, int N, int nproj, uint32_t m
     (void)nproj;
     const int es = b->pool->es;
     const int64_t n_ep = (k.mode == kShrink || k.dchunk <= 0) ? 0 : (k.D + k.dchunk - 1) / k.dchunk;
+    const bool use_runs = k.mode == kFused && b->n_runs > 0;
+    call.mg_s.clear();
+    call.mg_e.clear();
     for (int si = 0; si < int(b->segs.size()); ++si) {
         const DevSeg& s = b->segs[size_t(si)];
+        // MBGMV token ranges: the segment minus its MBGMM runs
+        std::vector<std::pair<int32_t, int32_t>> ranges;
+        int32_t cur = 0;
+        if (use_runs)
+            for (const auto& rn : b->runs[size_t(si)]) {
+                if (rn.first > cur) ranges.push_back({cur, rn.first});
+                cur = rn.second;
+            }
+        if (cur < s.n_tok) ranges.push_back({cur, s.n_tok});
         for (int pi = 0; pi < np; ++pi) {
             const int proj = proj_ids[pi];
             const int div = (k.mode == kExpand) ? 1 : ((proj < 3) ? N : 1);
             const int ra = s.rank / div;
-            for (int t0 = 0; t0 < s.n_tok; t0 += kItemTokCap) {
-                DevItem it{};
-                it.tab = b->seg_tab.empty() ? nullptr : b->seg_tab[size_t(si)];
-                it.vrow = s.vrow_off + int64_t(t0) * s.rank;
-                it.rank = s.rank;
-                it.seg = si;
-                it.pi = pi;
-                it.t0 = t0;
-                it.nt = std::min(kItemTokCap, s.n_tok - t0);
-                it.tok_off = s.tok_off + t0;
-                it.scale = s.scale;
-                it.n_sp = (k.mode == kExpand) ? 0 : (ra + kShrinkRows - 1) / kShrinkRows;
-                it.n_ep = int32_t(n_ep);
-                call.items.push_back(it);
-            }
+            for (const auto& rg : ranges)
+                for (int t0 = rg.first; t0 < rg.second; t0 += kItemTokCap) {
+                    DevItem it{};
+                    it.tab = b->seg_tab.empty() ? nullptr : b->seg_tab[size_t(si)];
+                    it.vrow = s.vrow_off + int64_t(t0) * s.rank;
+                    it.rank = s.rank;
+                    it.seg = si;
+                    it.pi = pi;
+                    it.t0 = t0;
+                    it.nt = std::min(kItemTokCap, rg.second - t0);
+                    it.tok_off = s.tok_off + t0;
+                    it.scale = s.scale;
+                    it.n_sp = (k.mode == kExpand) ? 0 : (ra + kShrinkRows - 1) / kShrinkRows;
+                    it.n_ep = int32_t(n_ep);
+                    call.items.push_back(it);
+                }
+            if (!use_runs) continue;
+            for (const auto& rn : b->runs[size_t(si)])
+                for (int t0 = rn.first; t0 < rn.second; t0 += kMgTileTok) {
+                    MgUnit u{};
+                    u.tab = b->seg_tab.empty() ? nullptr : b->seg_tab[size_t(si)];
+                    u.vbase = int64_t(pi) * b->NR + s.vrow_off + int64_t(t0) * s.rank;
+                    u.pi = pi;
+                    u.rank = s.rank;
+                    u.row0 = b->tok_idx[size_t(s.tok_off + t0)];
+                    u.nt = std::min(kMgTileTok, rn.second - t0);
+                    u.scale = s.scale;
+                    for (int r0 = 0; r0 < s.rank; r0 += kMgRows) {
+                        u.a = r0;
+                        u.b = std::min(kMgRows, s.rank - r0);
+                        call.mg_s.push_back(u);
+                    }
+                    for (int64_t c0 = 0; c0 < k.D; c0 += kMgCols) {
+                        u.a = int32_t(c0);
+                        u.b = int32_t(std::min<int64_t>(kMgCols, k.D - c0));
+                        call.mg_e.push_back(u);
+                    }
+                }
         }
     }
     std::vector<DevPiece> pieces;
@@ -857,6 +901,35 @@ extern "C" slora_status slora_batch_prepare(slora_batch_t b, const int64_t* tok_
         b->segs.push_back(sg);
         b->seg_tab.push_back(ad.dev_tab);
     }
+    // MBGMM runs: >= theta consecutive x rows of one adapter (fused, 16-bit, one GPU)
+    b->runs.assign(b->segs.size(), {});
+    b->n_runs = 0;
+    b->mg_units_max = 0;
+    {
+        static const int theta = [] {
+            const char* e = getenv("SLORA_MBGMM_MIN");
+            return e ? atoi(e) : kMgDefaultTheta;
+        }();
+        const bool ok_shape = p->cfg.dtype != SLORA_F32 && p->N() == 1 && theta > 0 && p->cfg.hidden % 64 == 0 &&
+                              p->cfg.hidden % kMgCols % 64 == 0 && mbgmm_smem(false, p->cfg.hidden, 0) <= 227 * 1024;
+        for (size_t si = 0; ok_shape && si < b->segs.size(); ++si) {
+            const DevSeg& sg = b->segs[si];
+            int32_t t = 0;
+            while (t < sg.n_tok) {
+                int32_t e2 = t + 1;
+                while (e2 < sg.n_tok && b->tok_idx[size_t(sg.tok_off + e2)] == b->tok_idx[size_t(sg.tok_off + e2 - 1)] + 1)
+                    ++e2;
+                if (e2 - t >= theta) {
+                    b->runs[si].push_back({t, e2});
+                    ++b->n_runs;
+                    const int64_t tiles = (e2 - t + kMgTileTok - 1) / kMgTileTok;
+                    b->mg_units_max += 4 * tiles * ((sg.rank + kMgRows - 1) / kMgRows +
+                                                    (p->cfg.hidden + kMgCols - 1) / kMgCols);
+                }
+                t = e2;
+            }
+        }
+    }
     for (auto& row : b->calls)
         for (auto& c : row) c.built = false;
     b->epoch = p->epoch;
@@ -872,7 +945,8 @@ extern "C" slora_status slora_batch_prepare(slora_batch_t b, const int64_t* tok_
     for (const DevSeg& s : b->segs) chunks += (s.n_tok + kItemTokCap - 1) / kItemTokCap;
     const int64_t max_items = 4 * chunks;
     const int64_t max_pieces_per_item = (kMaxRank + kShrinkRows - 1) / kShrinkRows + 64;
-    const size_t need = 256 + size_t(T) * 4 + 16 * (1024 + 4 * 1024 + size_t(max_items) * sizeof(DevItem) +
+    const size_t need = 256 + size_t(T) * 4 + 16 * (1024 + 4 * 1024 + size_t(b->mg_units_max) * sizeof(MgUnit) +
+                                                   size_t(max_items) * sizeof(DevItem) +
                                                    size_t(max_items * max_pieces_per_item) * sizeof(DevPiece));
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     CUDA_TRY(cudaSetDevice(p->cfg.device));
@@ -932,7 +1006,7 @@ extern "C" slora_status slora_batch_get_info(slora_batch_t b, slora_batch_info* 
     out->segments = int32_t(b->segs.size());
     out->sum_rank_tokens = b->NR;
     out->weight_bytes_per_proj = b->weight_bytes_per_proj;
-    out->mbgmm_segments = 0;
+    out->mbgmm_segments = b->n_runs;
     return ok();
 }
 
@@ -968,6 +1042,8 @@ slora_status ensure_call(slora_pool* p, slora_batch* b, int kc, uint32_t mask, v
     call.off_items = arena_put(b, call.items.data(), call.items.size() * sizeof(DevItem), s, e);
     if (!e) call.off_pieces = arena_put(b, call.pieces.data(), call.pieces.size() * sizeof(DevPiece), s, e);
     if (!e) call.off_cta = arena_put(b, call.cta_off.data(), call.cta_off.size() * sizeof(int32_t), s, e);
+    if (!e) call.off_mg_s = arena_put(b, call.mg_s.data(), call.mg_s.size() * sizeof(MgUnit), s, e);
+    if (!e) call.off_mg_e = arena_put(b, call.mg_e.data(), call.mg_e.size() * sizeof(MgUnit), s, e);
     if (e) return fail(SLORA_ERR_CUDA, "call descriptor upload: %s", cudaGetErrorString(e));
     call.built = true;
     call.mask = mask;
@@ -1033,6 +1109,60 @@ slora_status launch(slora_pool* p, int kc, LoraParams& q, void* stream) {
 }
 }  // namespace
 
+namespace {
+PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return static_cast<PFN_cuTensorMapEncodeTiled_v12000>(nullptr);
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+    }();
+    return fn;
+}
+
+// The two MBGMM launches of a fused call with long runs (shrink into the
+// call's workspace, then expand into y); the MBGMV launch for the remaining
+// tokens follows on the same stream.
+slora_status launch_mbgmm_pair(slora_pool* p, slora_batch* b, const slora_batch::Call& call, const LoraParams& q,
+                               const void* x, int64_t ldx, void* stream) {
+    PFN_cuTensorMapEncodeTiled_v12000 enc = tensor_map_encoder();
+    if (!enc) return fail(SLORA_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    MgParams m;
+    memset(&m, 0, sizeof(m));
+    const int64_t H = p->cfg.hidden;
+    const cuuint64_t dims[2] = {cuuint64_t(H), cuuint64_t(b->T)};
+    const cuuint64_t strides[1] = {cuuint64_t(ldx) * cuuint64_t(p->es)};
+    const cuuint32_t box[2] = {64, cuuint32_t(kMgTileTok)};
+    const cuuint32_t estr[2] = {1, 1};
+    CUresult cr = enc(&m.xmap, p->cfg.dtype == SLORA_F16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
+                      2, const_cast<void*>(x), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                      CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (cr != CUDA_SUCCESS) return fail(SLORA_ERR_CUDA, "cuTensorMapEncodeTiled: %d", int(cr));
+    uint8_t* base = static_cast<uint8_t*>(b->arena_dev);
+    m.pool = p->cfg.device_buffer;
+    m.page_elems = p->P;
+    m.v = q.v;
+    for (int pj = 0; pj < 4; ++pj) {
+        m.y[pj] = q.y[pj];
+        m.ldy[pj] = q.ldy[pj];
+        m.proj_ids[pj] = q.proj_ids[pj];
+    }
+    m.layer = q.layer;
+    m.K = int32_t(H);
+    int rmax = 16;
+    for (const MgUnit& u : call.mg_e) rmax = std::max(rmax, (u.rank + 15) & ~15);
+    const int dt = p->cfg.dtype == SLORA_F16 ? kF16 : kBF16;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    m.units = reinterpret_cast<const MgUnit*>(base + call.off_mg_s);
+    CUDA_TRY(launch_mbgmm(m, false, dt, int(call.mg_s.size()), mbgmm_smem(false, H, 0), s, true));
+    m.units = reinterpret_cast<const MgUnit*>(base + call.off_mg_e);
+    CUDA_TRY(launch_mbgmm(m, true, dt, int(call.mg_e.size()), mbgmm_smem(true, 0, rmax), s, true));
+    return SLORA_OK;
+}
+}  // namespace
+
 extern "C" slora_status slora_lora_apply(slora_pool_t p, slora_batch_t b, int32_t layer, uint32_t mask,
                                          const void* x, int64_t ldx, void* const y[4], const int64_t ldy[4],
                                          void* stream) {
@@ -1056,6 +1186,11 @@ extern "C" slora_status slora_lora_apply(slora_pool_t p, slora_batch_t b, int32_
         q.ldy[pj] = ldy[pj];
     }
     q.v_blocks = 1;
+    const slora_batch::Call& call = b->calls[0][q.nproj];
+    if (!call.mg_s.empty()) {
+        st = launch_mbgmm_pair(p, b, call, q, x, ldx, stream);
+        if (st) return st;
+    }
     return launch(p, 0, q, stream);
 }
 

@@ -1,0 +1,357 @@
+// mbgmm.cu -- tensor-core kernels for long prefill runs (MBGMM, PAPER.md
+// Sec. 5.3: "for the prefill stage ... MBGMM").
+//
+// A *run* is a maximal range of >= theta consecutive x rows (tokens) that use
+// the same adapter (a prefill request's tokens).  Its LoRA delta is a small
+// GEMM pair, y[n x d] += scale * (x[n x h] A[h x r]) B[r x d], so the weights
+// are read once per 64-token tile instead of once per token chunk.  Two
+// launches per call (before the MBGMV launch for the remaining tokens):
+//
+//  mbgmm_shrink_kernel<T>: one CTA per (run tile of <= 64 tokens, projection,
+//    group of <= 16 stored A rows).  The 16 A page rows (8 KB each at h=4096)
+//    are bulk-copied into smem once, at a 16-byte stagger; x streams through a
+//    4-stage ring of 64x64 tiles loaded by TMA (2-D tensor map, 128-byte
+//    swizzle).  4 consumer warps, one 16-token m-tile each, run
+//    mma.m16n8k16 (M = tokens, N = 8 A rows, K = 16) with ldmatrix operand
+//    loads (conflict-free: swizzle for x, stagger for A).  v (fp32) goes to
+//    the call's workspace in the MBGMV layout.
+//  mbgmm_expand_kernel<T>: one CTA per (run tile, projection, slab of <= 1024
+//    output columns).  The slab's r B row slices (2 KB each) are bulk-copied
+//    into smem (staggered); the tile's v is split into a 16-bit high and low
+//    part (v = hi + lo to ~2^-22) in smem; mma.m16n8k16 (M = tokens, N = 8
+//    columns, K = 16 rank rows, B operand via ldmatrix.trans), two MMAs per
+//    step (hi, lo); y = y + scale * D, rounded once.
+//
+// Both accumulate in fp32 in a fixed order (deterministic).  fp16/bf16 only
+// (fp32 batches stay on MBGMV: no TF32 for fp32 inputs).
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "slora_internal.h"
+
+namespace slora {
+namespace {
+
+__device__ __forceinline__ uint32_t su32(const void* p) { return static_cast<uint32_t>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void bar_init(uint64_t* b, uint32_t n) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(n) : "memory");
+}
+__device__ __forceinline__ void bar_fence_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void bar_arrive(uint64_t* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(su32(b)) : "memory");
+}
+__device__ __forceinline__ void bar_expect(uint64_t* b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bar_wait(uint64_t* b, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "W_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra W_%=;\n}" ::"r"(su32(b)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void copy_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* b) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(su32(dst)),
+        "l"(src), "r"(bytes), "r"(su32(b))
+        : "memory");
+}
+// 2-D TMA tile load (tensor map in kernel parameter space)
+__device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* b) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+        "[%4];" ::"r"(su32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(su32(b))
+        : "memory");
+}
+__device__ __forceinline__ void grid_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void grid_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void ldm4(uint32_t a, uint32_t (&r)[4]) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "r"(a));
+}
+__device__ __forceinline__ void ldm4t(uint32_t a, uint32_t (&r)[4]) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "r"(a));
+}
+__device__ __forceinline__ void named_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+template <typename T> struct Mma;
+template <> struct Mma<__half> {
+    __device__ static void run(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+        asm volatile(
+            "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
+            "{%0, %1, %2, %3};"
+            : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+            : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+    }
+    __device__ static uint16_t bits(float v) { return __half_as_ushort(__float2half_rn(v)); }
+    __device__ static float val(uint16_t b) { return __half2float(__ushort_as_half(b)); }
+    __device__ static uint32_t pack2(float lo, float hi) {
+        __half2 h = __floats2half2_rn(lo, hi);
+        return *reinterpret_cast<uint32_t*>(&h);
+    }
+    __device__ static float2 unpack2(uint32_t u) { return __half22float2(*reinterpret_cast<__half2*>(&u)); }
+};
+template <> struct Mma<__nv_bfloat16> {
+    __device__ static void run(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+        asm volatile(
+            "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
+            "{%0, %1, %2, %3};"
+            : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+            : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+    }
+    __device__ static uint16_t bits(float v) { return __bfloat16_as_ushort(__float2bfloat16_rn(v)); }
+    __device__ static float val(uint16_t b) { return __bfloat162float(__ushort_as_bfloat16(b)); }
+    __device__ static uint32_t pack2(float lo, float hi) {
+        __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
+        return *reinterpret_cast<uint32_t*>(&h);
+    }
+    __device__ static float2 unpack2(uint32_t u) { return __bfloat1622float2(*reinterpret_cast<__nv_bfloat162*>(&u)); }
+};
+
+constexpr int kMgConsumers = 4;                        // 4 x 16-token m-tiles
+constexpr int kMgThreads = (kMgConsumers + 1) * 32;    // + producer warp
+constexpr int kXStages = 4;
+constexpr int kXTileBytes = kMgTileTok * 64 * 2;       // 64 tokens x 64 elements (8 KB)
+
+__host__ __device__ inline size_t al(size_t x, size_t a) { return (x + a - 1) & ~(a - 1); }
+
+// shrink smem: [bars][A rows 16 x (K*2+16)][x ring 4 x 8 KB, 1 KB aligned]
+__host__ __device__ inline size_t mg_shrink_smem(int64_t K) {
+    return al(256 + size_t(kMgRows) * (K * 2 + 16), 1024) + size_t(kXStages) * kXTileBytes + 1024;
+}
+// expand smem: [bars][B slab r x (nc*2+16)][v hi, lo: 64 x (r+8) 16-bit each]
+__host__ __device__ inline size_t mg_expand_smem(int rmax) {
+    return 256 + size_t(rmax) * (kMgCols * 2 + 16) + 2 * size_t(kMgTileTok) * (rmax + 8) * 2 + 128;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kMgThreads, 1) mbgmm_shrink_kernel(const __grid_constant__ MgParams p) {
+    using O = Mma<T>;
+    constexpr int ES = 2;
+    extern __shared__ __align__(1024) unsigned char sm[];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const MgUnit u = p.units[blockIdx.x];
+    const int K = p.K;
+    const uint32_t arow = uint32_t(K) * ES + 16;  // staggered A row stride
+    uint64_t* abar = reinterpret_cast<uint64_t*>(sm);
+    uint64_t* xfull = abar + 1;
+    uint64_t* xempty = xfull + kXStages;
+    unsigned char* arows = sm + 256;
+    unsigned char* xring = sm + al(256 + size_t(kMgRows) * arow, 1024);
+    // the dynamic smem base is 1 KB aligned only up to the driver's guarantee: align the ring explicitly
+    xring = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(xring) + 1023) & ~uintptr_t(1023));
+    const int nrows = u.b;
+    const int nkc = K / 64;
+    if (tid == 0) {
+        bar_init(abar, 1);
+        for (int s = 0; s < kXStages; ++s) {
+            bar_init(&xfull[s], 1);
+            bar_init(&xempty[s], kMgConsumers);
+        }
+        bar_fence_init();
+    }
+    __syncthreads();
+    grid_trigger();
+    if (warp == kMgConsumers) {
+        // ---- producer: the group's A rows (pages: loader-written, safe before the PDL wait), then x tiles
+        const int proj = p.proj_ids[u.pi];
+        const int32_t* tab = u.tab + int64_t((p.layer * 4 + proj) * 2) * u.rank;  // [A rows][B rows]
+        if (lane == 0) bar_expect(abar, uint32_t(nrows) * uint32_t(K) * ES);
+        __syncwarp();
+        if (lane < nrows)
+            copy_g2s(arows + size_t(lane) * arow, static_cast<const T*>(p.pool) + int64_t(tab[u.a + lane]) * p.page_elems,
+                     uint32_t(K) * ES, abar);
+        grid_wait();
+        if (lane == 0)
+            for (int kc = 0; kc < nkc; ++kc) {
+                const int s = kc % kXStages;
+                if (kc >= kXStages) bar_wait(&xempty[s], ((kc / kXStages) - 1) & 1);
+                bar_expect(&xfull[s], kXTileBytes);
+                tma_2d(xring + size_t(s) * kXTileBytes, &p.xmap, kc * 64, u.row0, &xfull[s]);
+            }
+        return;
+    }
+    // ---- consumers: warp w = tokens 16w..16w+15
+    const int mi = lane >> 3, rr = lane & 7, g = lane >> 2, c = lane & 3;
+    const int xrow = warp * 16 + ((mi & 1) << 3) + rr;      // A-operand (x) row of this lane's ldmatrix
+    const int achk = mi >> 1;                               // its 16-byte chunk within the k-step
+    const int brow = min(((mi >> 1) << 3) + rr, nrows - 1); // B-operand (A row); padding rows repeat a real one
+    const uint32_t bbase = su32(arows) + uint32_t(brow) * arow + uint32_t((mi & 1) << 4);
+    const uint32_t xbase = su32(xring) + uint32_t(xrow) * 128u;
+    float d[2][4] = {};
+    bar_wait(abar, 0);
+    for (int kc = 0; kc < nkc; ++kc) {
+        const int s = kc % kXStages;
+        bar_wait(&xfull[s], (kc / kXStages) & 1);
+        const uint32_t xs = xbase + uint32_t(s) * kXTileBytes;
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+            uint32_t a[4], b[4];
+            const int chunk = 2 * kk + achk;  // 128-byte swizzle: 16-byte chunk j of row r sits at j ^ (r & 7)
+            ldm4(xs + uint32_t((chunk ^ (xrow & 7)) << 4), a);
+            ldm4(bbase + uint32_t(kc * 64 + kk * 16) * ES, b);
+            O::run(d[0], a, b[0], b[1]);
+            O::run(d[1], a, b[2], b[3]);
+        }
+        __syncwarp();
+        if (lane == 0) bar_arrive(&xempty[s]);
+    }
+    // d[n][0..1]: token 16w+g, A rows 8n+2c, 8n+2c+1; d[n][2..3]: token 16w+g+8
+#pragma unroll
+    for (int n = 0; n < 2; ++n)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int t = warp * 16 + g + 8 * h;
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int row = 8 * n + 2 * c + e;
+                if (t < u.nt && row < nrows) p.v[u.vbase + int64_t(t) * u.rank + u.a + row] = d[n][2 * h + e];
+            }
+        }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kMgThreads, 1) mbgmm_expand_kernel(const __grid_constant__ MgParams p) {
+    using O = Mma<T>;
+    constexpr int ES = 2;
+    extern __shared__ __align__(128) unsigned char sm[];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const MgUnit u = p.units[blockIdx.x];
+    const int r = u.rank, nc = u.b;
+    const int rp = (r + 15) & ~15;                 // rank padded to whole k-steps
+    const uint32_t brow = uint32_t(nc) * ES + 16;  // staggered B row-slice stride
+    const int vst = rp + 8;                        // v tile row stride (16-bit elements)
+    uint64_t* bbar = reinterpret_cast<uint64_t*>(sm);
+    unsigned char* slab = sm + 256;
+    uint16_t* vhi = reinterpret_cast<uint16_t*>(sm + 256 + size_t(r) * brow);
+    uint16_t* vlo = vhi + kMgTileTok * vst;
+    if (tid == 0) {
+        bar_init(bbar, 1);
+        bar_fence_init();
+    }
+    __syncthreads();
+    grid_trigger();
+    if (warp == kMgConsumers) {
+        const int proj = p.proj_ids[u.pi];
+        const int32_t* tab = u.tab + int64_t((p.layer * 4 + proj) * 2) * r + r;  // B rows
+        if (lane == 0) bar_expect(bbar, uint32_t(r) * uint32_t(nc) * ES);
+        __syncwarp();
+        for (int j = lane; j < r; j += 32)
+            copy_g2s(slab + size_t(j) * brow, static_cast<const T*>(p.pool) + int64_t(tab[j]) * p.page_elems + u.a,
+                     uint32_t(nc) * ES, bbar);
+        return;
+    }
+    grid_wait();  // v (previous kernel) and y are read below
+    // v tile -> smem, split into hi + lo (zero beyond the tile's tokens and the rank)
+    for (int e = tid; e < kMgTileTok * rp; e += kMgConsumers * 32) {
+        const int t = e / rp, j = e % rp;
+        const float val = (t < u.nt && j < r) ? __ldcg(p.v + u.vbase + int64_t(t) * r + j) : 0.f;
+        const uint16_t hb = O::bits(val);
+        vhi[t * vst + j] = hb;
+        vlo[t * vst + j] = O::bits(val - O::val(hb));
+    }
+    named_sync(1, kMgConsumers * 32);
+    bar_wait(bbar, 0);
+    const int mi = lane >> 3, rr = lane & 7, g = lane >> 2, c = lane & 3;
+    // A operand (v): row = token 16w + (mi&1)*8 + rr, k chunk (mi>>1)*8
+    const int arow_ = warp * 16 + ((mi & 1) << 3) + rr;
+    const uint32_t ahi = su32(vhi) + uint32_t(arow_ * vst + ((mi >> 1) << 3)) * ES;
+    const uint32_t alo = su32(vlo) + uint32_t(arow_ * vst + ((mi >> 1) << 3)) * ES;
+    T* y = reinterpret_cast<T*>(p.y[p.proj_ids[u.pi]]);
+    const int64_t ldy = p.ldy[p.proj_ids[u.pi]];
+    const int t0 = warp * 16 + g, t1 = t0 + 8;
+    T* y0 = y + int64_t(u.row0 + t0) * ldy + u.a;
+    T* y1 = y + int64_t(u.row0 + t1) * ldy + u.a;
+    for (int sc = 0; sc < nc; sc += 64) {
+        float d[8][4] = {};
+        for (int k = 0; k < rp; k += 16) {
+            uint32_t ah[4], alw[4];
+            ldm4(ahi + uint32_t(k) * ES, ah);
+            ldm4(alo + uint32_t(k) * ES, alw);
+            // B operand (B rows, k = rank row, n = column) through ldmatrix.trans: matrices
+            // (rows k..k+7 | k+8..k+15) x (cols n..n+7 | n+8..n+15); rows >= r repeat row r-1 (v is 0 there)
+            const int krow = min(k + ((mi & 1) << 3) + rr, r - 1);
+#pragma unroll
+            for (int n2 = 0; n2 < 4; ++n2) {
+                uint32_t b[4];
+                ldm4t(su32(slab) + uint32_t(krow) * brow + uint32_t(sc + n2 * 16 + ((mi >> 1) << 3)) * ES, b);
+                O::run(d[2 * n2], ah, b[0], b[1]);
+                O::run(d[2 * n2], alw, b[0], b[1]);
+                O::run(d[2 * n2 + 1], ah, b[2], b[3]);
+                O::run(d[2 * n2 + 1], alw, b[2], b[3]);
+            }
+        }
+        // y += scale * D: d[n][0..1] token t0, columns sc + 8n + 2c (+1); d[n][2..3] token t1
+        uint32_t yv[8][2];
+#pragma unroll
+        for (int n = 0; n < 8; ++n) {
+            const int col = sc + 8 * n + 2 * c;
+            yv[n][0] = t0 < u.nt ? *reinterpret_cast<const uint32_t*>(y0 + col) : 0u;
+            yv[n][1] = t1 < u.nt ? *reinterpret_cast<const uint32_t*>(y1 + col) : 0u;
+        }
+#pragma unroll
+        for (int n = 0; n < 8; ++n) {
+            const int col = sc + 8 * n + 2 * c;
+            if (t0 < u.nt) {
+                const float2 f = O::unpack2(yv[n][0]);
+                *reinterpret_cast<uint32_t*>(y0 + col) = O::pack2(f.x + u.scale * d[n][0], f.y + u.scale * d[n][1]);
+            }
+            if (t1 < u.nt) {
+                const float2 f = O::unpack2(yv[n][1]);
+                *reinterpret_cast<uint32_t*>(y1 + col) = O::pack2(f.x + u.scale * d[n][2], f.y + u.scale * d[n][3]);
+            }
+        }
+    }
+}
+
+template <typename T>
+cudaError_t launch_kernel(void (*k)(MgParams), const MgParams& p, int grid, size_t smem, cudaStream_t s, bool pdl) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(unsigned(grid));
+    cfg.blockDim = dim3(kMgThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl ? 1 : 0;
+    count_launch();
+    return cudaLaunchKernelEx(&cfg, k, p);
+}
+
+}  // namespace
+
+size_t mbgmm_smem(bool expand, int64_t K, int rmax) { return expand ? mg_expand_smem(rmax) : mg_shrink_smem(K); }
+
+cudaError_t configure_mbgmm_kernels() {
+    const int lim = 227 * 1024;
+    cudaError_t e;
+    if ((e = cudaFuncSetAttribute(mbgmm_shrink_kernel<__half>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim))) return e;
+    if ((e = cudaFuncSetAttribute(mbgmm_shrink_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim)))
+        return e;
+    if ((e = cudaFuncSetAttribute(mbgmm_expand_kernel<__half>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim))) return e;
+    return cudaFuncSetAttribute(mbgmm_expand_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
+}
+
+cudaError_t launch_mbgmm(const MgParams& p, bool expand, int dtype, int n_units, size_t smem, cudaStream_t s,
+                         bool pdl) {
+    if (n_units == 0) return cudaSuccess;
+    if (dtype == kF16)
+        return expand ? launch_kernel<__half>(mbgmm_expand_kernel<__half>, p, n_units, smem, s, pdl)
+                      : launch_kernel<__half>(mbgmm_shrink_kernel<__half>, p, n_units, smem, s, pdl);
+    return expand ? launch_kernel<__nv_bfloat16>(mbgmm_expand_kernel<__nv_bfloat16>, p, n_units, smem, s, pdl)
+                  : launch_kernel<__nv_bfloat16>(mbgmm_shrink_kernel<__nv_bfloat16>, p, n_units, smem, s, pdl);
+}
+
+}  // namespace slora

@@ -3,6 +3,7 @@
 #pragma once
 #include <cstdint>
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 namespace slora {
@@ -116,6 +117,40 @@ size_t lora_slot_stride(int mode, int64_t K, int esize);  // ring slot stride (b
 int lora_max_ctas(int mode, int dtype, size_t smem);
 cudaError_t launch_lora(const LoraParams& p, int mode, int dtype, int grid, cudaStream_t s, size_t smem);
 cudaError_t configure_lora_kernels(int device);
+
+// ------------------------------------------------------------------ MBGMM
+// Long prefill runs (>= theta consecutive x rows of one adapter) go to the
+// tensor-core MBGMM kernels (mbgmm.cu); units are built on the host.
+constexpr int kMgTileTok = 64;   // tokens per tile (4 mma m-tiles)
+constexpr int kMgRows = 16;      // stored A rows per shrink unit
+constexpr int kMgCols = 1024;    // output columns per expand unit
+constexpr int kMgDefaultTheta = 32;  // run length from which MBGMM is used (SLORA_MBGMM_MIN)
+struct MgUnit {
+    const int32_t* tab;  // adapter page table
+    int64_t vbase;       // v index of (tile token 0, rank row 0)
+    int32_t pi;          // projection index in the call's mask order
+    int32_t rank;
+    int32_t row0;        // x / y row of the tile's first token (the run's rows are consecutive)
+    int32_t nt;          // tokens in the tile (<= kMgTileTok)
+    int32_t a, b;        // shrink: first A row, rows; expand: first column, columns
+    float scale;
+    int32_t pad;
+};
+static_assert(sizeof(MgUnit) == 48, "MgUnit layout");
+struct alignas(64) MgParams {
+    CUtensorMap xmap;    // x as a 2-D tensor [rows T][K], 64x64 boxes, 128-byte swizzle
+    const void* pool;
+    int64_t page_elems;
+    const MgUnit* units;
+    float* v;            // the call's fp32 workspace (MBGMV layout)
+    void* y[4];
+    int64_t ldy[4];
+    int32_t proj_ids[4];
+    int32_t layer, K;
+};
+size_t mbgmm_smem(bool expand, int64_t K, int rmax);
+cudaError_t configure_mbgmm_kernels();
+cudaError_t launch_mbgmm(const MgParams& p, bool expand, int dtype, int n_units, size_t smem, cudaStream_t s, bool pdl);
 
 // Adapter scatter: jobs describe how rows of a packed staging buffer land in
 // pages (see api.cpp pack_shard).
