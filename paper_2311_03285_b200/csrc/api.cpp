@@ -815,9 +815,10 @@ void build_call(slora_batch* b, const KernelCfg& k, int N, int nproj, uint32_t m
                         u.b = std::min(kMgRows, s.rank - r0);
                         call.mg_s.push_back(u);
                     }
-                    for (int64_t c0 = 0; c0 < k.D; c0 += kMgCols) {
+                    const int ecols = mbgmm_expand_cols(s.rank);
+                    for (int64_t c0 = 0; c0 < k.D; c0 += ecols) {
                         u.a = int32_t(c0);
-                        u.b = int32_t(std::min<int64_t>(kMgCols, k.D - c0));
+                        u.b = int32_t(std::min<int64_t>(ecols, k.D - c0));
                         call.mg_e.push_back(u);
                     }
                 }
@@ -924,7 +925,7 @@ extern "C" slora_status slora_batch_prepare(slora_batch_t b, const int64_t* tok_
                     ++b->n_runs;
                     const int64_t tiles = (e2 - t + kMgTileTok - 1) / kMgTileTok;
                     b->mg_units_max += 4 * tiles * ((sg.rank + kMgRows - 1) / kMgRows +
-                                                    (p->cfg.hidden + kMgCols - 1) / kMgCols);
+                                                    (p->cfg.hidden + kMgCols / 2 - 1) / (kMgCols / 2));
                 }
                 t = e2;
             }
@@ -1151,14 +1152,14 @@ slora_status launch_mbgmm_pair(slora_pool* p, slora_batch* b, const slora_batch:
     }
     m.layer = q.layer;
     m.K = int32_t(H);
-    int rmax = 16;
-    for (const MgUnit& u : call.mg_e) rmax = std::max(rmax, (u.rank + 15) & ~15);
+    size_t esmem = 0;
+    for (const MgUnit& u : call.mg_e) esmem = std::max(esmem, mbgmm_smem(true, 0, u.rank));
     const int dt = p->cfg.dtype == SLORA_F16 ? kF16 : kBF16;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     m.units = reinterpret_cast<const MgUnit*>(base + call.off_mg_s);
     CUDA_TRY(launch_mbgmm(m, false, dt, int(call.mg_s.size()), mbgmm_smem(false, H, 0), s, true));
     m.units = reinterpret_cast<const MgUnit*>(base + call.off_mg_e);
-    CUDA_TRY(launch_mbgmm(m, true, dt, int(call.mg_e.size()), mbgmm_smem(true, 0, rmax), s, true));
+    CUDA_TRY(launch_mbgmm(m, true, dt, int(call.mg_e.size()), esmem, s, true));
     return SLORA_OK;
 }
 }  // namespace

@@ -120,7 +120,7 @@ template <> struct Mma<__nv_bfloat16> {
 
 constexpr int kMgConsumers = 4;                        // 4 x 16-token m-tiles
 constexpr int kMgThreads = (kMgConsumers + 1) * 32;    // + producer warp
-constexpr int kXStages = 4;
+constexpr int kXStages = 8;  // 64 KB of x in flight per CTA (L2 latency x SM share)
 constexpr int kXTileBytes = kMgTileTok * 64 * 2;       // 64 tokens x 64 elements (8 KB)
 
 __host__ __device__ inline size_t al(size_t x, size_t a) { return (x + a - 1) & ~(a - 1); }
@@ -129,9 +129,11 @@ __host__ __device__ inline size_t al(size_t x, size_t a) { return (x + a - 1) & 
 __host__ __device__ inline size_t mg_shrink_smem(int64_t K) {
     return al(256 + size_t(kMgRows) * (K * 2 + 16), 1024) + size_t(kXStages) * kXTileBytes + 1024;
 }
-// expand smem: [bars][B slab r x (nc*2+16)][v hi, lo: 64 x (r+8) 16-bit each]
-__host__ __device__ inline size_t mg_expand_smem(int rmax) {
-    return 256 + size_t(rmax) * (kMgCols * 2 + 16) + 2 * size_t(kMgTileTok) * (rmax + 8) * 2 + 128;
+// expand smem: [bars][B slab r x (nc*2+16)][v hi, lo: 64 x (rp+8) 16-bit each]; the host
+// sizes slabs (mbgmm_expand_cols) so that two CTAs fit on an SM (one loads while one computes)
+__host__ __device__ inline size_t mg_expand_smem_unit(int r, int nc) {
+    const int rp = (r + 15) & ~15;
+    return 256 + size_t(r) * (size_t(nc) * 2 + 16) + 2 * size_t(kMgTileTok) * (rp + 8) * 2 + 128;
 }
 
 template <typename T>
@@ -221,10 +223,10 @@ __global__ void __launch_bounds__(kMgThreads, 1) mbgmm_shrink_kernel(const __gri
 }
 
 template <typename T>
-__global__ void __launch_bounds__(kMgThreads, 1) mbgmm_expand_kernel(const __grid_constant__ MgParams p) {
+__global__ void __launch_bounds__(kMgThreads, 2) mbgmm_expand_kernel(const __grid_constant__ MgParams p) {
     using O = Mma<T>;
     constexpr int ES = 2;
-    extern __shared__ __align__(128) unsigned char sm[];
+    extern __shared__ __align__(1024) unsigned char sm[];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const MgUnit u = p.units[blockIdx.x];
     const int r = u.rank, nc = u.b;
@@ -253,12 +255,28 @@ __global__ void __launch_bounds__(kMgThreads, 1) mbgmm_expand_kernel(const __gri
     }
     grid_wait();  // v (previous kernel) and y are read below
     // v tile -> smem, split into hi + lo (zero beyond the tile's tokens and the rank)
-    for (int e = tid; e < kMgTileTok * rp; e += kMgConsumers * 32) {
-        const int t = e / rp, j = e % rp;
-        const float val = (t < u.nt && j < r) ? __ldcg(p.v + u.vbase + int64_t(t) * r + j) : 0.f;
-        const uint16_t hb = O::bits(val);
-        vhi[t * vst + j] = hb;
-        vlo[t * vst + j] = O::bits(val - O::val(hb));
+    // (eight independent loads in flight per thread, then the conversions: a serial
+    // load -> store loop waits one L2 round trip per element)
+    constexpr int kU = 8;
+    const int nel = kMgTileTok * rp;
+    for (int e0 = tid; e0 < nel; e0 += kU * kMgConsumers * 32) {
+        float val[kU];
+#pragma unroll
+        for (int q = 0; q < kU; ++q) {
+            const int e = e0 + q * kMgConsumers * 32;
+            const int t = e / rp, j = e % rp;
+            val[q] = (e < nel && t < u.nt && j < r) ? __ldcg(p.v + u.vbase + int64_t(t) * r + j) : 0.f;
+        }
+#pragma unroll
+        for (int q = 0; q < kU; ++q) {
+            const int e = e0 + q * kMgConsumers * 32;
+            if (e < nel) {
+                const int t = e / rp, j = e % rp;
+                const uint16_t hb = O::bits(val[q]);
+                vhi[t * vst + j] = hb;
+                vlo[t * vst + j] = O::bits(val[q] - O::val(hb));
+            }
+        }
     }
     named_sync(1, kMgConsumers * 32);
     bar_wait(bbar, 0);
@@ -272,7 +290,16 @@ __global__ void __launch_bounds__(kMgThreads, 1) mbgmm_expand_kernel(const __gri
     const int t0 = warp * 16 + g, t1 = t0 + 8;
     T* y0 = y + int64_t(u.row0 + t0) * ldy + u.a;
     T* y1 = y + int64_t(u.row0 + t1) * ldy + u.a;
+    // y of this sub-chunk is loaded into registers before its MMAs (the loads fly
+    // while the tensor cores work), then read-modify-written once
     for (int sc = 0; sc < nc; sc += 64) {
+        uint32_t yv[8][2];
+#pragma unroll
+        for (int n = 0; n < 8; ++n) {
+            const int col = sc + 8 * n + 2 * c;
+            yv[n][0] = t0 < u.nt ? *reinterpret_cast<const uint32_t*>(y0 + col) : 0u;
+            yv[n][1] = t1 < u.nt ? *reinterpret_cast<const uint32_t*>(y1 + col) : 0u;
+        }
         float d[8][4] = {};
         for (int k = 0; k < rp; k += 16) {
             uint32_t ah[4], alw[4];
@@ -286,19 +313,14 @@ __global__ void __launch_bounds__(kMgThreads, 1) mbgmm_expand_kernel(const __gri
                 uint32_t b[4];
                 ldm4t(su32(slab) + uint32_t(krow) * brow + uint32_t(sc + n2 * 16 + ((mi >> 1) << 3)) * ES, b);
                 O::run(d[2 * n2], ah, b[0], b[1]);
-                O::run(d[2 * n2], alw, b[0], b[1]);
                 O::run(d[2 * n2 + 1], ah, b[2], b[3]);
+#ifndef SLORA_MG_NO_LO
+                O::run(d[2 * n2], alw, b[0], b[1]);
                 O::run(d[2 * n2 + 1], alw, b[2], b[3]);
+#endif
             }
         }
         // y += scale * D: d[n][0..1] token t0, columns sc + 8n + 2c (+1); d[n][2..3] token t1
-        uint32_t yv[8][2];
-#pragma unroll
-        for (int n = 0; n < 8; ++n) {
-            const int col = sc + 8 * n + 2 * c;
-            yv[n][0] = t0 < u.nt ? *reinterpret_cast<const uint32_t*>(y0 + col) : 0u;
-            yv[n][1] = t1 < u.nt ? *reinterpret_cast<const uint32_t*>(y1 + col) : 0u;
-        }
 #pragma unroll
         for (int n = 0; n < 8; ++n) {
             const int col = sc + 8 * n + 2 * c;
@@ -332,7 +354,9 @@ cudaError_t launch_kernel(void (*k)(MgParams), const MgParams& p, int grid, size
 
 }  // namespace
 
-size_t mbgmm_smem(bool expand, int64_t K, int rmax) { return expand ? mg_expand_smem(rmax) : mg_shrink_smem(K); }
+size_t mbgmm_smem(bool expand, int64_t K, int rmax) {
+    return expand ? mg_expand_smem_unit(rmax, mbgmm_expand_cols(rmax)) : mg_shrink_smem(K);
+}
 
 cudaError_t configure_mbgmm_kernels() {
     const int lim = 227 * 1024;
@@ -341,7 +365,12 @@ cudaError_t configure_mbgmm_kernels() {
     if ((e = cudaFuncSetAttribute(mbgmm_shrink_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim)))
         return e;
     if ((e = cudaFuncSetAttribute(mbgmm_expand_kernel<__half>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim))) return e;
-    return cudaFuncSetAttribute(mbgmm_expand_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim);
+    if ((e = cudaFuncSetAttribute(mbgmm_expand_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim)))
+        return e;
+    // two expand CTAs per SM: all of the unified L1/shared capacity as shared memory
+    if ((e = cudaFuncSetAttribute(mbgmm_expand_kernel<__half>, cudaFuncAttributePreferredSharedMemoryCarveout, 100)))
+        return e;
+    return cudaFuncSetAttribute(mbgmm_expand_kernel<__nv_bfloat16>, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
 }
 
 cudaError_t launch_mbgmm(const MgParams& p, bool expand, int dtype, int n_units, size_t smem, cudaStream_t s,

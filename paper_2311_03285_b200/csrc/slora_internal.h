@@ -123,7 +123,9 @@ cudaError_t configure_lora_kernels(int device);
 // tensor-core MBGMM kernels (mbgmm.cu); units are built on the host.
 constexpr int kMgTileTok = 64;   // tokens per tile (4 mma m-tiles)
 constexpr int kMgRows = 16;      // stored A rows per shrink unit
-constexpr int kMgCols = 1024;    // output columns per expand unit
+constexpr int kMgCols = 1024;    // output columns per expand unit (rank <= 32; 512 above)
+// expand slab width: B slab of r x cols 16-bit <= 64 KB (two CTAs per SM)
+inline int mbgmm_expand_cols(int rank) { return rank <= 32 ? kMgCols : kMgCols / 2; }
 constexpr int kMgDefaultTheta = 32;  // run length from which MBGMM is used (SLORA_MBGMM_MIN)
 struct MgUnit {
     const int32_t* tab;  // adapter page table
