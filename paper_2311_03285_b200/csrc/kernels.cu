@@ -272,7 +272,10 @@ __host__ __device__ inline int shrink_rows_per_slot(int64_t K, int es) {
     return int((kSlotBytes + 128) / (K * es + 16));  // rows * (K*es + 16) <= kSlotBytes + 128 < slot_stride
 }
 // expand rows (B row slices of rowb bytes) also sit at a 16-byte stagger
-__host__ __device__ inline int expand_rows_per_slot(uint32_t rowb) { return int((kSlotBytes + 128) / (rowb + 16)); }
+__host__ __device__ inline int expand_rows_per_slot(uint32_t rowb) {  // a multiple of 4 (unrolled axpys) when >= 4
+    const int n = int((kSlotBytes + 128) / (rowb + 16));
+    return n >= 4 ? (n & ~3) : n;
+}
 // x row buffers: two (the next shrink piece's x loads while this one
 // computes) unless the rows are wide (16 KB: one, to keep the ring deep)
 __host__ __device__ inline int x_buffers(int64_t K, int es) { return K * es <= 8192 ? 2 : 1; }
@@ -850,7 +853,7 @@ __global__ void __launch_bounds__(kThreads, 1) mbgmv_kernel(const __grid_constan
     const int rps_s = shrink_rows_per_slot(K, ES);            // shrink rows per slot
     const size_t SS = slot_stride(MODE, K, ES);               // ring slot stride
     const int nxb = x_buffers(K, ES);                         // x row buffers
-    constexpr int kRoles = kConsumerWarps + 3;               // mempty arrivals: consumers, 2 streamers, prefetcher
+    constexpr int kRoles = kConsumerWarps + kStreamers + 1;  // mempty arrivals: consumers, streamers, prefetcher
 
     if (tid == 0) TRACE(0);
     if (tid == 0) {
@@ -948,14 +951,14 @@ __global__ void __launch_bounds__(kThreads, 1) mbgmv_kernel(const __grid_constan
             meta[m].kind = kPieceStop;
             mbar_arrive(&mfull[m]);
         }
-    } else if (warp == kWarpStreamer0 || warp == kWarpStreamer1) {
+    } else if (streamer_id(warp) >= 0) {
         // ============================ streamers ===========================
-        // Two warps issue alternate ring slots (bulk-copy issue costs ~90 ns
+        // kStreamers warps issue ring slots round robin (bulk-copy issue costs ~90 ns
         // per copy per warp, measured; two issuers double the rate).
         // Adapter pages are written only by the loader's scatter kernel, which
         // never triggers its dependents early, so the first piece's pages are
         // streamed before griddepcontrol.wait; x, y and v only after it.
-        const int sid = warp == kWarpStreamer0 ? 0 : 1;
+        const int sid = streamer_id(warp);
         Ring rg;
         uint32_t seq = 0;  // slot sequence number (shared numbering, both warps)
         bool waited = false;
@@ -970,7 +973,7 @@ __global__ void __launch_bounds__(kThreads, 1) mbgmv_kernel(const __grid_constan
             const uint32_t rowb = S ? arow_bytes : uint32_t(M.dcols * ES);
             const int rps = S ? rps_s : expand_rows_per_slot(rowb);
             auto issue_slot = [&](int base) {
-                const bool mine = (seq++ & 1u) == uint32_t(sid);
+                const bool mine = (seq++ % uint32_t(kStreamers)) == uint32_t(sid);
                 if (!mine) {
                     rg.advance(ns);
                     return;

@@ -52,14 +52,26 @@ static_assert(sizeof(DevPiece) == 16, "DevPiece layout");
 
 constexpr int kItemTokCap = 4;   // tokens per item (larger segments are chunked)
 constexpr int kMaxRank = 64;     // max rank of the MBGMV path
-constexpr int kShrinkRows = 16;  // A rows per shrink piece
+#ifndef SLORA_SHRINK_ROWS
+#define SLORA_SHRINK_ROWS 8
+#endif
+constexpr int kShrinkRows = SLORA_SHRINK_ROWS;  // A rows per shrink piece
 constexpr int kConsumerWarps = 8;
 // warp roles: 0-7 consumers, then streamer 0, resolver, streamer 1, expand-v
-// prefetcher, shrink publisher
+// prefetcher, shrink publisher, streamers 2.. (bulk-copy issue costs ~90 ns
+// per copy per warp, measured: more issuers stream 4 KB row slices faster)
+#ifndef SLORA_STREAMERS
+#define SLORA_STREAMERS 2
+#endif
+constexpr int kStreamers = SLORA_STREAMERS;
 constexpr int kWarpStreamer0 = kConsumerWarps, kWarpResolver = kConsumerWarps + 1,
               kWarpStreamer1 = kConsumerWarps + 2, kWarpPrefetch = kConsumerWarps + 3,
-              kWarpPublish = kConsumerWarps + 4;
-constexpr int kThreads = (kConsumerWarps + 5) * 32;
+              kWarpPublish = kConsumerWarps + 4, kWarpStreamerX = kConsumerWarps + 5;
+constexpr int kThreads = (kConsumerWarps + 3 + kStreamers) * 32;
+// streamer index of a warp (-1: not a streamer)
+inline __host__ __device__ int streamer_id(int warp) {
+    return warp == kWarpStreamer0 ? 0 : warp == kWarpStreamer1 ? 1 : (warp >= kWarpStreamerX ? 2 + warp - kWarpStreamerX : -1);
+}
 constexpr int kMaxChunks = 8;    // pages one stored A row spans (TP q/k/v: N)
 constexpr int kSlotBytes = 32 * 1024;  // ring slot
 constexpr int kMaxSlots = 16;
