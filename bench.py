@@ -135,7 +135,7 @@ class Workload:
         kv_tokens = 16  # KV pages of every request interleaved with adapter pages
         kv_pages = 2 * kv_tokens * layers * len(b.requests)
         self.pool = Pool(self.H, layers, need + kv_pages + 64, dtype=cfg.dtype, device=device, tp_size=tp,
-                         tp_rank=rank, order="shuffle", seed=1234 + rank,
+                         tp_rank=rank, order=os.environ.get("SLORA_BENCH_ORDER", "shuffle"), seed=1234 + rank,
                          max_adapters=max(256, len(b.ranks) + 8))
         rid = 0
         reqs = list(b.requests)

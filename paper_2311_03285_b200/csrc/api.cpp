@@ -116,7 +116,7 @@ int esize_of(slora_dtype d) { return d == SLORA_F32 ? 4 : 2; }
 // columns (<= 256 16-byte vectors: one per consumer thread; measured: bulk
 // copies of >= 2 KB stream at full rate).  ns = ring slots filling smem.
 // SLORA_DCHUNK overrides the expand width.
-KernelCfg make_kernel_cfg(int mode, int64_t K, int64_t D, int64_t P, int es, int dtype) {
+KernelCfg make_kernel_cfg(int mode, int64_t K, int64_t D, int64_t P, int es, int dtype, bool want_v8 = false) {
     (void)P;
     KernelCfg k;
     k.mode = mode;
@@ -143,6 +143,23 @@ KernelCfg make_kernel_cfg(int mode, int64_t K, int64_t D, int64_t P, int es, int
         return e ? atoi(e) : 0;
     }();
     if (ns_cap >= 2) ns = std::min(ns, ns_cap);
+    // warp-task kernel (mbgmv8.cu) when asked for (see fused_kc)
+    static const int64_t ebytes = [] {
+        const char* e = getenv("SLORA_V8_EBYTES");
+        return e ? int64_t(atoll(e)) : int64_t(16384);
+    }();
+    if (want_v8) {
+        k.v8 = true;
+        k.ebytes = ebytes;
+        k.ns = 0;
+        k.smem = 0;
+        int dev = 0, sms = 0;
+        cudaGetDevice(&dev);
+        if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) sms = 148;
+        k.grid = sms;
+        k.ok = true;
+        return k;
+    }
     if (ns < 2) return k;
     k.ns = ns;
     k.smem = lora_smem_bytes(mode, K, k.dchunk, ns, es);
@@ -174,7 +191,7 @@ struct slora_pool {
     bool release_pending = false;
     // kernel configurations: 0 fused (K=D=H), 1 shrink q/k/v (K=H),
     // 2 shrink o (K=H/N), 3 expand (D=H/N)
-    KernelCfg kcfg[4];
+    KernelCfg kcfg[5];  // 0 fused (ring pipeline), 1 shrink q/k/v, 2 shrink o, 3 expand, 4 fused warp-task
     long long* trace_dev = nullptr;   // SLORA_TRACE=1: kernel event timestamps
     // rotating per-launch slots: item-done counters (zeroed once; each item's
     // last expand piece re-zeroes its counter) and the fused v workspace
@@ -182,6 +199,7 @@ struct slora_pool {
     int64_t sync_stride = 0;          // ints per slot
     float* ws_dev = nullptr;
     int64_t ws_stride = 0;            // floats per slot
+    float* ws_slot_base = nullptr;    // slot of the call being launched
     uint64_t launch_seq = 0;
 
     int64_t free_pages() const { return int64_t(free_stack.size()); }
@@ -216,10 +234,11 @@ struct slora_batch {
         uint32_t mask = 0;
         std::vector<DevItem> items;
         std::vector<DevPiece> pieces;   // grouped by CTA (schedule_pieces)
+        std::vector<DevTask8> tasks8;   // v8 kernel: pieces with their items folded in
         std::vector<int32_t> cta_off;   // grid + 1
         std::vector<MgUnit> mg_s, mg_e; // MBGMM shrink / expand units (fused calls with long runs)
         size_t off_items = 0, off_pieces = 0, off_cta = 0, off_mg_s = 0, off_mg_e = 0;
-    } calls[4][5];
+    } calls[5][5];
     // per segment: token ranges [begin, end) of the segment's token list that
     // are MBGMM runs (>= theta consecutive x rows; fused 16-bit calls only)
     std::vector<std::vector<std::pair<int32_t, int32_t>>> runs;
@@ -289,6 +308,7 @@ extern "C" slora_status slora_pool_create(const slora_pool_config* cfg, slora_po
         if ((e = cudaSetDevice(cfg->device))) return cleanup(e, "cudaSetDevice");
         if ((e = configure_lora_kernels(cfg->device))) return cleanup(e, "configure kernels");
         if ((e = configure_mbgmm_kernels())) return cleanup(e, "configure MBGMM kernels");
+        if ((e = configure_lora8_kernels())) return cleanup(e, "configure MBGMV kernels");
         if ((e = cudaMalloc(&p->slot_tab_dev, sizeof(int32_t*) * size_t(cfg->max_adapters))))
             return cleanup(e, "cudaMalloc slot table");
         if ((e = cudaMemset(p->slot_tab_dev, 0, sizeof(int32_t*) * size_t(cfg->max_adapters))))
@@ -308,8 +328,9 @@ extern "C" slora_status slora_pool_create(const slora_pool_config* cfg, slora_po
         p->kcfg[1] = make_kernel_cfg(kShrink, H, P, P, es, dt);
         p->kcfg[2] = make_kernel_cfg(kShrink, cfg->tp_size > 1 ? P : H, P, P, es, dt);
         p->kcfg[3] = make_kernel_cfg(kExpand, P, P, P, es, dt);
+        p->kcfg[4] = make_kernel_cfg(kFused, H, H, P, es, dt, true);
         if (const char* vb = getenv("SLORA_VERBOSE"); vb && atoi(vb) > 0)
-            for (int c = 0; c < 4; ++c)
+            for (int c = 0; c < 5; ++c)
                 fprintf(stderr, "slora: kcfg[%d] mode=%d K=%lld D=%lld dchunk=%lld ns=%d smem=%zu grid=%d ok=%d\n", c,
                         p->kcfg[c].mode, (long long)p->kcfg[c].K, (long long)p->kcfg[c].D,
                         (long long)p->kcfg[c].dchunk, p->kcfg[c].ns, p->kcfg[c].smem, p->kcfg[c].grid,
@@ -771,15 +792,22 @@ void build_call(slora_batch* b, const KernelCfg& k, int N, int nproj, uint32_t m
         return e ? atoi(e) : 0;
     }();
     auto item_dchunk = [&](int rank) -> int64_t {
+        if (k.v8) {  // ~ebytes of B per expand task, in whole warp passes (32 lanes x 16 B)
+            const int64_t pass = 32 * 16 / es;
+            int64_t c = (k.ebytes / (int64_t(rank) * es) + pass - 1) / pass * pass;
+            c = std::max<int64_t>(pass, std::min<int64_t>(c, (k.D + pass - 1) / pass * pass));
+            return c;
+        }
         const int64_t half = k.dchunk / 2;
         if (hirank > 0 && rank >= hirank && half > 0 && k.D % half == 0 && (half * es) % 16 == 0) return half;
         return k.dchunk;
     };
     auto item_n_ep = [&](int rank) -> int64_t {
-        if (k.mode == kShrink || k.dchunk <= 0) return 0;
+        if (k.mode == kShrink || (k.dchunk <= 0 && !k.v8)) return 0;
         const int64_t dc = item_dchunk(rank);
         return (k.D + dc - 1) / dc;
     };
+    const int srows = k.v8 ? 1 : kShrinkRows;  // stored A rows per shrink piece
     const bool use_runs = k.mode == kFused && b->n_runs > 0;
     call.mg_s.clear();
     call.mg_e.clear();
@@ -810,7 +838,7 @@ void build_call(slora_batch* b, const KernelCfg& k, int N, int nproj, uint32_t m
                     it.nt = std::min(kItemTokCap, rg.second - t0);
                     it.tok_off = s.tok_off + t0;
                     it.scale = s.scale;
-                    it.n_sp = (k.mode == kExpand) ? 0 : (ra + kShrinkRows - 1) / kShrinkRows;
+                    it.n_sp = (k.mode == kExpand) ? 0 : (ra + srows - 1) / srows;
                     it.n_ep = int32_t(item_n_ep(s.rank));
                     call.items.push_back(it);
                 }
@@ -847,8 +875,8 @@ void build_call(slora_batch* b, const KernelCfg& k, int N, int nproj, uint32_t m
         const int proj = proj_ids[it.pi];
         const int ra = it.rank / ((k.mode == kExpand) ? 1 : ((proj < 3) ? N : 1));
         if (k.mode != kExpand)
-            for (int r0 = 0; r0 < ra; r0 += kShrinkRows) {
-                const int nr = std::min(kShrinkRows, ra - r0);
+            for (int r0 = 0; r0 < ra; r0 += srows) {
+                const int nr = std::min(srows, ra - r0);
                 pieces.push_back({kPieceS, ii, r0, nr});
                 cost.push_back(int64_t(nr) * k.K * es + kPieceOverhead);
             }
@@ -860,11 +888,49 @@ void build_call(slora_batch* b, const KernelCfg& k, int N, int nproj, uint32_t m
             }
     }
     schedule_pieces(pieces, cost, k.grid, call.pieces, call.cta_off);
+    call.tasks8.clear();
+    if (k.v8)
+        for (const DevPiece& pc : call.pieces) {
+            const DevItem& it = call.items[size_t(pc.item)];
+            DevTask8 t{};
+            t.tab = it.tab;
+            t.vrow = it.vrow;
+            t.kind = pc.kind;
+            t.a = pc.a;
+            t.b = pc.b;
+            t.item = pc.item;
+            t.rank = it.rank;
+            t.pi = it.pi;
+            t.nt = it.nt;
+            t.tok_off = it.tok_off;
+            t.n_sp = it.n_sp;
+            t.n_ep = it.n_ep;
+            t.scale = it.scale;
+            call.tasks8.push_back(t);
+        }
 }
 }  // namespace
 
 namespace {
 slora_status ensure_call(slora_pool* p, slora_batch* b, int kc, uint32_t mask, void* stream);
+
+// Which single-GPU fused kernel serves a call of np projections.  Measured on
+// C2 decode (tools/layer_micro.py, graphs of 32 layers): the ring pipeline
+// (kernels.cu) streams the large q/k/v call faster (24.4 vs 36 us per launch);
+// the warp-task kernel (mbgmv8.cu) wins an o-only sequence (17.3 vs 19.4 us)
+// but not the interleaved q/k/v + o layer (21.8 vs 21.7 us per launch), so the
+// ring pipeline serves every call by default.  SLORA_MBGMV=warp selects the
+// warp-task kernel for every call, SLORA_MBGMV=auto for the o call only.
+int fused_kc(const slora_pool* p, int np) {
+    static const int force = [] {
+        const char* e = getenv("SLORA_MBGMV");
+        if (!e) return 1;
+        return std::string(e) == "warp" ? 2 : (std::string(e) == "auto" ? 0 : 1);
+    }();
+    const bool v8 = force == 2 || (force == 0 && np == 1);
+    if (v8 && p->kcfg[4].ok) return 4;
+    return 0;
+}
 }
 
 extern "C" slora_status slora_batch_prepare(slora_batch_t b, const int64_t* tok_adapter, int32_t T, void* stream) {
@@ -960,10 +1026,10 @@ extern "C" slora_status slora_batch_prepare(slora_batch_t b, const int64_t* tok_
     int64_t chunks = 0;
     for (const DevSeg& s : b->segs) chunks += (s.n_tok + kItemTokCap - 1) / kItemTokCap;
     const int64_t max_items = 4 * chunks;
-    const int64_t max_pieces_per_item = (kMaxRank + kShrinkRows - 1) / kShrinkRows + 64;
+    const int64_t max_pieces_per_item = kMaxRank + 64;  // v8: one piece per stored A row
     const size_t need = 256 + size_t(T) * 4 + 16 * (1024 + 4 * 1024 + size_t(b->mg_units_max) * sizeof(MgUnit) +
                                                    size_t(max_items) * sizeof(DevItem) +
-                                                   size_t(max_items * max_pieces_per_item) * sizeof(DevPiece));
+                                                   size_t(max_items * max_pieces_per_item) * sizeof(DevTask8));
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     CUDA_TRY(cudaSetDevice(p->cfg.device));
     if (b->upload_pending) CUDA_TRY(cudaEventSynchronize(b->upload_ev));  // pinned arena free again
@@ -984,6 +1050,9 @@ extern "C" slora_status slora_batch_prepare(slora_batch_t b, const int64_t* tok_
     if (e) return fail(SLORA_ERR_CUDA, "batch upload: %s", cudaGetErrorString(e));
     // per-launch sync slots and fused workspace, sized for this batch
     const int64_t sync_need = 2 + max_items + 32;
+    // workspace slot = three regions of ws_need floats: the ring kernel's v,
+    // the warp-task kernel's v (readiness flags, kept "empty" between
+    // launches) and MBGMM's v
     const int64_t ws_need = 4 * b->NR + 64;
     if (sync_need > p->sync_stride) {
         if (p->sync_dev) CUDA_TRY(cudaFreeAsync(p->sync_dev, s));
@@ -994,16 +1063,18 @@ extern "C" slora_status slora_batch_prepare(slora_batch_t b, const int64_t* tok_
     }
     if (ws_need > p->ws_stride) {
         if (p->ws_dev) CUDA_TRY(cudaFreeAsync(p->ws_dev, s));
-        const int64_t st = ws_need * 2;
+        const int64_t st = ws_need * 3;
         CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&p->ws_dev), sizeof(float) * st * kLaunchSlots, s));
+        // all entries "empty" (0xFFFFFFFF): the warp-task kernel's readiness flags (mbgmv8.cu stage_v)
+        CUDA_TRY(cudaMemsetAsync(p->ws_dev, 0xFF, sizeof(float) * st * kLaunchSlots, s));
         p->ws_stride = st;
     }
     // eager descriptors for the usual calls (q/k/v together, o alone)
     slora_status st2 = SLORA_OK;
     if (b->adapted > 0) {
         if (p->N() == 1) {
-            if (!st2 && p->kcfg[0].ok) st2 = ensure_call(p, b, 0, 0x7, stream);
-            if (!st2 && p->kcfg[0].ok) st2 = ensure_call(p, b, 0, 0x8, stream);
+            if (!st2) st2 = ensure_call(p, b, fused_kc(p, 3), 0x7, stream);
+            if (!st2) st2 = ensure_call(p, b, fused_kc(p, 1), 0x8, stream);
         } else {
             if (!st2 && p->kcfg[1].ok) st2 = ensure_call(p, b, 1, 0x7, stream);
             if (!st2 && p->kcfg[2].ok) st2 = ensure_call(p, b, 2, 0x8, stream);
@@ -1056,7 +1127,10 @@ slora_status ensure_call(slora_pool* p, slora_batch* b, int kc, uint32_t mask, v
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     cudaError_t e = cudaSuccess;
     call.off_items = arena_put(b, call.items.data(), call.items.size() * sizeof(DevItem), s, e);
-    if (!e) call.off_pieces = arena_put(b, call.pieces.data(), call.pieces.size() * sizeof(DevPiece), s, e);
+    if (!e && call.tasks8.empty())
+        call.off_pieces = arena_put(b, call.pieces.data(), call.pieces.size() * sizeof(DevPiece), s, e);
+    if (!e && !call.tasks8.empty())
+        call.off_pieces = arena_put(b, call.tasks8.data(), call.tasks8.size() * sizeof(DevTask8), s, e);
     if (!e) call.off_cta = arena_put(b, call.cta_off.data(), call.cta_off.size() * sizeof(int32_t), s, e);
     if (!e) call.off_mg_s = arena_put(b, call.mg_s.data(), call.mg_s.size() * sizeof(MgUnit), s, e);
     if (!e) call.off_mg_e = arena_put(b, call.mg_e.data(), call.mg_e.size() * sizeof(MgUnit), s, e);
@@ -1090,6 +1164,7 @@ slora_status prepare_call(slora_pool* p, slora_batch* b, int kc, int32_t layer, 
     q.tok_idx = reinterpret_cast<const int32_t*>(base + b->off_tok);
     q.items = reinterpret_cast<const DevItem*>(base + call.off_items);
     q.pieces = reinterpret_cast<const DevPiece*>(base + call.off_pieces);
+    q.tasks = reinterpret_cast<const DevTask8*>(base + call.off_pieces);
     q.cta_off = reinterpret_cast<const int32_t*>(base + call.off_cta);
     q.n_pieces = int32_t(call.pieces.size());
     q.n_items = int32_t(call.items.size());
@@ -1111,7 +1186,8 @@ slora_status prepare_call(slora_pool* p, slora_batch* b, int kc, int32_t layer, 
         q.a_div[pj] = (pj < 3) ? N : 1;
         q.a_row_pages[pj] = (pj < 3) ? N : 1;
     }
-    if (k.mode == kFused) q.v = p->ws_dev + int64_t(slot) * p->ws_stride;
+    p->ws_slot_base = p->ws_dev + int64_t(slot) * p->ws_stride;
+    if (k.mode == kFused) q.v = p->ws_slot_base + (k.v8 ? p->ws_stride / 3 : 0);
     q.trace = p->trace_dev;
     return SLORA_OK;
 }
@@ -1120,7 +1196,10 @@ slora_status launch(slora_pool* p, int kc, LoraParams& q, void* stream) {
     const KernelCfg& k = p->kcfg[kc];
     CUDA_TRY(cudaSetDevice(p->cfg.device));
     const int dt = p->cfg.dtype == SLORA_F32 ? kF32 : (p->cfg.dtype == SLORA_F16 ? kF16 : kBF16);
-    CUDA_TRY(launch_lora(q, k.mode, dt, k.grid, static_cast<cudaStream_t>(stream), k.smem));
+    if (k.v8)
+        CUDA_TRY(launch_lora8(q, k.mode, dt, k.grid, static_cast<cudaStream_t>(stream)));
+    else
+        CUDA_TRY(launch_lora(q, k.mode, dt, k.grid, static_cast<cudaStream_t>(stream), k.smem));
     return ok();
 }
 }  // namespace
@@ -1159,7 +1238,7 @@ slora_status launch_mbgmm_pair(slora_pool* p, slora_batch* b, const slora_batch:
     uint8_t* base = static_cast<uint8_t*>(b->arena_dev);
     m.pool = p->cfg.device_buffer;
     m.page_elems = p->P;
-    m.v = q.v;
+    m.v = p->ws_slot_base + 2 * (p->ws_stride / 3);  // the slot's MBGMM region (see slora_batch_prepare)
     for (int pj = 0; pj < 4; ++pj) {
         m.y[pj] = q.y[pj];
         m.ldy[pj] = q.ldy[pj];
@@ -1192,8 +1271,11 @@ extern "C" slora_status slora_lora_apply(slora_pool_t p, slora_batch_t b, int32_
         if (mask & (1u << pj))
             if (!y[pj] || !aligned16(y[pj], ldy[pj], p->es) || ldy[pj] < p->cfg.hidden)
                 return fail(SLORA_ERR_SHAPE, "y[%d] alignment/stride", pj);
+    int np = 0;
+    for (int pj = 0; pj < 4; ++pj) np += (mask >> pj) & 1;
+    const int kc = fused_kc(p, np);
     LoraParams q;
-    st = prepare_call(p, b, 0, layer, mask, stream, q);
+    st = prepare_call(p, b, kc, layer, mask, stream, q);
     if (st) return st;
     q.x = x;
     q.ldx = ldx;
@@ -1202,12 +1284,12 @@ extern "C" slora_status slora_lora_apply(slora_pool_t p, slora_batch_t b, int32_
         q.ldy[pj] = ldy[pj];
     }
     q.v_blocks = 1;
-    const slora_batch::Call& call = b->calls[0][q.nproj];
+    const slora_batch::Call& call = b->calls[kc][q.nproj];
     if (!call.mg_s.empty()) {
         st = launch_mbgmm_pair(p, b, call, q, x, ldx, stream);
         if (st) return st;
     }
-    return launch(p, 0, q, stream);
+    return launch(p, kc, q, stream);
 }
 
 extern "C" slora_status slora_lora_v_elems(slora_batch_t b, uint32_t mask, int32_t div, int64_t* out) {

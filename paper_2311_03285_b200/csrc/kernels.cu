@@ -278,7 +278,10 @@ __host__ __device__ inline int expand_rows_per_slot(uint32_t rowb) {  // a multi
 }
 // x row buffers: two (the next shrink piece's x loads while this one
 // computes) unless the rows are wide (16 KB: one, to keep the ring deep)
-__host__ __device__ inline int x_buffers(int64_t K, int es) { return K * es <= 8192 ? 2 : 1; }
+#ifndef SLORA_XBUF
+#define SLORA_XBUF 2
+#endif
+__host__ __device__ inline int x_buffers(int64_t K, int es) { return K * es <= 8192 ? SLORA_XBUF : 1; }
 __host__ __device__ inline size_t slot_stride(int mode, int64_t K, int es) {
     const int rps = mode == kExpand ? 0 : shrink_rows_per_slot(K, es);
     return size_t(kSlotBytes) + 256 + size_t((16 * rps) & 127);
@@ -439,6 +442,9 @@ __device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r
                  : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
                  : "r"(addr));
 }
+#ifndef SLORA_SHRINK_NACC
+#define SLORA_SHRINK_NACC 4
+#endif
 template <typename T> struct MmaOp {  // fp32: never used (no TF32 for fp32 inputs)
     __device__ static void run(float (&)[4], uint32_t, uint32_t, uint32_t, uint32_t) {}
 };
@@ -500,6 +506,10 @@ __device__ __forceinline__ void shrink_piece_mma(const LoraParams& p, const Piec
             uint32_t lap = l0;
             if (a >= ns) { a -= ns; ++lap; }
             mbar_wait(&full[a], lap & 1);
+            if (warp == 0 && lane == 0) {
+                const int sq = int(lap) * ns + a;
+                if (sq < 240) TRACE(512 + sq);
+            }
         }
         if (gb == 0 && warp == 0 && lane == 0 && i < 48) TRACE(304 + i);
         if (math) {
@@ -510,8 +520,9 @@ __device__ __forceinline__ void shrink_piece_mma(const LoraParams& p, const Piec
             if (a >= ns) a -= ns;
             const uint32_t bbase = ring_u32 + uint32_t(a) * uint32_t(SS) + uint32_t(row & (rps - 1)) * srow +
                                    uint32_t(k0w + mi * 8) * ES;
-            float d[4] = {0.f, 0.f, 0.f, 0.f};
             const int npair = kslice >> 5;  // k-step pairs
+#if SLORA_SHRINK_NACC == 1
+            float d[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll 4
             for (int kp = 0; kp < npair; ++kp) {
                 uint32_t xa0, xa1, xa2, xa3, b0, b1, b2, b3;
@@ -520,6 +531,39 @@ __device__ __forceinline__ void shrink_piece_mma(const LoraParams& p, const Piec
                 MmaOp<T>::run(d, xa0, xa1, b0, b1);
                 MmaOp<T>::run(d, xa2, xa3, b2, b3);
             }
+#else
+            // four independent accumulators (k-steps 4q .. 4q+3): the MMA
+            // dependency chain is npair/2 deep instead of 2*npair; combined in
+            // a fixed order at the end (deterministic)
+            float da[4][4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) da[u][0] = da[u][1] = da[u][2] = da[u][3] = 0.f;
+            int kp = 0;
+#pragma unroll 2
+            for (; kp + 1 < npair; kp += 2) {
+                uint32_t xa[2][4], bb[2][4];
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    ldsm_x4(xbase + uint32_t(kp + u) * xadv, xa[u][0], xa[u][1], xa[u][2], xa[u][3]);
+                    ldsm_x4(bbase + uint32_t(kp + u) * (32u * ES), bb[u][0], bb[u][1], bb[u][2], bb[u][3]);
+                }
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    MmaOp<T>::run(da[2 * u], xa[u][0], xa[u][1], bb[u][0], bb[u][1]);
+                    MmaOp<T>::run(da[2 * u + 1], xa[u][2], xa[u][3], bb[u][2], bb[u][3]);
+                }
+            }
+            if (kp < npair) {
+                uint32_t xa0, xa1, xa2, xa3, b0, b1, b2, b3;
+                ldsm_x4(xbase + uint32_t(kp) * xadv, xa0, xa1, xa2, xa3);
+                ldsm_x4(bbase + uint32_t(kp) * (32u * ES), b0, b1, b2, b3);
+                MmaOp<T>::run(da[0], xa0, xa1, b0, b1);
+                MmaOp<T>::run(da[1], xa2, xa3, b2, b3);
+            }
+            float d[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) d[e] = (da[0][e] + da[1][e]) + (da[2][e] + da[3][e]);
+#endif
             // d0, d1: token g, rows gb + 2c, gb + 2c + 1 (d2, d3: tokens g + 8, zero)
             if (g < nt) {
                 if (gb + 2 * c < nrows) red[(warp * kShrinkRows + gb + 2 * c) * kItemTokCap + g] = d[0];

@@ -50,6 +50,19 @@ struct DevPiece {
 };
 static_assert(sizeof(DevPiece) == 16, "DevPiece layout");
 
+// The warp-task kernel's unit (mbgmv8.cu): a piece with its item's fields
+// folded in, so that a warp resolves it with one load + one page-table hop.
+struct DevTask8 {
+    const int32_t* tab;  // the adapter's device page table
+    int64_t vrow;        // v row offset of the item's token chunk
+    int32_t kind, a, b, item;
+    int32_t rank, pi, nt, tok_off;
+    int32_t n_sp, n_ep;
+    float scale;
+    int32_t pad;
+};
+static_assert(sizeof(DevTask8) == 64, "DevTask8 layout");
+
 constexpr int kItemTokCap = 4;   // tokens per item (larger segments are chunked)
 constexpr int kMaxRank = 64;     // max rank of the MBGMV path
 #ifndef SLORA_SHRINK_ROWS
@@ -89,6 +102,7 @@ struct LoraParams {
     const int32_t* tok_idx;
     const DevItem* items;
     const DevPiece* pieces;       // grouped by CTA: CTA b runs pieces [cta_off[b], cta_off[b+1])
+    const DevTask8* tasks;        // v8: the same pieces with their items folded in
     const int32_t* cta_off;       // grid + 1 entries
     int32_t n_pieces;
     int32_t n_items;
@@ -121,6 +135,8 @@ struct KernelCfg {
     size_t smem = 0;
     int grid = 0;                 // persistent CTAs
     bool ok = false;
+    bool v8 = false;              // warp-task kernel (mbgmv8.cu) instead of the ring pipeline
+    int64_t ebytes = 0;           // v8: target B bytes per expand task (rank-dependent column chunk)
 };
 
 // smem bytes for a launch (host and device agree via smem_layout in kernels.cu)
@@ -129,6 +145,15 @@ size_t lora_slot_stride(int mode, int64_t K, int esize);  // ring slot stride (b
 int lora_max_ctas(int mode, int dtype, size_t smem);
 cudaError_t launch_lora(const LoraParams& p, int mode, int dtype, int grid, cudaStream_t s, size_t smem);
 cudaError_t configure_lora_kernels(int device);
+// warp-task MBGMV (mbgmv8.cu): kW8 warps per CTA, one CTA per SM, one stored A
+// row per shrink task
+#ifndef SLORA_W8
+#define SLORA_W8 8
+#endif
+constexpr int kW8 = SLORA_W8;
+size_t lora8_smem_bytes();
+cudaError_t configure_lora8_kernels();
+cudaError_t launch_lora8(const LoraParams& p, int mode, int dtype, int grid, cudaStream_t s);
 
 // ------------------------------------------------------------------ MBGMM
 // Long prefill runs (>= theta consecutive x rows of one adapter) go to the
