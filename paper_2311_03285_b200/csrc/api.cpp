@@ -200,6 +200,7 @@ struct slora_pool {
     float* ws_dev = nullptr;
     int64_t ws_stride = 0;            // floats per slot
     float* ws_slot_base = nullptr;    // slot of the call being launched
+    int64_t ws_region = 0;            // floats per workspace region: ring v, warp-task v, MBGMM v (kMgKsplit parts)
     uint64_t launch_seq = 0;
 
     int64_t free_pages() const { return int64_t(free_stack.size()); }
@@ -853,11 +854,16 @@ void build_call(slora_batch* b, const KernelCfg& k, int N, int nproj, uint32_t m
                     u.row0 = b->tok_idx[size_t(s.tok_off + t0)];
                     u.nt = std::min(kMgTileTok, rn.second - t0);
                     u.scale = s.scale;
-                    for (int r0 = 0; r0 < s.rank; r0 += kMgRows) {
-                        u.a = r0;
-                        u.b = std::min(kMgRows, s.rank - r0);
-                        call.mg_s.push_back(u);
-                    }
+                    const bool whole = mbgmm_shrink_whole_rank();
+                    const int srows = whole ? s.rank : kMgRows;  // A rows per shrink unit
+                    for (int r0 = 0; r0 < s.rank; r0 += srows)
+                        for (int ks = 0; ks < (whole ? kMgKsplit : 1); ++ks) {  // tcgen05: k-split parts
+                            u.a = r0;
+                            u.b = std::min(srows, s.rank - r0);
+                            u.pad = ks;
+                            call.mg_s.push_back(u);
+                        }
+                    u.pad = 0;
                     const int ecols = mbgmm_expand_cols(s.rank);
                     for (int64_t c0 = 0; c0 < k.D; c0 += ecols) {
                         u.a = int32_t(c0);
@@ -993,7 +999,8 @@ extern "C" slora_status slora_batch_prepare(slora_batch_t b, const int64_t* tok_
             return e ? atoi(e) : kMgDefaultTheta;
         }();
         const bool ok_shape = p->cfg.dtype != SLORA_F32 && p->N() == 1 && theta > 0 && p->cfg.hidden % 64 == 0 &&
-                              p->cfg.hidden % kMgCols % 64 == 0 && mbgmm_smem(false, p->cfg.hidden, 0) <= 227 * 1024;
+                              p->cfg.hidden % kMgCols % 64 == 0 && mbgmm_smem(false, p->cfg.hidden, 0) <= 227 * 1024 &&
+                              (!mbgmm_shrink_whole_rank() || (p->cfg.hidden / 64) % kMgKsplit == 0);
         for (size_t si = 0; ok_shape && si < b->segs.size(); ++si) {
             const DevSeg& sg = b->segs[si];
             int32_t t = 0;
@@ -1063,11 +1070,12 @@ extern "C" slora_status slora_batch_prepare(slora_batch_t b, const int64_t* tok_
     }
     if (ws_need > p->ws_stride) {
         if (p->ws_dev) CUDA_TRY(cudaFreeAsync(p->ws_dev, s));
-        const int64_t st = ws_need * 3;
+        const int64_t st = ws_need * (2 + kMgKsplit);
         CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&p->ws_dev), sizeof(float) * st * kLaunchSlots, s));
         // all entries "empty" (0xFFFFFFFF): the warp-task kernel's readiness flags (mbgmv8.cu stage_v)
         CUDA_TRY(cudaMemsetAsync(p->ws_dev, 0xFF, sizeof(float) * st * kLaunchSlots, s));
         p->ws_stride = st;
+        p->ws_region = ws_need;
     }
     // eager descriptors for the usual calls (q/k/v together, o alone)
     slora_status st2 = SLORA_OK;
@@ -1187,7 +1195,7 @@ slora_status prepare_call(slora_pool* p, slora_batch* b, int kc, int32_t layer, 
         q.a_row_pages[pj] = (pj < 3) ? N : 1;
     }
     p->ws_slot_base = p->ws_dev + int64_t(slot) * p->ws_stride;
-    if (k.mode == kFused) q.v = p->ws_slot_base + (k.v8 ? p->ws_stride / 3 : 0);
+    if (k.mode == kFused) q.v = p->ws_slot_base + (k.v8 ? p->ws_region : 0);
     q.trace = p->trace_dev;
     return SLORA_OK;
 }
@@ -1238,7 +1246,9 @@ slora_status launch_mbgmm_pair(slora_pool* p, slora_batch* b, const slora_batch:
     uint8_t* base = static_cast<uint8_t*>(b->arena_dev);
     m.pool = p->cfg.device_buffer;
     m.page_elems = p->P;
-    m.v = p->ws_slot_base + 2 * (p->ws_stride / 3);  // the slot's MBGMM region (see slora_batch_prepare)
+    m.v = p->ws_slot_base + 2 * p->ws_region;  // the slot's MBGMM regions (see slora_batch_prepare)
+    m.ksplit = mbgmm_shrink_whole_rank() ? kMgKsplit : 1;
+    m.vpart = p->ws_region;
     for (int pj = 0; pj < 4; ++pj) {
         m.y[pj] = q.y[pj];
         m.ldy[pj] = q.ldy[pj];

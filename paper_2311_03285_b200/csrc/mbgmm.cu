@@ -265,7 +265,10 @@ __global__ void __launch_bounds__(kMgThreads, 2) mbgmm_expand_kernel(const __gri
         for (int q = 0; q < kU; ++q) {
             const int e = e0 + q * kMgConsumers * 32;
             const int t = e / rp, j = e % rp;
-            val[q] = (e < nel && t < u.nt && j < r) ? __ldcg(p.v + u.vbase + int64_t(t) * r + j) : 0.f;
+            float a = 0.f;
+            if (e < nel && t < u.nt && j < r)
+                for (int ks = 0; ks < p.ksplit; ++ks) a += __ldcg(p.v + ks * p.vpart + u.vbase + int64_t(t) * r + j);
+            val[q] = a;  // the shrink's k-split partial sums, added in part order (deterministic)
         }
 #pragma unroll
         for (int q = 0; q < kU; ++q) {
@@ -336,11 +339,212 @@ __global__ void __launch_bounds__(kMgThreads, 2) mbgmm_expand_kernel(const __gri
     }
 }
 
+
+// ------------------------------------------------------------------ tcgen05
+// mbgmm_shrink_tc_kernel<T>: one CTA per (run tile of <= 64 tokens,
+// projection, quarter of K) computes the tile's shrink on the 5th-generation tensor
+// cores: D[token][j] (fp32, TMEM) = sum_k x[token][k] A_j[k] for all r stored
+// A rows at once (N = r rounded up to 16), so x streams through the SM once
+// per tile instead of once per group of A rows.  Per 64-wide k-block:
+//   * the x tile arrives by TMA (2-D tensor map, SWIZZLE_128B = the canonical
+//     K-major layout the tensor core reads), 8 stages of 64 rows x 128 B;
+//     the MMA uses M = 128 (the smallest single-CTA shape with a plain
+//     lane = row accumulator layout): stages are 8 KB apart, so operand rows
+//     64..127 are the next stage's tile and only feed accumulator rows that
+//     are never read back;
+//   * the A k-block (N rows x 128 B, gathered from N pool pages) is copied by
+//     two loader warps with cp.async (16 B per lane) straight into the
+//     canonical layout -- row n at (n/8)*1024 + (n%8)*128, 16-byte chunk c at
+//     (c ^ n%8)*16 -- rows >= r zero-filled; each loader makes its copies
+//     visible to the async proxy (fence.proxy.async) before arriving on the
+//     stage's barrier;
+//   * one thread issues 4 tcgen05.mma.cta_group::1.kind::f16 (K = 16 each,
+//     descriptors advanced 32 B inside the swizzle atom) into 4 independent
+//     TMEM accumulators (k-step j -> accumulator j: short dependency chains),
+//     then tcgen05.commit frees the stage.
+// Epilogue: warps 0-1 (TMEM lanes 0-63 = the tile's tokens) load the 4
+// accumulators (tcgen05.ld.32x32b.x16), add them in a fixed order
+// ((d0 + d1) + (d2 + d3): deterministic) and write the part's partial v; the
+// expand kernel adds the kMgKsplit parts in order.
+constexpr int kTcThreads = 192;  // warps 0-1 epilogue, 2 TMEM + x producer, 3 MMA issuer, 4-5 A loaders
+#ifndef SLORA_TC_STAGES
+#define SLORA_TC_STAGES 6  // 6 x 16 KB: two CTAs per SM
+#endif
+constexpr int kTcStages = SLORA_TC_STAGES;
+constexpr int kTcXStage = kXTileBytes;  // 8 KB (see above: M = 128 windows overlap the next stage)
+constexpr int kTcAStage = 64 * 128;     // N <= 64 rows x 128 B
+constexpr int kTcLoaders = 64;
+constexpr int kTcAhead = 4;             // A stages a loader keeps in flight before publishing
+
+__host__ __device__ inline size_t mg_shrink_tc_smem(int64_t) {
+    return 1024 + 1024 + size_t(kTcStages) * (kTcXStage + kTcAStage) + kTcXStage;
+}
+
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
+    // start address >> 4 (bits 0-13), LBO 1 (unused for swizzled K-major), SBO = 1024 B >> 4 (bits 32-45),
+    // version 1 (bit 46), layout SWIZZLE_128B = 2 (bits 61-63)
+    return uint64_t((saddr >> 4) & 0x3FFF) | (uint64_t(1) << 16) | (uint64_t(64) << 32) | (uint64_t(1) << 46) |
+           (uint64_t(2) << 61);
+}
+template <typename T> struct TcFmt;
+template <> struct TcFmt<__half> { static constexpr uint32_t v = 0; };
+template <> struct TcFmt<__nv_bfloat16> { static constexpr uint32_t v = 1; };
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&d)[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+        "%15}, [%16];"
+        : "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3]), "=r"(d[4]), "=r"(d[5]), "=r"(d[6]), "=r"(d[7]), "=r"(d[8]),
+          "=r"(d[9]), "=r"(d[10]), "=r"(d[11]), "=r"(d[12]), "=r"(d[13]), "=r"(d[14]), "=r"(d[15])
+        : "r"(taddr));
+}
+
 template <typename T>
-cudaError_t launch_kernel(void (*k)(MgParams), const MgParams& p, int grid, size_t smem, cudaStream_t s, bool pdl) {
+__global__ void __launch_bounds__(kTcThreads, 2) mbgmm_shrink_tc_kernel(const __grid_constant__ MgParams p) {
+    extern __shared__ __align__(1024) unsigned char smraw[];
+    unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const MgUnit u = p.units[blockIdx.x];
+    const int K = p.K;
+    const int nkc = K / 64 / p.ksplit;  // k-blocks of this unit's part of K
+    const int kb0 = u.pad * nkc;        // its first k-block
+    float* vout = p.v + u.pad * p.vpart;
+    const int r = u.rank;
+    const int npad = (r + 15) & ~15;  // MMA N
+    uint64_t* xfull = reinterpret_cast<uint64_t*>(sm);
+    uint64_t* afull = xfull + kTcStages;
+    uint64_t* sempty = afull + kTcStages;
+    uint64_t* done = sempty + kTcStages;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+    unsigned char* aring = sm + 1024;                               // kTcStages x 8 KB (1 KB-aligned atoms)
+    unsigned char* xring = aring + size_t(kTcStages) * kTcAStage;   // kTcStages x 8 KB + 8 KB pad
+    if (tid == 0) {
+        for (int s = 0; s < kTcStages; ++s) {
+            bar_init(&xfull[s], 1);
+            bar_init(&afull[s], kTcLoaders);
+            bar_init(&sempty[s], 1);
+        }
+        bar_init(done, 1);
+        bar_fence_init();
+    }
+    if (warp == 2) {  // TMEM: 4 accumulators x 64 columns
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(su32(tmem_slot)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    grid_trigger();
+    const uint32_t tmem = *reinterpret_cast<volatile uint32_t*>(tmem_slot);
+    if (warp >= 4) {
+        // ---- A loaders: thread i copies chunk (i & 7) of rows (i >> 3) + 8 m (pages: loader-written,
+        // safe before the PDL wait)
+        const int i = tid - 128, c = i & 7, n0 = i >> 3;
+        const int proj = p.proj_ids[u.pi];
+        const int32_t* tab = u.tab + int64_t((p.layer * 4 + proj) * 2) * r;
+        const T* pool = static_cast<const T*>(p.pool);
+        const T* src[8];
+#pragma unroll
+        for (int m = 0; m < 8; ++m) {
+            const int n = n0 + 8 * m;
+            src[m] = pool + int64_t(tab[min(n, r - 1)]) * p.page_elems + c * 8;
+        }
+        const uint32_t abase = su32(aring) + uint32_t(n0 & 7) * 128u + uint32_t((c ^ (n0 & 7)) << 4);
+        for (int kc = 0; kc < nkc; ++kc) {
+            const int s = kc % kTcStages;
+            if (kc >= kTcStages) bar_wait(&sempty[s], ((kc / kTcStages) - 1) & 1);
+            const uint32_t dst = abase + uint32_t(s) * kTcAStage;
+#pragma unroll
+            for (int m = 0; m < 8; ++m) {
+                const int n = n0 + 8 * m;
+                if (n < npad)
+                    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst + uint32_t(m) * 1024u),
+                                 "l"(src[m] + int64_t(kb0 + kc) * 64), "r"(n < r ? 16 : 0)
+                                 : "memory");
+            }
+            asm volatile("cp.async.commit_group;" ::: "memory");
+            if (kc >= kTcAhead) {  // publish the stage issued kTcAhead k-blocks ago
+                asm volatile("cp.async.wait_group %0;" ::"n"(kTcAhead) : "memory");
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                bar_arrive(&afull[(kc - kTcAhead) % kTcStages]);
+            }
+        }
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        for (int kc = max(0, nkc - kTcAhead); kc < nkc; ++kc) bar_arrive(&afull[kc % kTcStages]);
+    } else if (tid == 64) {
+        // ---- x producer (after the PDL wait: x is the previous launch's output)
+        grid_wait();
+        for (int kc = 0; kc < nkc; ++kc) {
+            const int s = kc % kTcStages;
+            if (kc >= kTcStages) bar_wait(&sempty[s], ((kc / kTcStages) - 1) & 1);
+            bar_expect(&xfull[s], kXTileBytes);
+            tma_2d(xring + size_t(s) * kTcXStage, &p.xmap, (kb0 + kc) * 64, u.row0, &xfull[s]);
+        }
+    } else if (tid == 96) {
+        // ---- MMA issuer (one thread)
+        const uint32_t idesc = (1u << 4) | (TcFmt<T>::v << 7) | (TcFmt<T>::v << 10) | (uint32_t(npad >> 3) << 17) |
+                               ((128u >> 4) << 24);
+        const uint32_t xb = su32(xring), ab = su32(aring);
+        for (int kc = 0; kc < nkc; ++kc) {
+            const int s = kc % kTcStages;
+            const uint32_t ph = (kc / kTcStages) & 1;
+            bar_wait(&xfull[s], ph);
+            bar_wait(&afull[s], ph);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {  // k-step k (32 B inside the 128-byte swizzle atom) -> accumulator k
+                const uint64_t da = umma_desc_sw128(xb + uint32_t(s) * kTcXStage + uint32_t(k) * 32u);
+                const uint64_t db = umma_desc_sw128(ab + uint32_t(s) * kTcAStage + uint32_t(k) * 32u);
+                const uint32_t acc = kc > 0 ? 1u : 0u;
+                asm volatile(
+                    "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                    "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem + uint32_t(k) * 64u),
+                    "l"(da), "l"(db), "r"(idesc), "r"(acc)
+                    : "memory");
+            }
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                             su32(&sempty[s]))
+                         : "memory");
+        }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(done))
+                     : "memory");
+    } else if (warp < 2) {
+        // ---- epilogue: TMEM lanes 0-63 = the tile's tokens
+        bar_wait(done, 0);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const int t = warp * 32 + lane;
+        const uint32_t lrow = uint32_t(warp * 32) << 16;
+        for (int j0 = 0; j0 < npad; j0 += 16) {
+            uint32_t d0[16], d1[16], d2[16], d3[16];
+            tmem_ld16(tmem + lrow + 0 * 64 + uint32_t(j0), d0);
+            tmem_ld16(tmem + lrow + 1 * 64 + uint32_t(j0), d1);
+            tmem_ld16(tmem + lrow + 2 * 64 + uint32_t(j0), d2);
+            tmem_ld16(tmem + lrow + 3 * 64 + uint32_t(j0), d3);
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            if (t < u.nt)
+#pragma unroll
+                for (int j = 0; j < 16; ++j)
+                    if (j0 + j < r)
+                        vout[u.vbase + int64_t(t) * r + j0 + j] =
+                            (__uint_as_float(d0[j]) + __uint_as_float(d1[j])) +
+                            (__uint_as_float(d2[j]) + __uint_as_float(d3[j]));
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 2) {
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+    }
+}
+
+template <typename T>
+cudaError_t launch_kernel(void (*k)(MgParams), const MgParams& p, int grid, size_t smem, cudaStream_t s, bool pdl,
+                          int threads = kMgThreads) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(unsigned(grid));
-    cfg.blockDim = dim3(kMgThreads);
+    cfg.blockDim = dim3(unsigned(threads));
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
@@ -354,8 +558,23 @@ cudaError_t launch_kernel(void (*k)(MgParams), const MgParams& p, int grid, size
 
 }  // namespace
 
+// SLORA_MBGMM_TC=1 selects the tcgen05 shrink.  Off by default: measured on
+// C2-mixed (tools/layer_micro.py) it is bit-exact but slower than the
+// mma.sync shrink at these shapes (<= 64-token tiles, N = r <= 64): 92-99 vs
+// 84 us per layer launch.
+static bool use_tc();
+bool mbgmm_shrink_whole_rank() { return use_tc(); }
+static bool use_tc() {
+    static const bool on = [] {
+        const char* e = getenv("SLORA_MBGMM_TC");
+        return e && atoi(e) == 1;
+    }();
+    return on;
+}
+
 size_t mbgmm_smem(bool expand, int64_t K, int rmax) {
-    return expand ? mg_expand_smem_unit(rmax, mbgmm_expand_cols(rmax)) : mg_shrink_smem(K);
+    return expand ? mg_expand_smem_unit(rmax, mbgmm_expand_cols(rmax))
+                  : (use_tc() ? mg_shrink_tc_smem(K) : mg_shrink_smem(K));
 }
 
 cudaError_t configure_mbgmm_kernels() {
@@ -363,6 +582,11 @@ cudaError_t configure_mbgmm_kernels() {
     cudaError_t e;
     if ((e = cudaFuncSetAttribute(mbgmm_shrink_kernel<__half>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim))) return e;
     if ((e = cudaFuncSetAttribute(mbgmm_shrink_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim)))
+        return e;
+    if ((e = cudaFuncSetAttribute(mbgmm_shrink_tc_kernel<__half>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim)))
+        return e;
+    if ((e = cudaFuncSetAttribute(mbgmm_shrink_tc_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  lim)))
         return e;
     if ((e = cudaFuncSetAttribute(mbgmm_expand_kernel<__half>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim))) return e;
     if ((e = cudaFuncSetAttribute(mbgmm_expand_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim)))
@@ -376,6 +600,10 @@ cudaError_t configure_mbgmm_kernels() {
 cudaError_t launch_mbgmm(const MgParams& p, bool expand, int dtype, int n_units, size_t smem, cudaStream_t s,
                          bool pdl) {
     if (n_units == 0) return cudaSuccess;
+    if (!expand && use_tc())
+        return dtype == kF16 ? launch_kernel<__half>(mbgmm_shrink_tc_kernel<__half>, p, n_units, smem, s, pdl, kTcThreads)
+                             : launch_kernel<__nv_bfloat16>(mbgmm_shrink_tc_kernel<__nv_bfloat16>, p, n_units, smem, s,
+                                                            pdl, kTcThreads);
     if (dtype == kF16)
         return expand ? launch_kernel<__half>(mbgmm_expand_kernel<__half>, p, n_units, smem, s, pdl)
                       : launch_kernel<__half>(mbgmm_shrink_kernel<__half>, p, n_units, smem, s, pdl);

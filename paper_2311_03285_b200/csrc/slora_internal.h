@@ -173,7 +173,7 @@ struct MgUnit {
     int32_t nt;          // tokens in the tile (<= kMgTileTok)
     int32_t a, b;        // shrink: first A row, rows; expand: first column, columns
     float scale;
-    int32_t pad;
+    int32_t pad;         // tcgen05 shrink: k-split part
 };
 static_assert(sizeof(MgUnit) == 48, "MgUnit layout");
 struct alignas(64) MgParams {
@@ -186,8 +186,15 @@ struct alignas(64) MgParams {
     int64_t ldy[4];
     int32_t proj_ids[4];
     int32_t layer, K;
+    int32_t ksplit;      // shrink k-split parts (unit.pad = part); the expand sums them in order
+    int64_t vpart;       // floats between the parts' v regions
 };
+#ifndef SLORA_MG_KSPLIT
+#define SLORA_MG_KSPLIT 2
+#endif
+constexpr int kMgKsplit = SLORA_MG_KSPLIT;  // tcgen05 shrink: K parts per (tile, projection)
 size_t mbgmm_smem(bool expand, int64_t K, int rmax);
+bool mbgmm_shrink_whole_rank();  // tcgen05 shrink: one unit per (tile, projection) covering all r A rows
 cudaError_t configure_mbgmm_kernels();
 cudaError_t launch_mbgmm(const MgParams& p, bool expand, int dtype, int n_units, size_t smem, cudaStream_t s, bool pdl);
 
