@@ -126,6 +126,12 @@ class Workload:
         import torch
         from paper_2311_03285_b200 import Batch, Pool
         self.cfg, self.L, self.N, self.k = cfg, layers, tp, rank
+        # next-call L2 prefetch hints (slora_lora_prefetch_next), single GPU
+        # (SLORA_BENCH_L2PF: "o" = the q/k/v launch prefetches the o call, "qkv" = the o
+        # launch prefetches the next layer's q/k/v, "both", "0" = none)
+        pf = os.environ.get("SLORA_BENCH_L2PF", "0") if tp == 1 else "0"
+        self.pf_o, self.pf_qkv = pf in ("o", "both", "1"), pf in ("qkv", "both", "1")
+        self.l2pf = pf if (self.pf_o or self.pf_qkv) else None
         self.batch = wl.make_batch(cfg)
         b = self.batch
         self.T, self.H = b.T, cfg.hidden
@@ -139,18 +145,36 @@ class Workload:
                          max_adapters=max(256, len(b.ranks) + 8))
         rid = 0
         reqs = list(b.requests)
+        load_s, load_bytes = 0.0, 0
         for i, a in enumerate(b.unique):
             if rid < len(reqs):
                 self.pool.kv_alloc(rid, kv_tokens)
                 rid += 1
             host = wl.adapter_host_buffer(cfg, a, layers)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
             self.pool.adapter_load(a, b.ranks[a], host, stream=stream)
+            torch.cuda.synchronize()
+            load_s += time.perf_counter() - t0
+            load_bytes += host.nbytes
+        # a2: host -> pool adapter load (pageable numpy buffer -> library's pinned
+        # staging -> H2D -> page scatter), synchronous per adapter
+        self.load = {"adapters": len(b.unique), "bytes": int(load_bytes), "ms": round(1e3 * load_s, 3),
+                     "GBps": round(load_bytes / max(load_s, 1e-9) / 1e9, 2),
+                     "note": "full (unsharded) host tensors of all layers; this rank copies its 1/N shard"}
         while rid < len(reqs):
             self.pool.kv_alloc(rid, kv_tokens)
             rid += 1
         torch.cuda.synchronize()
         self.dbatch = Batch(self.pool)
         self.dbatch.prepare(b.token_adapter, stream=stream)
+        # a4: batch descriptor (grouping, work lists, LPT schedule, upload), host time per prepare
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(20):
+            self.dbatch.prepare(b.token_adapter, stream=stream)
+        self.prepare_us = round((time.perf_counter() - t0) / 20 * 1e6, 1)
+        torch.cuda.synchronize()
         td = {"f32": torch.float32, "f16": torch.float16, "bf16": torch.bfloat16}[cfg.dtype]
         self.td = td
         dev = f"cuda:{device}"
@@ -213,10 +237,14 @@ class Workload:
                 ys = [self.y[l, p] for p in range(4)]
                 e0 = torch.cuda.Event(enable_timing=True) if events is not None else None
                 if e0: e0.record(stream)
+                if self.pf_o:  # the q/k/v launch pulls the o call's pages into L2
+                    b.prefetch_next(l, "o")
                 b.apply(l, "qkv", self.x[l], H, ys, [H] * 4, stream=stream)
                 if e0:
                     e1 = torch.cuda.Event(enable_timing=True); e1.record(stream)
                     e2 = torch.cuda.Event(enable_timing=True); e2.record(stream)
+                if self.pf_qkv and l + 1 < self.L:  # the o launch pulls the next layer's q/k/v pages
+                    b.prefetch_next(l + 1, "qkv")
                 b.apply(l, "o", self.x[l], H, ys, [H] * 4, stream=stream)
                 if e0:
                     e3 = torch.cuda.Event(enable_timing=True); e3.record(stream)
@@ -347,9 +375,11 @@ def run_ours(args):
                             (layers * (W.bytes_qkv + W.bytes_o) / 1e9),
                       "step": "batch_prepare + layers x (qkv apply, o apply)",
                       "launch": "CUDA graph replay of the layer launches (PDL edges); prepare per step"
-                      if use_graph else "eager launches"},
+                      if use_graph else "eager launches",
+                      "l2_prefetch_next_call": W.l2pf},
            "gpu_launches": int(launches_per_step * args.steps if use_graph else launches),
-           "host_enqueue_ms_eager_step": round(host_ms, 3), "clocks": ck}
+           "host_enqueue_ms_eager_step": round(host_ms, 3), "clocks": ck,
+           "batch_prepare_host_us": W.prepare_us, "adapter_load": W.load}
     if roofline:
         out["roofline"] = roofline
     if ws == 1 and not args.no_e2e:

@@ -164,6 +164,11 @@ KernelCfg make_kernel_cfg(int mode, int64_t K, int64_t D, int64_t P, int es, int
     k.ns = ns;
     k.smem = lora_smem_bytes(mode, K, k.dchunk, ns, es);
     k.grid = lora_max_ctas(mode, dtype, k.smem);
+    static const int grid_cap = [] {  // experiment knob: fewer persistent CTAs than SMs
+        const char* e = getenv("SLORA_GRID");
+        return e ? atoi(e) : 0;
+    }();
+    if (grid_cap > 0) k.grid = std::min(k.grid, grid_cap);
     k.ok = k.grid > 0;
     return k;
 }
@@ -246,6 +251,10 @@ struct slora_batch {
     int32_t n_runs = 0;
     int64_t mg_units_max = 0;  // units of one 4-projection fused call (arena sizing)
     size_t off_tok = 0;
+    size_t off_pf = 0;         // PfSeg per segment (next-call L2 prefetch)
+    int32_t pf_rows = 0;       // sum over segments of 2*rank
+    int32_t pf_layer = 0;      // pending slora_lora_prefetch_next hint (consumed by the next apply)
+    uint32_t pf_mask = 0;
     // device arena (bump allocated per prepare) + its pinned staging mirror
     size_t arena_cap = 0, arena_used = 0;
     void* arena_host = nullptr;
@@ -1034,7 +1043,7 @@ extern "C" slora_status slora_batch_prepare(slora_batch_t b, const int64_t* tok_
     for (const DevSeg& s : b->segs) chunks += (s.n_tok + kItemTokCap - 1) / kItemTokCap;
     const int64_t max_items = 4 * chunks;
     const int64_t max_pieces_per_item = kMaxRank + 64;  // v8: one piece per stored A row
-    const size_t need = 256 + size_t(T) * 4 + 16 * (1024 + 4 * 1024 + size_t(b->mg_units_max) * sizeof(MgUnit) +
+    const size_t need = 256 + size_t(T) * 4 + b->segs.size() * sizeof(PfSeg) + 16 * (1024 + 4 * 1024 + size_t(b->mg_units_max) * sizeof(MgUnit) +
                                                    size_t(max_items) * sizeof(DevItem) +
                                                    size_t(max_items * max_pieces_per_item) * sizeof(DevTask8));
     cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -1054,6 +1063,17 @@ extern "C" slora_status slora_batch_prepare(slora_batch_t b, const int64_t* tok_
     b->arena_used = 0;
     cudaError_t e = cudaSuccess;
     b->off_tok = arena_put(b, b->tok_idx.data(), b->tok_idx.size() * sizeof(int32_t), s, e);
+    {
+        std::vector<PfSeg> pf(b->segs.size());
+        int32_t off = 0;
+        for (size_t si = 0; si < b->segs.size(); ++si) {
+            pf[si] = PfSeg{b->seg_tab[si], off, b->segs[si].rank};
+            off += 2 * b->segs[si].rank;
+        }
+        b->pf_rows = off;
+        b->pf_mask = 0;
+        if (!e && !pf.empty()) b->off_pf = arena_put(b, pf.data(), pf.size() * sizeof(PfSeg), s, e);
+    }
     if (e) return fail(SLORA_ERR_CUDA, "batch upload: %s", cudaGetErrorString(e));
     // per-launch sync slots and fused workspace, sized for this batch
     const int64_t sync_need = 2 + max_items + 32;
@@ -1294,12 +1314,35 @@ extern "C" slora_status slora_lora_apply(slora_pool_t p, slora_batch_t b, int32_
         q.ldy[pj] = ldy[pj];
     }
     q.v_blocks = 1;
+    if (b->pf_mask) {  // one-shot hint: the ring kernel prefetches the next call's pages into L2
+        if (!p->kcfg[kc].v8 && !b->segs.empty()) {
+            q.pf_segs = reinterpret_cast<const PfSeg*>(static_cast<uint8_t*>(b->arena_dev) + b->off_pf);
+            q.pf_nseg = int32_t(b->segs.size());
+            q.pf_rows = b->pf_rows;
+            q.pf_layer = b->pf_layer;
+            q.pf_mask = b->pf_mask;
+        }
+        b->pf_mask = 0;
+    }
     const slora_batch::Call& call = b->calls[kc][q.nproj];
     if (!call.mg_s.empty()) {
         st = launch_mbgmm_pair(p, b, call, q, x, ldx, stream);
         if (st) return st;
     }
     return launch(p, kc, q, stream);
+}
+
+extern "C" slora_status slora_lora_prefetch_next(slora_pool_t p, slora_batch_t b, int32_t layer, uint32_t mask) {
+    if (mask == 0) {
+        if (b) b->pf_mask = 0;
+        return b ? ok() : fail(SLORA_ERR_INVALID_ARG, "null batch");
+    }
+    slora_status st = common_checks(p, b, layer, mask);
+    if (st) return st;
+    if (p->N() != 1) return fail(SLORA_ERR_INVALID_ARG, "prefetch hints are single-GPU (slora_lora_apply)");
+    b->pf_layer = layer;
+    b->pf_mask = mask;
+    return ok();
 }
 
 extern "C" slora_status slora_lora_v_elems(slora_batch_t b, uint32_t mask, int32_t div, int64_t* out) {

@@ -80,10 +80,14 @@ constexpr int kStreamers = SLORA_STREAMERS;
 constexpr int kWarpStreamer0 = kConsumerWarps, kWarpResolver = kConsumerWarps + 1,
               kWarpStreamer1 = kConsumerWarps + 2, kWarpPrefetch = kConsumerWarps + 3,
               kWarpPublish = kConsumerWarps + 4, kWarpStreamerX = kConsumerWarps + 5;
-constexpr int kThreads = (kConsumerWarps + 3 + kStreamers) * 32;
+// last warp: L2 prefetcher of the next call's adapter pages (LoraParams.pf_*)
+constexpr int kWarpL2 = kConsumerWarps + 3 + kStreamers;
+constexpr int kThreads = (kWarpL2 + 1) * 32;
 // streamer index of a warp (-1: not a streamer)
 inline __host__ __device__ int streamer_id(int warp) {
-    return warp == kWarpStreamer0 ? 0 : warp == kWarpStreamer1 ? 1 : (warp >= kWarpStreamerX ? 2 + warp - kWarpStreamerX : -1);
+    return warp == kWarpStreamer0 ? 0
+           : warp == kWarpStreamer1 ? 1
+           : (warp >= kWarpStreamerX && warp < kWarpL2 ? 2 + warp - kWarpStreamerX : -1);
 }
 constexpr int kMaxChunks = 8;    // pages one stored A row spans (TP q/k/v: N)
 constexpr int kSlotBytes = 32 * 1024;  // ring slot
@@ -95,6 +99,15 @@ constexpr int kTraceSlots = 1024;  // debug trace: globaltimer events per traced
 enum Mode : int { kFused = 0, kShrink = 1, kExpand = 2 };
 enum DType : int { kF32 = 0, kF16 = 1, kBF16 = 2 };
 enum PieceKind : int { kPieceS = 0, kPieceE = 1, kPieceStop = 2 };
+
+// Next-call L2 prefetch (slora_lora_prefetch_next): one entry per segment of
+// the batch; off = prefix sum of 2*rank (A and B rows of one projection).
+struct PfSeg {
+    const int32_t* tab;  // the adapter's device page table
+    int32_t off;         // first row of this segment in the per-projection row list
+    int32_t rank;
+};
+static_assert(sizeof(PfSeg) == 16, "PfSeg layout");
 
 struct LoraParams {
     const void* pool;             // page buffer
@@ -124,6 +137,11 @@ struct LoraParams {
     const float* v_in;            // expand input
     int32_t v_blocks;
     int64_t NR;                   // sum over adapted tokens of rank
+    const PfSeg* pf_segs;         // L2 prefetch of call (pf_layer, pf_mask); pf_mask 0 = none
+    int32_t pf_nseg;
+    int32_t pf_rows;              // rows per projection = sum over segments of 2*rank
+    int32_t pf_layer;
+    uint32_t pf_mask;
 };
 
 // Per-launch kernel configuration (chosen on the host, see api.cpp).
