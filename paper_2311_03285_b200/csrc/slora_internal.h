@@ -63,7 +63,10 @@ struct DevTask8 {
 };
 static_assert(sizeof(DevTask8) == 64, "DevTask8 layout");
 
-constexpr int kItemTokCap = 4;   // tokens per item (larger segments are chunked)
+#ifndef SLORA_ITEM_TOK
+#define SLORA_ITEM_TOK 4
+#endif
+constexpr int kItemTokCap = SLORA_ITEM_TOK;  // tokens per item (larger segments are chunked)
 constexpr int kMaxRank = 64;     // max rank of the MBGMV path
 #ifndef SLORA_SHRINK_ROWS
 #define SLORA_SHRINK_ROWS 8

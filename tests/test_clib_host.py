@@ -123,6 +123,10 @@ def test_device_calls_refused_on_bookkeeping_pool():
     with pytest.raises(sl.SloraError) as e:
         b.apply(0, "qkv", 0, 8, [0, 0, 0, 0], [8] * 4)
     assert e.value.name == "NO_DEVICE"
+    with pytest.raises(sl.SloraError) as e:  # L2 prefetch hints need a device pool too
+        b.prefetch_next(0, "o")
+    assert e.value.name == "NO_DEVICE"
+    b.prefetch_next(0, 0)  # clearing a hint is always allowed
     with pytest.raises(sl.SloraError) as e:
         b.prepare(np.array([1, 5], np.int64))
     assert e.value.name == "NONRESIDENT_ADAPTER"
