@@ -18,6 +18,7 @@
 #include <cstring>
 #include <queue>
 #include <string>
+#include <thread>
 #include <unordered_map>
 #include <vector>
 
@@ -489,26 +490,71 @@ extern "C" slora_status slora_kv_pages(slora_pool_t p, int64_t rid, int32_t laye
 //   A (h x r, canonical) -> q/k/v: all h rows, columns [k*r/N, (k+1)*r/N)
 //                           o    : rows [k*P, (k+1)*P), all r columns
 //   B (r x d, canonical) -> all r rows, columns [k*P, (k+1)*P)
+// A host copy recorded by pack_shard and run at flush time by copy_segments.
+struct CopySeg {
+    uint8_t* dst;
+    const uint8_t* src;
+    size_t bytes;
+};
+
+// Run the staging copies of one flush on several host threads (a single
+// memcpy stream from pageable memory tops out near 10 GB/s, below the PCIe
+// link the staged bytes then cross).  Segments are split into ~4 MB pieces.
+static void copy_segments(std::vector<CopySeg>& segs) {
+    std::vector<CopySeg> work;
+    const size_t piece = size_t(4) << 20;
+    size_t total = 0;
+    for (const CopySeg& s : segs)
+        for (size_t o = 0; o < s.bytes; o += piece) {
+            work.push_back({s.dst + o, s.src + o, std::min(piece, s.bytes - o)});
+            total += work.back().bytes;
+        }
+    segs.clear();
+    static const int nthr = [] {
+        const char* e = getenv("SLORA_LOAD_THREADS");
+        const int hw = int(std::thread::hardware_concurrency());
+        return e ? std::max(1, atoi(e)) : std::max(1, std::min(8, hw));
+    }();
+    const int nt = int(std::min<size_t>(size_t(nthr), std::max<size_t>(1, total / (size_t(2) << 20))));
+    if (nt <= 1) {
+        for (const CopySeg& s : work) memcpy(s.dst, s.src, s.bytes);
+        return;
+    }
+    std::vector<std::thread> th;
+    for (int t = 1; t < nt; ++t)
+        th.emplace_back([&work, t, nt] {
+            for (size_t i = size_t(t); i < work.size(); i += size_t(nt)) memcpy(work[i].dst, work[i].src, work[i].bytes);
+        });
+    for (size_t i = 0; i < work.size(); i += size_t(nt)) memcpy(work[i].dst, work[i].src, work[i].bytes);
+    for (auto& x : th) x.join();
+}
+
 static void pack_shard(const slora_pool* p, const uint8_t* A, const uint8_t* B, int proj, int tensor, int r,
-                       uint8_t* dst, int& rows_out, int& cols_out) {
+                       uint8_t* dst, int& rows_out, int& cols_out, std::vector<CopySeg>& segs) {
     const int64_t H = p->cfg.hidden, P = p->P;
     const int N = p->N(), k = p->cfg.tp_rank, es = p->es;
     if (tensor == 0) {
         if (proj < 3) {
             const int rc = r / N;
+            if (N == 1)  // the whole dense A (H x r row-major) is the shard
+                segs.push_back({dst, A, size_t(H * r) * es});
+            else
             for (int64_t row = 0; row < H; ++row)
                 memcpy(dst + size_t(row * rc) * es, A + size_t(row * r + int64_t(k) * rc) * es, size_t(rc) * es);
             rows_out = int(H);
             cols_out = rc;
         } else {
-            memcpy(dst, A + size_t(int64_t(k) * P * r) * es, size_t(P * r) * es);
+            segs.push_back({dst, A + size_t(int64_t(k) * P * r) * es, size_t(P * r) * es});
             rows_out = int(P);
             cols_out = r;
         }
     } else {
-        for (int j = 0; j < r; ++j)
-            memcpy(dst + size_t(int64_t(j) * P) * es, B + size_t(int64_t(j) * H + int64_t(k) * P) * es,
-                   size_t(P) * es);
+        if (N == 1)  // rows of B are whole pages: one copy
+            segs.push_back({dst, B, size_t(int64_t(r) * H) * es});
+        else
+            for (int j = 0; j < r; ++j)
+                memcpy(dst + size_t(int64_t(j) * P) * es, B + size_t(int64_t(j) * H + int64_t(k) * P) * es,
+                       size_t(P) * es);
         rows_out = r;
         cols_out = int(P);
     }
@@ -568,8 +614,10 @@ extern "C" slora_status slora_adapter_load(slora_pool_t p, int64_t id, int32_t r
         int buf = 0;
         size_t used = kJobBytes;
         std::vector<ScatterJob> jobs;
+        std::vector<CopySeg> segs;
         auto flush = [&]() -> cudaError_t {
             if (jobs.empty()) return cudaSuccess;
+            copy_segments(segs);
             memcpy(p->stage_host[buf], jobs.data(), jobs.size() * sizeof(ScatterJob));
             cudaError_t e2 = cudaMemcpyAsync(p->stage_dev[buf], p->stage_host[buf], used, cudaMemcpyHostToDevice, s);
             if (!e2) e2 = launch_scatter(static_cast<uint8_t*>(p->stage_dev[buf]) + kJobBytes,
@@ -600,7 +648,8 @@ extern "C" slora_status slora_adapter_load(slora_pool_t p, int64_t id, int32_t r
                         if (e) break;
                     }
                     int rows, cols;
-                    pack_shard(p, A, B, pr, t, rank, static_cast<uint8_t*>(p->stage_host[buf]) + used, rows, cols);
+                    pack_shard(p, A, B, pr, t, rank, static_cast<uint8_t*>(p->stage_host[buf]) + used, rows, cols,
+                               segs);
                     ScatterJob jb;
                     jb.src_off = int64_t((used - kJobBytes) / size_t(es));
                     jb.pages = ad.dev_tab + page_cursor;
@@ -801,6 +850,14 @@ void build_call(slora_batch* b, const KernelCfg& k, int N, int nproj, uint32_t m
         const char* e = getenv("SLORA_HIRANK_SPLIT");
         return e ? atoi(e) : 0;
     }();
+    // Single-projection (o) calls: items of rank >= 32 get half-width expand
+    // pieces, whose rank-64 pieces are otherwise the launch's stragglers
+    // (measured on C2 decode: 1.249 -> 1.237 ms/step; SLORA_O_HIRANK=r to
+    // move the threshold, 0 = off)
+    static const int o_hirank = [] {
+        const char* e = getenv("SLORA_O_HIRANK");
+        return e ? atoi(e) : 32;
+    }();
     auto item_dchunk = [&](int rank) -> int64_t {
         if (k.v8) {  // ~ebytes of B per expand task, in whole warp passes (32 lanes x 16 B)
             const int64_t pass = 32 * 16 / es;
@@ -810,6 +867,8 @@ void build_call(slora_batch* b, const KernelCfg& k, int N, int nproj, uint32_t m
         }
         const int64_t half = k.dchunk / 2;
         if (hirank > 0 && rank >= hirank && half > 0 && k.D % half == 0 && (half * es) % 16 == 0) return half;
+        if (o_hirank > 0 && np == 1 && rank >= o_hirank && half > 0 && k.D % half == 0 && (half * es) % 16 == 0)
+            return half;
         return k.dchunk;
     };
     auto item_n_ep = [&](int rank) -> int64_t {

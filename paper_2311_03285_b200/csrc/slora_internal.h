@@ -64,9 +64,13 @@ struct DevTask8 {
 static_assert(sizeof(DevTask8) == 64, "DevTask8 layout");
 
 #ifndef SLORA_ITEM_TOK
-#define SLORA_ITEM_TOK 4
+#define SLORA_ITEM_TOK 2
 #endif
-constexpr int kItemTokCap = SLORA_ITEM_TOK;  // tokens per item (larger segments are chunked)
+// tokens per item (larger segments are chunked).  Measured on C2 decode
+// (profiles/knob_sweep_r01.txt): 4 -> 1.403, 3 -> 1.311, 2 -> 1.249,
+// 1 -> 1.346 ms/step; 2 halves the x buffers (ring depth 4 -> 5 slots) and
+// the Zipf-head items, whose expand pieces were the stragglers.
+constexpr int kItemTokCap = SLORA_ITEM_TOK;
 constexpr int kMaxRank = 64;     // max rank of the MBGMV path
 #ifndef SLORA_SHRINK_ROWS
 #define SLORA_SHRINK_ROWS 8
