@@ -29,6 +29,7 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 
 #include "slora_internal.h"
@@ -125,10 +126,15 @@ constexpr int kXTileBytes = kMgTileTok * 64 * 2;       // 64 tokens x 64 element
 
 __host__ __device__ inline size_t al(size_t x, size_t a) { return (x + a - 1) & ~(a - 1); }
 
-// shrink smem: [bars][A rows 16 x (K*2+16)][x ring 4 x 8 KB, 1 KB aligned]
-__host__ __device__ inline size_t mg_shrink_smem(int64_t K) {
-    return al(256 + size_t(kMgRows) * (K * 2 + 16), 1024) + size_t(kXStages) * kXTileBytes + 1024;
+// shrink smem: [bars][A rows R x (K*2+16)][x ring 8 x 8 KB, 1 KB aligned], R = 16 stored
+// A rows per unit, or 8 when 16 rows of K do not fit (K = 8192: 16 rows would be 256 KB)
+__host__ __device__ inline size_t mg_shrink_smem_rows(int64_t K, int rows) {
+    return al(256 + size_t(rows) * (K * 2 + 16), 1024) + size_t(kXStages) * kXTileBytes + 1024;
 }
+__host__ __device__ inline int mg_rows(int64_t K) {
+    return mg_shrink_smem_rows(K, kMgRows) <= size_t(227) * 1024 ? kMgRows : kMgRows / 2;
+}
+__host__ __device__ inline size_t mg_shrink_smem(int64_t K) { return mg_shrink_smem_rows(K, mg_rows(K)); }
 // expand smem: [bars][B slab r x (nc*2+16)][v hi, lo: 64 x (rp+8) 16-bit each]; the host
 // sizes slabs (mbgmm_expand_cols) so that two CTAs fit on an SM (one loads while one computes)
 __host__ __device__ inline size_t mg_expand_smem_unit(int r, int nc) {
@@ -149,7 +155,7 @@ __global__ void __launch_bounds__(kMgThreads, 1) mbgmm_shrink_kernel(const __gri
     uint64_t* xfull = abar + 1;
     uint64_t* xempty = xfull + kXStages;
     unsigned char* arows = sm + 256;
-    unsigned char* xring = sm + al(256 + size_t(kMgRows) * arow, 1024);
+    unsigned char* xring = sm + al(256 + size_t(mg_rows(K)) * arow, 1024);
     // the dynamic smem base is 1 KB aligned only up to the driver's guarantee: align the ring explicitly
     xring = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(xring) + 1023) & ~uintptr_t(1023));
     const int nrows = u.b;
@@ -291,8 +297,11 @@ __global__ void __launch_bounds__(kMgThreads, 2) mbgmm_expand_kernel(const __gri
     T* y = reinterpret_cast<T*>(p.y[p.proj_ids[u.pi]]);
     const int64_t ldy = p.ldy[p.proj_ids[u.pi]];
     const int t0 = warp * 16 + g, t1 = t0 + 8;
-    T* y0 = y + int64_t(u.row0 + t0) * ldy + u.a;
-    T* y1 = y + int64_t(u.row0 + t1) * ldy + u.a;
+    // gathered mode (segments of scattered tokens): x-map row i is token p.yrow[i]
+    const int64_t yr0 = t0 < u.nt ? (p.yrow ? p.yrow[u.row0 + t0] : u.row0 + t0) : 0;
+    const int64_t yr1 = t1 < u.nt ? (p.yrow ? p.yrow[u.row0 + t1] : u.row0 + t1) : 0;
+    T* y0 = y + yr0 * ldy + u.a;
+    T* y1 = y + yr1 * ldy + u.a;
     // y of this sub-chunk is loaded into registers before its MMAs (the loads fly
     // while the tensor cores work), then read-modify-written once
     for (int sc = 0; sc < nc; sc += 64) {
@@ -570,6 +579,27 @@ static bool use_tc() {
         return e && atoi(e) == 1;
     }();
     return on;
+}
+
+int mbgmm_rows(int64_t K) { return mg_rows(K); }
+
+// Gathered MBGMM input: out row i = x row idx[i] (K elements, 16-byte vectors).
+// Launched without PDL: it reads x, which the previous kernel may write.
+__global__ void gather_rows_kernel(const uint4* __restrict__ x, int64_t ldx16, const int32_t* __restrict__ idx, int n,
+                                   uint4* __restrict__ out, int64_t k16) {
+    for (int i = blockIdx.x; i < n; i += gridDim.x) {
+        const uint4* src = x + int64_t(__ldg(idx + i)) * ldx16;
+        uint4* dst = out + int64_t(i) * k16;
+        for (int64_t c = threadIdx.x; c < k16; c += blockDim.x) dst[c] = __ldcs(src + c);
+    }
+}
+cudaError_t launch_gather_rows(const void* x, int64_t ldx, const int32_t* idx, int n, void* out, int64_t K, int es,
+                               cudaStream_t s) {
+    if (n <= 0) return cudaSuccess;
+    count_launch();
+    gather_rows_kernel<<<std::min(n, 148 * 8), 256, 0, s>>>(static_cast<const uint4*>(x), ldx * es / 16, idx, n,
+                                                            static_cast<uint4*>(out), K * es / 16);
+    return cudaGetLastError();
 }
 
 size_t mbgmm_smem(bool expand, int64_t K, int rmax) {

@@ -213,12 +213,16 @@ struct alignas(64) MgParams {
     int32_t layer, K;
     int32_t ksplit;      // shrink k-split parts (unit.pad = part); the expand sums them in order
     int64_t vpart;       // floats between the parts' v regions
+    const int32_t* yrow; // gathered mode: y row of x-map row i (the batch's tok_idx); nullptr: row i
 };
 #ifndef SLORA_MG_KSPLIT
 #define SLORA_MG_KSPLIT 2
 #endif
 constexpr int kMgKsplit = SLORA_MG_KSPLIT;  // tcgen05 shrink: K parts per (tile, projection)
 size_t mbgmm_smem(bool expand, int64_t K, int rmax);
+int mbgmm_rows(int64_t K);       // stored A rows per mma.sync shrink unit (16, or 8 when 16 rows of K do not fit)
+cudaError_t launch_gather_rows(const void* x, int64_t ldx, const int32_t* idx, int n, void* out, int64_t K, int es,
+                               cudaStream_t s);
 bool mbgmm_shrink_whole_rank();  // tcgen05 shrink: one unit per (tile, projection) covering all r A rows
 cudaError_t configure_mbgmm_kernels();
 cudaError_t launch_mbgmm(const MgParams& p, bool expand, int dtype, int n_units, size_t smem, cudaStream_t s, bool pdl);
