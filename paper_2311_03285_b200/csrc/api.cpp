@@ -1101,11 +1101,18 @@ extern "C" slora_status slora_batch_prepare(slora_batch_t b, const int64_t* tok_
             const char* e = getenv("SLORA_MBGMM_GATHER_MIN");
             return e ? atoi(e) : 8;  // measured on C4: 32 -> 16.2, 16 -> 13.0, 8 -> 12.2 ms/step (off: 18.0)
         }();
+        // ... and only for rank >= 32: a rank-8 segment never pays for the gather
+        // and the two extra launches (measured on C1, all rank 8: 0.71 -> 2.45
+        // ms/step when its Zipf-head segments were gathered)
+        static const int rank_g = [] {
+            const char* e = getenv("SLORA_MBGMM_GATHER_RANK");
+            return e ? atoi(e) : 32;
+        }();
         b->mg_gather = false;
         if (ok_shape && b->n_runs == 0 && theta_g > 0)
             for (size_t si = 0; si < b->segs.size(); ++si) {
                 const DevSeg& sg = b->segs[si];
-                if (sg.n_tok < theta_g) continue;
+                if (sg.n_tok < theta_g || sg.rank < rank_g) continue;
                 b->runs[si].push_back({0, sg.n_tok});
                 ++b->n_runs;
                 b->mg_gather = true;
