@@ -1108,8 +1108,15 @@ extern "C" slora_status slora_batch_prepare(slora_batch_t b, const int64_t* tok_
             const char* e = getenv("SLORA_MBGMM_GATHER_RANK");
             return e ? atoi(e) : 32;
         }();
+        // ... and only when those segments hold at least half of the adapted
+        // tokens: the gather and the two MBGMM launches run before the call's
+        // MBGMV launch, so one large segment in a decode batch does not pay
+        // (measured on C3, one 18-token rank-64 segment of 64: 2.14 -> 4.07 ms)
+        int64_t gather_tok = 0;
+        for (const DevSeg& sg : b->segs)
+            if (sg.n_tok >= theta_g && sg.rank >= rank_g) gather_tok += sg.n_tok;
         b->mg_gather = false;
-        if (ok_shape && b->n_runs == 0 && theta_g > 0)
+        if (ok_shape && b->n_runs == 0 && theta_g > 0 && 2 * gather_tok >= b->adapted)
             for (size_t si = 0; si < b->segs.size(); ++si) {
                 const DevSeg& sg = b->segs[si];
                 if (sg.n_tok < theta_g || sg.rank < rank_g) continue;
