@@ -192,7 +192,13 @@ slora_status slora_batch_get_info(slora_batch_t batch, slora_batch_info* out);
  *     y_p[i, :] = round( y_p[i, :] + scale_a * (x[i, :] A_{a,layer,p}) B_{a,layer,p} )
  *   x: T x hidden, row stride ldx elements; y[p]: T x hidden, stride ldy[p];
  *   pool dtype; 16-byte aligned rows.  fp32 accumulation; one rounding.
- *   Only for tp_size == 1 (else INVALID_ARG). */
+ *   Only for tp_size == 1 (else INVALID_ARG).
+ *   Segments are served by MBGMV, or -- consecutive runs of >= 32 tokens of
+ *   one adapter, or (decode batches) segments of >= 8 scattered tokens of
+ *   rank >= 32 holding at least half of the adapted tokens -- by the MBGMM
+ *   tensor-core pair (reading R9); all intermediates (v, gathered
+ *   x rows) live in pool-owned workspaces sized by slora_batch_prepare and
+ *   are used in stream order. */
 slora_status slora_lora_apply(slora_pool_t pool, slora_batch_t batch, int32_t layer,
                               uint32_t proj_mask, const void* x, int64_t ldx,
                               void* const y[4], const int64_t ldy[4], void* stream);
