@@ -1099,7 +1099,7 @@ extern "C" slora_status slora_batch_prepare(slora_batch_t b, const int64_t* tok_
         // contiguous workspace per call and y is written through tok_idx.
         static const int theta_g = [] {
             const char* e = getenv("SLORA_MBGMM_GATHER_MIN");
-            return e ? atoi(e) : 8;  // measured on C4: 32 -> 16.2, 16 -> 13.0, 8 -> 12.2 ms/step (off: 18.0)
+            return e ? atoi(e) : 4;  // measured on C4: 32 -> 16.2, 16 -> 13.0, 8 -> 12.2, 4 -> 10.2 ms/step (off: 18.0)
         }();
         // ... and only for rank >= 32: a rank-8 segment never pays for the gather
         // and the two extra launches (measured on C1, all rank 8: 0.71 -> 2.45

@@ -1,6 +1,6 @@
 """GPU parity of gathered MBGMM: decode batches whose adapter segments hold
 many scattered tokens (reading R9: dispatch by segment token count, not by
-phase).  With no consecutive prefill runs, segments of >= 8 tokens and rank
+phase).  With no consecutive prefill runs, segments of >= 4 tokens and rank
 >= 32 (when they hold at least half of the adapted tokens) go to the
 tensor-core MBGMM kernels on x rows gathered into a contiguous workspace, y
 written back through the token index; the rest of the batch stays on MBGMV.
@@ -36,7 +36,7 @@ def test_gathered_mbgmm_exact_integer_bit_exact(dtype, ranks):
     cfg = decode_cfg(dtype, ranks)
     batch = wl.make_batch(cfg)
     case = Case(cfg, batch, order="shuffle", seed=9, weight_fn=int_weights(cfg), kv_interleave=2)
-    assert _segments(case) >= 1, "segments of >= 8 scattered tokens must go to MBGMM"
+    assert _segments(case) >= 1, "segments of >= 4 scattered tokens must go to MBGMM"
     rng = np.random.default_rng(4)
     x = wl.round_to(rng.integers(-1, 2, size=(batch.T, cfg.hidden)).astype(np.float32), dtype)
     ys = [wl.round_to(rng.integers(-64, 65, size=(batch.T, cfg.hidden)).astype(np.float32), dtype)
