@@ -194,7 +194,7 @@ slora_status slora_batch_get_info(slora_batch_t batch, slora_batch_info* out);
  *   pool dtype; 16-byte aligned rows.  fp32 accumulation; one rounding.
  *   Only for tp_size == 1 (else INVALID_ARG).
  *   Segments are served by MBGMV, or -- consecutive runs of >= 32 tokens of
- *   one adapter, or (decode batches) segments of >= 8 scattered tokens of
+ *   one adapter, or (decode batches) segments of >= 4 scattered tokens of
  *   rank >= 32 holding at least half of the adapted tokens -- by the MBGMM
  *   tensor-core pair (reading R9); all intermediates (v, gathered
  *   x rows) live in pool-owned workspaces sized by slora_batch_prepare and
