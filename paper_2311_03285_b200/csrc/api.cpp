@@ -210,6 +210,13 @@ struct slora_pool {
     float* ws_slot_base = nullptr;    // slot of the call being launched
     int64_t ws_region = 0;            // floats per workspace region: ring v, warp-task v, MBGMM v (kMgKsplit parts)
     uint64_t launch_seq = 0;
+    // MBGMV group kernel: partial-v workspace and per-item counters (zeroed
+    // once, self-resetting), shared by the calls of every batch of the pool
+    float* g_ws = nullptr;
+    int64_t g_ws_cap = 0;              // floats
+    int32_t* g_cnt = nullptr;
+    int64_t g_cnt_cap = 0;             // ints
+    int sms = 148;
 
     int64_t free_pages() const { return int64_t(free_stack.size()); }
     int N() const { return cfg.tp_size; }
@@ -248,6 +255,18 @@ struct slora_batch {
         std::vector<MgUnit> mg_s, mg_e; // MBGMM shrink / expand units (fused calls with long runs)
         size_t off_items = 0, off_pieces = 0, off_cta = 0, off_mg_s = 0, off_mg_e = 0;
     } calls[5][5];
+    // fused single-GPU MBGMV group-kernel plans (mbgmv.cu), per projection count
+    struct GroupPlan {
+        bool built = false, ok = false;
+        uint32_t mask = 0;
+        int C = 0, G = 0, grid = 0, ns = 0, Kc = 0, Dc = 0, SS = 0, cps = 0;
+        size_t smem = 0;
+        double pred_us = 0;
+        std::vector<GItem> items;       // grouped: group g owns [goff[g], goff[g+1])
+        std::vector<int32_t> goff;
+        int64_t ws_floats = 0;
+        size_t off_items = 0, off_goff = 0;
+    } gplans[5];
     // per segment: token ranges [begin, end) of the segment's token list that
     // are MBGMM runs (>= theta consecutive x rows; fused 16-bit calls only)
     std::vector<std::vector<std::pair<int32_t, int32_t>>> runs;
@@ -323,6 +342,8 @@ extern "C" slora_status slora_pool_create(const slora_pool_config* cfg, slora_po
         if ((e = configure_lora_kernels(cfg->device))) return cleanup(e, "configure kernels");
         if ((e = configure_mbgmm_kernels())) return cleanup(e, "configure MBGMM kernels");
         if ((e = configure_lora8_kernels())) return cleanup(e, "configure MBGMV kernels");
+        if ((e = configure_mbgmv_group())) return cleanup(e, "configure MBGMV group kernels");
+        if ((e = cudaDeviceGetAttribute(&p->sms, cudaDevAttrMultiProcessorCount, cfg->device))) return cleanup(e, "SM count");
         if ((e = cudaMalloc(&p->slot_tab_dev, sizeof(int32_t*) * size_t(cfg->max_adapters))))
             return cleanup(e, "cudaMalloc slot table");
         if ((e = cudaMemset(p->slot_tab_dev, 0, sizeof(int32_t*) * size_t(cfg->max_adapters))))
@@ -381,6 +402,8 @@ extern "C" slora_status slora_pool_destroy(slora_pool_t p) {
         if (p->sync_dev) cudaFree(p->sync_dev);
         if (p->ws_dev) cudaFree(p->ws_dev);
         if (p->xg_dev) cudaFree(p->xg_dev);
+        if (p->g_ws) cudaFree(p->g_ws);
+        if (p->g_cnt) cudaFree(p->g_cnt);
         if (p->trace_dev) cudaFree(p->trace_dev);
     }
     delete p;
@@ -988,10 +1011,180 @@ void build_call(slora_batch* b, const KernelCfg& k, int N, int nproj, uint32_t m
             call.tasks8.push_back(t);
         }
 }
+// --------------------------------------------- MBGMV group kernel plan
+// Streaming rate of the whole GPU (GB/s) for the group kernel's copy pattern:
+// 8-row slots of `rowbytes` bulk copies, `cps` persistent CTAs per SM, one
+// producer warp each, in the C2 decode launch sequence under a CUDA graph
+// with programmatic dependent launch (tools/stream_micro2.cu, measured on
+// this pool's B200: profiles/stream_micro_r02.txt).
+double group_stream_gbs(int cps, int64_t rowbytes) {  // two producer warps per CTA
+    if (cps >= 2) return rowbytes >= 4096 ? 6300 : rowbytes >= 2048 ? 6160 : rowbytes >= 1024 ? 5800 : 3810;
+    return rowbytes >= 4096 ? 6100 : rowbytes >= 2048 ? 5980 : rowbytes >= 1024 ? 4300 : 2320;
+}
+
+// Plan one fused call on the group kernel (mbgmv.cu): items = (segment,
+// projection, chunk of <= tok_cap tokens) outside the MBGMM runs; for each
+// (CTAs per SM, group size C) that the shapes allow, LPT-assign the items to
+// the G = grid / C groups on streamed bytes and predict the launch time from
+// the measured streaming rate; keep the fastest.  SLORA_GROUP_C /
+// SLORA_GROUP_CPS pin the choice (experiments).
+void plan_group_call(slora_batch* b, uint32_t mask, slora_batch::GroupPlan& gp) {
+    const slora_pool* p = b->pool;
+    gp = slora_batch::GroupPlan{};
+    gp.built = true;
+    gp.mask = mask;
+    if (p->N() != 1) return;
+    int proj_ids[4], np = 0;
+    for (int pj = 0; pj < 4; ++pj)
+        if (mask & (1u << pj)) proj_ids[np++] = pj;
+    (void)proj_ids;
+    const int64_t H = p->cfg.hidden;
+    const int es = p->es;
+    const int VE = 16 / es;
+    // token ranges of each segment outside its MBGMM runs
+    struct Unit { int si, pi, t0, nt; };
+    std::vector<Unit> units;
+    for (int si = 0; si < int(b->segs.size()); ++si) {
+        const DevSeg& sg = b->segs[size_t(si)];
+        int32_t cur = 0;
+        std::vector<std::pair<int32_t, int32_t>> ranges;
+        if (b->n_runs > 0)
+            for (const auto& rn : b->runs[size_t(si)]) {
+                if (rn.first > cur) ranges.push_back({cur, rn.first});
+                cur = rn.second;
+            }
+        if (cur < sg.n_tok) ranges.push_back({cur, sg.n_tok});
+        for (int pi = 0; pi < np; ++pi)
+            for (const auto& rg : ranges) units.push_back({si, pi, rg.first, rg.second - rg.first});
+    }
+    // SLORA_GROUP_C / _CPS pin every call; SLORA_GROUP_C_O / _CPS_O only single-projection (o) calls
+    auto knob = [](const char* a, const char* b, bool single) {
+        const char* e = single ? getenv(b) : nullptr;
+        if (!e) e = getenv(a);
+        return e ? atoi(e) : 0;
+    };
+    const int force_c = knob("SLORA_GROUP_C", "SLORA_GROUP_C_O", np == 1);
+    const int force_cps = knob("SLORA_GROUP_CPS", "SLORA_GROUP_CPS_O", np == 1);
+    static const int64_t item_ovh = [] {  // per-item fixed cost in streamed-byte units (exchange, barriers)
+        const char* e = getenv("SLORA_GROUP_ITEM_OVH");
+        return e ? int64_t(atoll(e)) : int64_t(8192);
+    }();
+    slora_batch::GroupPlan best;
+    for (int cps = 1; cps <= 2; ++cps) {
+        if (force_cps && cps != force_cps) continue;
+        for (int C : {1, 2, 4, 8, 16}) {
+            if (force_c && C != force_c) continue;
+            if (H % C) continue;
+            const int64_t Kc = H / C, Dc = H / C;
+            if ((Kc * es) % 16) continue;
+            if (es == 2 && Kc % 256) continue;  // 8 warps x whole pairs of 16-element k-steps
+            if (es == 2 && Kc > 2048) continue; // x fragments in registers (<= 16 k-steps per warp)
+            const int64_t nv = Dc / VE;
+            if (Dc % VE || (es == 4 && nv > kGConsumers * 32)) continue;  // fp32 expand: one vector per thread
+            const int64_t rowbytes = Kc * es;
+            if (rowbytes > 4096) continue;
+            const int SS = int(8 * (rowbytes + 16));
+            const int64_t budget = cps == 2 ? 113 * 1024 : 227 * 1024;  // two CTAs per SM: <= 113 KB each
+            const int ns = int(std::min<int64_t>(kGMaxSlots, (budget - kGFixedSmem) / SS));
+            if (ns < 3) continue;
+            const int grid = (cps * p->sms) / C * C;
+            const int G = grid / C;
+            if (G < 1) continue;
+            const int tok_cap = kGMaxTok;  // tensor-core expand: N = 8 tokens
+            // items and their streamed bytes per CTA
+            std::vector<GItem> its;
+            std::vector<int64_t> cost;
+            for (const Unit& u : units) {
+                const DevSeg& sg = b->segs[size_t(u.si)];
+                for (int t0 = u.t0; t0 < u.t0 + u.nt; t0 += tok_cap) {
+                    GItem it{};
+                    it.tab = b->seg_tab.empty() ? nullptr : b->seg_tab[size_t(u.si)];
+                    it.rank = sg.rank;
+                    it.nt = std::min(tok_cap, u.t0 + u.nt - t0);
+                    it.pi = u.pi;
+                    it.scale = sg.scale;
+                    for (int t = 0; t < it.nt; ++t) it.tok[t] = b->tok_idx[size_t(sg.tok_off + t0 + t)];
+                    its.push_back(it);
+                    cost.push_back(int64_t(2) * sg.rank * rowbytes + item_ovh);
+                }
+            }
+            std::vector<int32_t> order(its.size());
+            for (size_t i = 0; i < order.size(); ++i) order[i] = int32_t(i);
+            std::stable_sort(order.begin(), order.end(),
+                             [&](int32_t a, int32_t c2) { return cost[size_t(a)] > cost[size_t(c2)]; });
+            using HE = std::pair<int64_t, int32_t>;
+            std::priority_queue<HE, std::vector<HE>, std::greater<HE>> heap;
+            for (int g = 0; g < G; ++g) heap.push({0, g});
+            std::vector<std::vector<int32_t>> lists(static_cast<size_t>(G), std::vector<int32_t>{});
+            for (int32_t i : order) {
+                HE h = heap.top();
+                heap.pop();
+                lists[size_t(h.second)].push_back(i);
+                h.first += cost[size_t(i)];
+                heap.push(h);
+            }
+            int64_t makespan = 0;
+            bool fits = true;
+            while (!heap.empty()) {
+                makespan = std::max(makespan, heap.top().first);
+                heap.pop();
+            }
+            for (const auto& l : lists) fits = fits && int(l.size()) <= kGMaxItems;
+            if (!fits) continue;
+            const double rate = group_stream_gbs(cps, rowbytes) * 1e3 / (double(cps) * p->sms);  // bytes/us per CTA
+            const double us = double(makespan) / rate;
+            if (best.ok && us >= best.pred_us) continue;
+            slora_batch::GroupPlan cand;
+            cand.built = true;
+            cand.ok = true;
+            cand.mask = mask;
+            cand.C = C;
+            cand.G = G;
+            cand.grid = grid;
+            cand.ns = ns;
+            cand.Kc = int(Kc);
+            cand.Dc = int(Dc);
+            cand.SS = SS;
+            cand.cps = cps;
+            cand.smem = size_t(kGFixedSmem) + size_t(ns) * size_t(SS);
+            cand.pred_us = us;
+            cand.goff.assign(size_t(G) + 1, 0);
+            int64_t ws = 0;
+            for (int g = 0; g < G; ++g) {
+                cand.goff[size_t(g)] = int32_t(cand.items.size());
+                for (int32_t i : lists[size_t(g)]) {
+                    GItem it = its[size_t(i)];
+                    it.ws = int32_t(ws);
+                    ws += int64_t(C) * it.nt * it.rank;
+                    cand.items.push_back(it);
+                }
+            }
+            cand.goff[size_t(G)] = int32_t(cand.items.size());
+            cand.ws_floats = ws;
+            best = std::move(cand);
+        }
+    }
+    if (best.ok) gp = std::move(best);
+    if (const char* vb = getenv("SLORA_VERBOSE"); vb && atoi(vb) > 0 && gp.ok) {
+        int64_t mx = 0, tot = 0;
+        for (int g = 0; g < gp.G; ++g) {
+            int64_t l = 0;
+            for (int i = gp.goff[size_t(g)]; i < gp.goff[size_t(g) + 1]; ++i)
+                l += 2 * int64_t(gp.items[size_t(i)].rank) * gp.Kc * es;
+            mx = std::max(mx, l);
+            tot += l;
+        }
+        fprintf(stderr, "slora: group plan mask=0x%x C=%d G=%d cps=%d ns=%d smem=%zu items=%zu pred=%.2fus "
+                        "balance=%.3f\n", mask, gp.C, gp.G, gp.cps, gp.ns, gp.smem, gp.items.size(), gp.pred_us,
+                double(tot) / std::max<int64_t>(1, mx * gp.G));
+    }
+}
+
 }  // namespace
 
 namespace {
 slora_status ensure_call(slora_pool* p, slora_batch* b, int kc, uint32_t mask, void* stream);
+slora_status ensure_group(slora_pool* p, slora_batch* b, uint32_t mask, void* stream);
 
 // Which single-GPU fused kernel serves a call of np projections.  Measured on
 // C2 decode (tools/layer_micro.py, graphs of 32 layers): the ring pipeline
@@ -1130,6 +1323,7 @@ extern "C" slora_status slora_batch_prepare(slora_batch_t b, const int64_t* tok_
     }
     for (auto& row : b->calls)
         for (auto& c : row) c.built = false;
+    for (auto& g : b->gplans) g.built = false;
     b->epoch = p->epoch;
     b->prepared = true;
     if (!p->dev) {
@@ -1143,7 +1337,9 @@ extern "C" slora_status slora_batch_prepare(slora_batch_t b, const int64_t* tok_
     for (const DevSeg& s : b->segs) chunks += (s.n_tok + kItemTokCap - 1) / kItemTokCap;
     const int64_t max_items = 4 * chunks;
     const int64_t max_pieces_per_item = kMaxRank + 64;  // v8: one piece per stored A row
-    const size_t need = 256 + size_t(T) * 4 + b->segs.size() * sizeof(PfSeg) + 16 * (1024 + 4 * 1024 + size_t(b->mg_units_max) * sizeof(MgUnit) +
+    const int64_t gitems_max = 4 * (int64_t(b->segs.size()) + (b->adapted + 3) / 4 + b->n_runs + 1);
+    const size_t gneed = 5 * (size_t(gitems_max) * sizeof(GItem) + size_t(2 * p->sms + 2) * 4 + 1024);
+    const size_t need = gneed + 256 + size_t(T) * 4 + b->segs.size() * sizeof(PfSeg) + 16 * (1024 + 4 * 1024 + size_t(b->mg_units_max) * sizeof(MgUnit) +
                                                    size_t(max_items) * sizeof(DevItem) +
                                                    size_t(max_items * max_pieces_per_item) * sizeof(DevTask8));
     cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -1211,6 +1407,8 @@ extern "C" slora_status slora_batch_prepare(slora_batch_t b, const int64_t* tok_
         if (p->N() == 1) {
             if (!st2) st2 = ensure_call(p, b, fused_kc(p, 3), 0x7, stream);
             if (!st2) st2 = ensure_call(p, b, fused_kc(p, 1), 0x8, stream);
+            if (!st2) st2 = ensure_group(p, b, 0x7, stream);
+            if (!st2) st2 = ensure_group(p, b, 0x8, stream);
         } else {
             if (!st2 && p->kcfg[1].ok) st2 = ensure_call(p, b, 1, 0x7, stream);
             if (!st2 && p->kcfg[2].ok) st2 = ensure_call(p, b, 2, 0x8, stream);
@@ -1274,6 +1472,48 @@ slora_status ensure_call(slora_pool* p, slora_batch* b, int kc, uint32_t mask, v
     call.built = true;
     call.mask = mask;
     return SLORA_OK;
+}
+
+// Build + upload the group-kernel plan of a fused call (first use after a
+// prepare) and grow the pool's partial-v workspace / counters to fit it.
+slora_status ensure_group(slora_pool* p, slora_batch* b, uint32_t mask, void* stream) {
+    int np = 0;
+    for (int pj = 0; pj < 4; ++pj) np += (mask >> pj) & 1;
+    slora_batch::GroupPlan& gp = b->gplans[np];
+    if (gp.built && gp.mask == mask) return SLORA_OK;
+    plan_group_call(b, mask, gp);
+    if (!gp.ok || !p->dev) return SLORA_OK;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    cudaError_t e = cudaSuccess;
+    gp.off_items = arena_put(b, gp.items.data(), gp.items.size() * sizeof(GItem), s, e);
+    if (!e) gp.off_goff = arena_put(b, gp.goff.data(), gp.goff.size() * sizeof(int32_t), s, e);
+    if (e) return fail(SLORA_ERR_CUDA, "group plan upload: %s", cudaGetErrorString(e));
+    const int64_t ws_need = std::max<int64_t>(gp.ws_floats, 1);
+    if (ws_need > p->g_ws_cap) {
+        if (p->g_ws) CUDA_TRY(cudaFreeAsync(p->g_ws, s));
+        const int64_t cap = ws_need * 2;
+        CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&p->g_ws), sizeof(float) * size_t(cap), s));
+        p->g_ws_cap = cap;
+    }
+    const int64_t cnt_need = 2 * int64_t(gp.items.size()) + 2;
+    if (cnt_need > p->g_cnt_cap) {
+        if (p->g_cnt) CUDA_TRY(cudaFreeAsync(p->g_cnt, s));
+        const int64_t cap = cnt_need * 2;
+        CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&p->g_cnt), sizeof(int32_t) * size_t(cap), s));
+        CUDA_TRY(cudaMemsetAsync(p->g_cnt, 0, sizeof(int32_t) * size_t(cap), s));
+        p->g_cnt_cap = cap;
+    }
+    return SLORA_OK;
+}
+
+// Which fused MBGMV kernel serves single-GPU calls: the group kernel
+// (mbgmv.cu) with SLORA_MBGMV=group, else the round-1 ring pipeline (kernels.cu)
+bool use_group_kernel() {
+    static const bool on = [] {
+        const char* e = getenv("SLORA_MBGMV");
+        return e && std::string(e) == "group";
+    }();
+    return on;
 }
 
 // Resolve (building + uploading on first use) the call descriptor and fill the
@@ -1443,6 +1683,44 @@ extern "C" slora_status slora_lora_apply(slora_pool_t p, slora_batch_t b, int32_
     if (!call.mg_s.empty()) {
         st = launch_mbgmm_pair(p, b, call, q, x, ldx, stream);
         if (st) return st;
+    }
+    if (use_group_kernel()) {
+        st = ensure_group(p, b, mask, stream);
+        if (st) return st;
+        const slora_batch::GroupPlan& gp = b->gplans[np];
+        if (gp.ok) {
+            if (gp.items.empty()) return ok();
+            GroupParams g;
+            memset(&g, 0, sizeof(g));
+            uint8_t* base = static_cast<uint8_t*>(b->arena_dev);
+            g.pool = p->cfg.device_buffer;
+            g.P = p->P;
+            g.items = reinterpret_cast<const GItem*>(base + gp.off_items);
+            g.goff = reinterpret_cast<const int32_t*>(base + gp.off_goff);
+            g.ws = p->g_ws;
+            g.cnt = p->g_cnt;
+            g.C = gp.C;
+            g.Kc = gp.Kc;
+            g.Dc = gp.Dc;
+            g.ns = gp.ns;
+            g.SS = gp.SS;
+            g.layer = layer;
+            for (int pj = 0; pj < 4; ++pj) {
+                g.proj_ids[pj] = q.proj_ids[pj];
+                g.y[pj] = y[pj];
+                g.ldy[pj] = ldy[pj];
+            }
+            g.x = x;
+            g.ldx = ldx;
+            static const int gdbg = [] { const char* e = getenv("SLORA_GDBG"); return e ? atoi(e) : 0; }();
+            g.dbg = gdbg;
+            static const int tr_layer = [] { const char* e = getenv("SLORA_TRACE_LAYER"); return e ? atoi(e) : 16; }();
+            if (p->trace_dev && layer == tr_layer) g.trace = p->trace_dev + (np == 1 ? 8192 : 0);
+            const int dt = p->cfg.dtype == SLORA_F32 ? kF32 : (p->cfg.dtype == SLORA_F16 ? kF16 : kBF16);
+            CUDA_TRY(cudaSetDevice(p->cfg.device));
+            CUDA_TRY(launch_mbgmv_group(g, dt, gp.grid, gp.smem, static_cast<cudaStream_t>(stream)));
+            return ok();
+        }
     }
     return launch(p, kc, q, stream);
 }
