@@ -210,13 +210,9 @@ struct slora_pool {
     float* ws_slot_base = nullptr;    // slot of the call being launched
     int64_t ws_region = 0;            // floats per workspace region: ring v, warp-task v, MBGMM v (kMgKsplit parts)
     uint64_t launch_seq = 0;
-    // MBGMV group kernel: partial-v workspace and per-item counters (zeroed
-    // once, self-resetting), shared by the calls of every batch of the pool
-    float* g_ws = nullptr;
-    int64_t g_ws_cap = 0;              // floats
-    int32_t* g_cnt = nullptr;
-    int64_t g_cnt_cap = 0;             // ints
     int sms = 148;
+    int32_t* g_ctr = nullptr;          // MBGMV cluster kernel: claim counters, kGCtrSlots pairs (zeroed once)
+    uint64_t g_seq = 0;                // rotating counter slot of the next launch
 
     int64_t free_pages() const { return int64_t(free_stack.size()); }
     int N() const { return cfg.tp_size; }
@@ -262,10 +258,9 @@ struct slora_batch {
         int C = 0, G = 0, grid = 0, ns = 0, Kc = 0, Dc = 0, SS = 0, cps = 0;
         size_t smem = 0;
         double pred_us = 0;
-        std::vector<GItem> items;       // grouped: group g owns [goff[g], goff[g+1])
-        std::vector<int32_t> goff;
-        int64_t ws_floats = 0;
-        size_t off_items = 0, off_goff = 0;
+        int64_t makespan = 0;           // predicted bytes of the busiest CTA
+        std::vector<GItem> items;       // largest first (claim order)
+        size_t off_items = 0;
     } gplans[5];
     // per segment: token ranges [begin, end) of the segment's token list that
     // are MBGMM runs (>= theta consecutive x rows; fused 16-bit calls only)
@@ -344,6 +339,8 @@ extern "C" slora_status slora_pool_create(const slora_pool_config* cfg, slora_po
         if ((e = configure_lora8_kernels())) return cleanup(e, "configure MBGMV kernels");
         if ((e = configure_mbgmv_group())) return cleanup(e, "configure MBGMV group kernels");
         if ((e = cudaDeviceGetAttribute(&p->sms, cudaDevAttrMultiProcessorCount, cfg->device))) return cleanup(e, "SM count");
+        if ((e = cudaMalloc(&p->g_ctr, sizeof(int32_t) * 2 * kGCtrSlots))) return cleanup(e, "cudaMalloc counters");
+        if ((e = cudaMemset(p->g_ctr, 0, sizeof(int32_t) * 2 * kGCtrSlots))) return cleanup(e, "cudaMemset counters");
         if ((e = cudaMalloc(&p->slot_tab_dev, sizeof(int32_t*) * size_t(cfg->max_adapters))))
             return cleanup(e, "cudaMalloc slot table");
         if ((e = cudaMemset(p->slot_tab_dev, 0, sizeof(int32_t*) * size_t(cfg->max_adapters))))
@@ -402,8 +399,7 @@ extern "C" slora_status slora_pool_destroy(slora_pool_t p) {
         if (p->sync_dev) cudaFree(p->sync_dev);
         if (p->ws_dev) cudaFree(p->ws_dev);
         if (p->xg_dev) cudaFree(p->xg_dev);
-        if (p->g_ws) cudaFree(p->g_ws);
-        if (p->g_cnt) cudaFree(p->g_cnt);
+        if (p->g_ctr) cudaFree(p->g_ctr);
         if (p->trace_dev) cudaFree(p->trace_dev);
     }
     delete p;
@@ -1017,33 +1013,42 @@ void build_call(slora_batch* b, const KernelCfg& k, int N, int nproj, uint32_t m
 // producer warp each, in the C2 decode launch sequence under a CUDA graph
 // with programmatic dependent launch (tools/stream_micro2.cu, measured on
 // this pool's B200: profiles/stream_micro_r02.txt).
+int group_max_clusters(int dtype, int C, size_t smem) {
+    static std::unordered_map<uint64_t, int> cache;
+    const uint64_t key = (uint64_t(dtype) << 48) ^ (uint64_t(C) << 40) ^ uint64_t(smem);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+    int dev = 0;
+    const int n = cudaGetDevice(&dev) == cudaSuccess ? mbgmv_group_max_clusters(dtype, C, smem) : 0;
+    cache.emplace(key, n);
+    return n;
+}
+
 double group_stream_gbs(int cps, int64_t rowbytes) {  // two producer warps per CTA
     if (cps >= 2) return rowbytes >= 4096 ? 6300 : rowbytes >= 2048 ? 6160 : rowbytes >= 1024 ? 5800 : 3810;
     return rowbytes >= 4096 ? 6100 : rowbytes >= 2048 ? 5980 : rowbytes >= 1024 ? 4300 : 2320;
 }
 
-// Plan one fused call on the group kernel (mbgmv.cu): items = (segment,
-// projection, chunk of <= tok_cap tokens) outside the MBGMM runs; for each
-// (CTAs per SM, group size C) that the shapes allow, LPT-assign the items to
-// the G = grid / C groups on streamed bytes and predict the launch time from
-// the measured streaming rate; keep the fastest.  SLORA_GROUP_C /
-// SLORA_GROUP_CPS pin the choice (experiments).
+// Plan one fused call on the cluster kernel (mbgmv.cu): items = (segment,
+// projection, chunk of <= 8 tokens) outside the MBGMM runs, sorted largest
+// first (the order the clusters claim them in).  For each (CTAs per SM,
+// cluster size C) that the shapes allow, simulate the greedy claiming (= LPT)
+// over the G clusters the GPU holds at once and predict the launch time from
+// the measured streaming rate; keep the fastest.  SLORA_GROUP_C / _CPS (and
+// _C_O / _CPS_O for single-projection calls) pin the choice (experiments).
 void plan_group_call(slora_batch* b, uint32_t mask, slora_batch::GroupPlan& gp) {
     const slora_pool* p = b->pool;
     gp = slora_batch::GroupPlan{};
     gp.built = true;
     gp.mask = mask;
     if (p->N() != 1) return;
-    int proj_ids[4], np = 0;
-    for (int pj = 0; pj < 4; ++pj)
-        if (mask & (1u << pj)) proj_ids[np++] = pj;
-    (void)proj_ids;
+    int np = 0;
+    for (int pj = 0; pj < 4; ++pj) np += (mask >> pj) & 1;
     const int64_t H = p->cfg.hidden;
     const int es = p->es;
     const int VE = 16 / es;
-    // token ranges of each segment outside its MBGMM runs
-    struct Unit { int si, pi, t0, nt; };
-    std::vector<Unit> units;
+    // items: token ranges of each segment outside its MBGMM runs, chunks of <= kGMaxTok tokens
+    std::vector<GItem> its;
     for (int si = 0; si < int(b->segs.size()); ++si) {
         const DevSeg& sg = b->segs[size_t(si)];
         int32_t cur = 0;
@@ -1055,20 +1060,34 @@ void plan_group_call(slora_batch* b, uint32_t mask, slora_batch::GroupPlan& gp) 
             }
         if (cur < sg.n_tok) ranges.push_back({cur, sg.n_tok});
         for (int pi = 0; pi < np; ++pi)
-            for (const auto& rg : ranges) units.push_back({si, pi, rg.first, rg.second - rg.first});
+            for (const auto& rg : ranges)
+                for (int t0 = rg.first; t0 < rg.second; t0 += kGMaxTok) {
+                    GItem it{};
+                    it.tab = b->seg_tab.empty() ? nullptr : b->seg_tab[size_t(si)];
+                    it.rank = sg.rank;
+                    it.nt = std::min(kGMaxTok, rg.second - t0);
+                    it.pi = pi;
+                    it.scale = sg.scale;
+                    for (int t = 0; t < it.nt; ++t) it.tok[t] = b->tok_idx[size_t(sg.tok_off + t0 + t)];
+                    its.push_back(it);
+                }
     }
-    // SLORA_GROUP_C / _CPS pin every call; SLORA_GROUP_C_O / _CPS_O only single-projection (o) calls
-    auto knob = [](const char* a, const char* b, bool single) {
-        const char* e = single ? getenv(b) : nullptr;
+    // largest first (rank, then tokens); stable, so equal items keep batch order
+    std::stable_sort(its.begin(), its.end(), [](const GItem& a, const GItem& c2) {
+        return a.rank != c2.rank ? a.rank > c2.rank : a.nt > c2.nt;
+    });
+    auto knob = [](const char* a, const char* bk, bool single) {
+        const char* e = single ? getenv(bk) : nullptr;
         if (!e) e = getenv(a);
         return e ? atoi(e) : 0;
     };
     const int force_c = knob("SLORA_GROUP_C", "SLORA_GROUP_C_O", np == 1);
     const int force_cps = knob("SLORA_GROUP_CPS", "SLORA_GROUP_CPS_O", np == 1);
-    static const int64_t item_ovh = [] {  // per-item fixed cost in streamed-byte units (exchange, barriers)
+    static const int64_t item_ovh = [] {  // per-item fixed cost in streamed-byte units (x, y, exchange)
         const char* e = getenv("SLORA_GROUP_ITEM_OVH");
         return e ? int64_t(atoll(e)) : int64_t(8192);
     }();
+    const int dtc = es == 4 ? kF32 : (p->cfg.dtype == SLORA_F16 ? kF16 : kBF16);
     slora_batch::GroupPlan best;
     for (int cps = 1; cps <= 2; ++cps) {
         if (force_cps && cps != force_cps) continue;
@@ -1079,58 +1098,33 @@ void plan_group_call(slora_batch* b, uint32_t mask, slora_batch::GroupPlan& gp) 
             if ((Kc * es) % 16) continue;
             if (es == 2 && Kc % 256) continue;  // 8 warps x whole pairs of 16-element k-steps
             if (es == 2 && Kc > 2048) continue; // x fragments in registers (<= 16 k-steps per warp)
-            const int64_t nv = Dc / VE;
-            if (Dc % VE || (es == 4 && nv > kGConsumers * 32)) continue;  // fp32 expand: one vector per thread
+            if (Dc % VE || (es == 4 && Dc / VE > kGConsumers * 32)) continue;  // fp32 expand: a vector per thread
             const int64_t rowbytes = Kc * es;
             if (rowbytes > 4096) continue;
             const int SS = int(8 * (rowbytes + 16));
             const int64_t budget = cps == 2 ? 113 * 1024 : 227 * 1024;  // two CTAs per SM: <= 113 KB each
             const int ns = int(std::min<int64_t>(kGMaxSlots, (budget - kGFixedSmem) / SS));
-            if (ns < 3) continue;
-            const int grid = (cps * p->sms) / C * C;
-            const int G = grid / C;
+            if (ns < (es == 4 ? 10 : 4)) continue;  // fp32 shrink holds its X slot over <= 8 A slots
+            const size_t smem = size_t(kGFixedSmem) + size_t(ns) * size_t(SS);
+            // clusters the GPCs hold at once (C >= 4 does not tile every GPC: measured 33 clusters of 4
+            // at one CTA per SM, 71 at two)
+            const int G = std::min((cps * p->sms) / C, group_max_clusters(dtc, C, smem));
             if (G < 1) continue;
-            const int tok_cap = kGMaxTok;  // tensor-core expand: N = 8 tokens
-            // items and their streamed bytes per CTA
-            std::vector<GItem> its;
-            std::vector<int64_t> cost;
-            for (const Unit& u : units) {
-                const DevSeg& sg = b->segs[size_t(u.si)];
-                for (int t0 = u.t0; t0 < u.t0 + u.nt; t0 += tok_cap) {
-                    GItem it{};
-                    it.tab = b->seg_tab.empty() ? nullptr : b->seg_tab[size_t(u.si)];
-                    it.rank = sg.rank;
-                    it.nt = std::min(tok_cap, u.t0 + u.nt - t0);
-                    it.pi = u.pi;
-                    it.scale = sg.scale;
-                    for (int t = 0; t < it.nt; ++t) it.tok[t] = b->tok_idx[size_t(sg.tok_off + t0 + t)];
-                    its.push_back(it);
-                    cost.push_back(int64_t(2) * sg.rank * rowbytes + item_ovh);
-                }
-            }
-            std::vector<int32_t> order(its.size());
-            for (size_t i = 0; i < order.size(); ++i) order[i] = int32_t(i);
-            std::stable_sort(order.begin(), order.end(),
-                             [&](int32_t a, int32_t c2) { return cost[size_t(a)] > cost[size_t(c2)]; });
+            // greedy claiming of the sorted items = LPT; bytes streamed per CTA
             using HE = std::pair<int64_t, int32_t>;
             std::priority_queue<HE, std::vector<HE>, std::greater<HE>> heap;
             for (int g = 0; g < G; ++g) heap.push({0, g});
-            std::vector<std::vector<int32_t>> lists(static_cast<size_t>(G), std::vector<int32_t>{});
-            for (int32_t i : order) {
+            for (const GItem& it : its) {
                 HE h = heap.top();
                 heap.pop();
-                lists[size_t(h.second)].push_back(i);
-                h.first += cost[size_t(i)];
+                h.first += int64_t(2) * it.rank * rowbytes + item_ovh;
                 heap.push(h);
             }
             int64_t makespan = 0;
-            bool fits = true;
             while (!heap.empty()) {
                 makespan = std::max(makespan, heap.top().first);
                 heap.pop();
             }
-            for (const auto& l : lists) fits = fits && int(l.size()) <= kGMaxItems;
-            if (!fits) continue;
             const double rate = group_stream_gbs(cps, rowbytes) * 1e3 / (double(cps) * p->sms);  // bytes/us per CTA
             const double us = double(makespan) / rate;
             if (best.ok && us >= best.pred_us) continue;
@@ -1140,43 +1134,28 @@ void plan_group_call(slora_batch* b, uint32_t mask, slora_batch::GroupPlan& gp) 
             cand.mask = mask;
             cand.C = C;
             cand.G = G;
-            cand.grid = grid;
+            cand.grid = G * C;
             cand.ns = ns;
             cand.Kc = int(Kc);
             cand.Dc = int(Dc);
             cand.SS = SS;
             cand.cps = cps;
-            cand.smem = size_t(kGFixedSmem) + size_t(ns) * size_t(SS);
+            cand.smem = smem;
             cand.pred_us = us;
-            cand.goff.assign(size_t(G) + 1, 0);
-            int64_t ws = 0;
-            for (int g = 0; g < G; ++g) {
-                cand.goff[size_t(g)] = int32_t(cand.items.size());
-                for (int32_t i : lists[size_t(g)]) {
-                    GItem it = its[size_t(i)];
-                    it.ws = int32_t(ws);
-                    ws += int64_t(C) * it.nt * it.rank;
-                    cand.items.push_back(it);
-                }
-            }
-            cand.goff[size_t(G)] = int32_t(cand.items.size());
-            cand.ws_floats = ws;
+            cand.makespan = makespan;
             best = std::move(cand);
         }
     }
-    if (best.ok) gp = std::move(best);
+    if (best.ok) {
+        gp = std::move(best);
+        gp.items = std::move(its);
+    }
     if (const char* vb = getenv("SLORA_VERBOSE"); vb && atoi(vb) > 0 && gp.ok) {
-        int64_t mx = 0, tot = 0;
-        for (int g = 0; g < gp.G; ++g) {
-            int64_t l = 0;
-            for (int i = gp.goff[size_t(g)]; i < gp.goff[size_t(g) + 1]; ++i)
-                l += 2 * int64_t(gp.items[size_t(i)].rank) * gp.Kc * es;
-            mx = std::max(mx, l);
-            tot += l;
-        }
+        int64_t tot = 0;
+        for (const GItem& it : gp.items) tot += 2 * int64_t(it.rank) * gp.Kc * es;
         fprintf(stderr, "slora: group plan mask=0x%x C=%d G=%d cps=%d ns=%d smem=%zu items=%zu pred=%.2fus "
                         "balance=%.3f\n", mask, gp.C, gp.G, gp.cps, gp.ns, gp.smem, gp.items.size(), gp.pred_us,
-                double(tot) / std::max<int64_t>(1, mx * gp.G));
+                double(tot) / std::max<int64_t>(1, gp.makespan * gp.G));
     }
 }
 
@@ -1486,23 +1465,7 @@ slora_status ensure_group(slora_pool* p, slora_batch* b, uint32_t mask, void* st
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     cudaError_t e = cudaSuccess;
     gp.off_items = arena_put(b, gp.items.data(), gp.items.size() * sizeof(GItem), s, e);
-    if (!e) gp.off_goff = arena_put(b, gp.goff.data(), gp.goff.size() * sizeof(int32_t), s, e);
     if (e) return fail(SLORA_ERR_CUDA, "group plan upload: %s", cudaGetErrorString(e));
-    const int64_t ws_need = std::max<int64_t>(gp.ws_floats, 1);
-    if (ws_need > p->g_ws_cap) {
-        if (p->g_ws) CUDA_TRY(cudaFreeAsync(p->g_ws, s));
-        const int64_t cap = ws_need * 2;
-        CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&p->g_ws), sizeof(float) * size_t(cap), s));
-        p->g_ws_cap = cap;
-    }
-    const int64_t cnt_need = 2 * int64_t(gp.items.size()) + 2;
-    if (cnt_need > p->g_cnt_cap) {
-        if (p->g_cnt) CUDA_TRY(cudaFreeAsync(p->g_cnt, s));
-        const int64_t cap = cnt_need * 2;
-        CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&p->g_cnt), sizeof(int32_t) * size_t(cap), s));
-        CUDA_TRY(cudaMemsetAsync(p->g_cnt, 0, sizeof(int32_t) * size_t(cap), s));
-        p->g_cnt_cap = cap;
-    }
     return SLORA_OK;
 }
 
@@ -1696,9 +1659,8 @@ extern "C" slora_status slora_lora_apply(slora_pool_t p, slora_batch_t b, int32_
             g.pool = p->cfg.device_buffer;
             g.P = p->P;
             g.items = reinterpret_cast<const GItem*>(base + gp.off_items);
-            g.goff = reinterpret_cast<const int32_t*>(base + gp.off_goff);
-            g.ws = p->g_ws;
-            g.cnt = p->g_cnt;
+            g.n_items = int32_t(gp.items.size());
+            g.ctr = p->g_ctr + 2 * int64_t(p->g_seq++ % kGCtrSlots);
             g.C = gp.C;
             g.Kc = gp.Kc;
             g.Dc = gp.Dc;

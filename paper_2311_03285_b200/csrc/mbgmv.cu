@@ -4,43 +4,44 @@
 // Eq. lora_factored; reading R1: page j of A holds column j of A).
 //
 // Decomposition.  The host (api.cpp plan_group_call) cuts the batch into
-// items = (adapter segment, projection, chunk of <= 8 tokens) and assigns
-// them (LPT on streamed bytes) to G groups of C consecutive CTAs of one
-// persistent grid.  All C CTAs of a group walk the same item list; CTA c
+// items = (adapter segment, projection, chunk of <= 8 tokens), sorted largest
+// first.  A grid of thread-block clusters of C CTAs claims them dynamically:
+// the leader CTA of a cluster takes the next item from a per-launch atomic
+// counter and broadcasts its index into every CTA of the cluster (distributed
+// shared memory), so clusters that start late or run slow simply take fewer
+// items.  All C CTAs of a cluster process the same items; CTA c (cluster rank)
 //   shrink:   reads the K-slice c (Kc = K/C elements) of each of the item's r
-//             stored A rows and computes partial dot products with the same
-//             slice of the tokens' x rows (mma.sync m16n8k16: M = tokens,
-//             N = 8 A rows, K = 16, fp32 accumulate);
-//   exchange: writes its partial (nt x r fp32) to a small L2 workspace and
-//             releases the item's arrival counter; the exchange warp of every
-//             CTA of the group waits for the C arrivals and sums the C
-//             partials in a fixed order -> v (complete, fp32) in shared memory;
+//             stored A rows and forms partial dot products with the same slice
+//             of the tokens' x rows (mma.sync m16n8k16: M = tokens, N = 8 A
+//             rows, K = 16, fp32 accumulate) -> its partial v (nt x r fp32)
+//             in its own shared memory;
+//   exchange: the exchange warp of every CTA reads the C partials of the item
+//             through distributed shared memory (after each owner's remote
+//             release-arrive) and sums them in rank order -> v (complete);
 //   expand:   reads the output-column slice c (Dc = D/C) of the item's r B
 //             rows and writes y[tok][slice] = y + scale * sum_j v_j B_j
-//             (mma.sync m16n8k8: M = 16 output columns (B^T through
+//             (mma.sync m16n8k8: M = 16 output columns (B^T via
 //             ldmatrix.trans), N = tokens, K = 8 rank rows; v enters as a
-//             16-bit hi + lo pair, so the products keep ~fp32 accuracy; fp32
+//             16-bit hi + lo pair so the products keep ~fp32 accuracy; fp32
 //             accumulate, one rounding into y).
-// fp32 inputs never use tensor cores (no TF32, reading R5): the fp32 shrink
-// and expand are CUDA-core FFMA loops.
+// fp32 inputs never use tensor cores (no TF32, reading R5): their shrink and
+// expand are CUDA-core FFMA loops.
 //
-// Warp roles: 8 consumer warps (shrink, expand), a producer warp streaming A
-// and B row slices with cp.async.bulk (TMA engine, SASS UBLKCP) into a ring
-// of 8-row slots in the consumers' order, and an exchange warp.  The
-// consumers software-pipeline the items kGDepth deep (shrink i+2 before the
-// expand of i), so the exchange of item i overlaps two shrinks.  The weights
-// are never written by the previous kernel, so the producer streams them
-// before griddepcontrol.wait (programmatic dependent launch); x, y, the
-// workspace and the counters are only touched after it.
+// Data movement: two producer warps stream, in the consumers' order, 8-row
+// slots into a shared-memory ring with cp.async.bulk (TMA engine, SASS
+// UBLKCP): per item an X slot (the tokens' x row slices) then its A row
+// slices, and later its B row slices then a Y slot (the tokens' y row
+// slices).  The weights are never written by the previous kernel, so weight
+// slots are issued before griddepcontrol.wait (programmatic dependent launch);
+// X and Y slots of the ring's first lap are deferred until after it.  The
+// consumers touch global memory only to store y, and the exchange never leaves
+// the cluster: no load sits on the consumers' critical path.
 //
 // Determinism: every v entry is (each warp's mma chain over its k-range)
-// summed over the 8 warps in order, then over the C slices in order; every y
-// element is one fixed-order mma accumulation.  Results depend only on
-// (K, C, r), never on page placement, batch order or the group assignment.
-//
-// Deadlock freedom: a CTA only waits for the CTAs of its own group, which
-// process the same list in the same order; the grid never exceeds the number
-// of co-resident CTAs (host), so every group is resident as a whole.
+// summed over the 8 warps in order, then over the C slices in rank order;
+// every y element is one fixed-order mma accumulation.  Results depend only
+// on (K, C, r), never on page placement, batch order or which cluster claims
+// an item.  Clusters never wait for each other (only on the shared counter).
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
@@ -62,98 +63,242 @@ __device__ __forceinline__ long long gtimer() {
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
 }
-// diagnostics: event ev of this CTA (CTAs 0-15; events < 256: 0-63 phases, 64-159 consumer slot
-// k ready, 160-255 producer slot k issued)
+// diagnostics: event ev of this CTA (CTAs 0-15; events < 256: 0-63 phases, 64-127 consumer got
+// slot k, 128-191 consumer starts waiting for slot k, 192-255 producer issued weight slot k)
 #define GTRACE(ev)                                                                                 \
     do {                                                                                           \
         if (p.trace && blockIdx.x < 16 && (ev) < 256) p.trace[blockIdx.x * 256 + (ev)] = gtimer(); \
     } while (0)
 // diagnostics: per-CTA summary [CTA < 512][4]: 0 start, 1 consumers past griddepcontrol.wait,
-// 2 first slot ready, 3 consumers done
-#define GTRACE_ALL(ev)                                                                          \
-    do {                                                                                        \
-        if (p.trace && blockIdx.x < 512) p.trace[16 * 256 + blockIdx.x * 4 + (ev)] = gtimer(); \
+// 2 items processed, 3 consumers done
+#define GTRACE_ALL(ev, val)                                                                  \
+    do {                                                                                     \
+        if (p.trace && blockIdx.x < 512) p.trace[16 * 256 + blockIdx.x * 4 + (ev)] = (val); \
     } while (0)
 
-constexpr int kIdRing = 8;  // page-id ring entries (items)
+constexpr int kIdRing = 4;  // page-id ring entries (items)
+constexpr int kNP = 3;      // partial-v buffers (item m uses m % 3)
+constexpr int kVB = kGMaxTok * 64;  // floats of one v / partial buffer
+constexpr int kQD = kGQueue;        // claimed-item ring (item m uses m % kQD)
 
 struct GSmem {
-    uint64_t* full;   // [kGMaxSlots] slot filled (producer expect_tx + TMA bytes)
-    uint64_t* empty;  // [kGMaxSlots] slot released (one arrival per consumer warp)
-    uint64_t* dbar;   // item descriptors staged
-    uint64_t* vfull;  // [2] v of item i ready (exchange warp)
-    uint64_t* vempty; // [2] v of item i consumed (consumer warps)
-    uint64_t* idfull; // [kIdRing] page ids of item m landed (cp.async, 32 lanes)
-    uint64_t* idempty;// [kIdRing] page ids of item m read by both producer warps
-    GItem* desc;      // [kGMaxItems]
-    int32_t* ids;     // [kIdRing][128] page ids of items m % kIdRing: A rows then B rows
-    float* red;       // [2][8 warps][8 tokens][8 rows] per-slot shrink partials
-    float* vbuf;      // [2][nt][r] v of items i % 2 (complete)
+    uint64_t* full;    // [kGMaxSlots] slot filled (producer expect_tx + TMA bytes)
+    uint64_t* empty;   // [kGMaxSlots] slot released (one arrival per consumer warp)
+    uint64_t* vfull;   // [2] v of item i ready (exchange warp)
+    uint64_t* vempty;  // [2] v of item i consumed (consumer warps)
+    uint64_t* idfull;  // [kIdRing] page ids of item m landed (cp.async, 32 lanes)
+    uint64_t* idempty; // [kIdRing] page ids of item m read by every producer warp
+    uint64_t* pready;  // [kNP] partials of item m ready in all C CTAs (C remote arrivals)
+    uint64_t* pfree;   // [kNP] this CTA's partial of item m read by all C CTAs (C remote arrivals)
+    uint64_t* qfull;   // [kQD] claimed index of item m written by the leader (remote arrive)
+    uint64_t* qempty;  // [kQD] (leader CTA) index of item m read by all C CTAs (C remote arrivals)
+    uint64_t* dfull;   // [kQD] descriptor of item m staged (bulk copy, or a stop marker)
+    uint64_t* dempty;  // [kQD] descriptor of item m no longer needed (consumer warps)
+    int32_t* iq;       // [kQD] claimed global item index of item m (-1: no more items)
+    int32_t* deferq;   // [kGProducers][16] deferred activation slots: stream position
+    int32_t* deferi;   // [kGProducers][16] deferred activation slots: item * 2 + (0 = X, 1 = Y)
+    uint32_t zero16;   // shared address of 16 zero bytes (ldmatrix rows of absent tokens)
+    GItem* desc;       // [kQD]
+    int32_t* ids;      // [kIdRing][128] page ids of items m % kIdRing: A rows then B rows
+    float* red;        // [2][8 warps][8 tokens][8 rows] per-slot shrink partials
+    float* vbuf;       // [2][nt][r] v of items i % 2 (complete)
+    float* part;       // [kNP][nt][r] this CTA's partial v of items m % kNP
     unsigned char* ring;
 };
 __device__ __forceinline__ GSmem carve(unsigned char* s) {
     GSmem L;
     L.full = reinterpret_cast<uint64_t*>(s);
     L.empty = L.full + kGMaxSlots;
-    L.dbar = L.empty + kGMaxSlots;
-    L.vfull = L.dbar + 1;
+    L.vfull = L.empty + kGMaxSlots;
     L.vempty = L.vfull + 2;
     L.idfull = L.vempty + 2;
     L.idempty = L.idfull + kIdRing;
-    L.desc = reinterpret_cast<GItem*>(s + 512);
-    L.ids = reinterpret_cast<int32_t*>(s + 512 + kGMaxItems * 64);
-    L.red = reinterpret_cast<float*>(s + 512 + kGMaxItems * 64 + kIdRing * 128 * 4);
+    L.pready = L.idempty + kIdRing;
+    L.pfree = L.pready + kNP;
+    L.qfull = L.pfree + kNP;
+    L.qempty = L.qfull + kQD;
+    L.dfull = L.qempty + kQD;
+    L.dempty = L.dfull + kQD;   // barriers end at 8 * (16+16+2+2+4+4+3+3+4*8) = 656 bytes
+    L.zero16 = smem_u32(s + 704);  // 64 zero bytes at 704
+    L.iq = reinterpret_cast<int32_t*>(s + 768);
+    L.deferq = reinterpret_cast<int32_t*>(s + 832);
+    L.deferi = L.deferq + kGProducers * 16;  // ends at 832 + 256 = 1088
+    L.desc = reinterpret_cast<GItem*>(s + 1152);
+    L.ids = reinterpret_cast<int32_t*>(s + 1152 + kQD * 64);
+    L.red = reinterpret_cast<float*>(s + 1152 + kQD * 64 + kIdRing * 128 * 4);
     L.vbuf = L.red + 2 * 8 * 64;
+    L.part = L.vbuf + 2 * kVB;
     L.ring = s + kGFixedSmem;
     return L;
 }
+static_assert(kGFixedSmem == 1152 + kQD * 64 + kIdRing * 128 * 4 + 2 * 8 * 64 * 4 + 2 * kVB * 4 + kNP * kVB * 4,
+              "shared-memory layout");
 
-struct RingPos {
-    int slot = 0;
-    uint32_t lap = 0;
-    __device__ __forceinline__ void advance(int ns) {
-        if (++slot == ns) {
-            slot = 0;
-            ++lap;
-        }
-    }
-};
+// The slot stream, in the consumers' order: S(0), S(1), then for i = 0, 1, ...:
+// S(i+2), E(i), where S(m) = [X(m), A(m) rows in slots of 8] and E(i) =
+// [B(i) rows in slots of 8, Y(i)].  nslot(r) = ceil(r / 8).
+__device__ __forceinline__ int nslot(int r) { return (r + 7) >> 3; }
+
+// Item m of this cluster (its descriptor in desc[m % kQD]) once staged; nullptr
+// after the last one.  Every role of every CTA sees the same sequence.
+__device__ __forceinline__ const GItem* item_at(const GSmem& S, int m) {
+    mbar_wait(&S.dfull[m % kQD], (m / kQD) & 1);
+    const GItem* it = &S.desc[m % kQD];
+    return it->rank > 0 ? it : nullptr;
+}
 
 // ------------------------------------------------------------ producers
-// Stream, per item m of the group, its A row slices (shrink) and B row slices
-// (expand) in the consumers' order A0, A1, A2, B0, A3, B1, ..., B(n-1); each
-// 8-row slot is one mbarrier transaction of up to 8 bulk copies issued by
-// lanes 0-7.  kGProducers warps walk the same sequence and issue alternate
-// slots (a warp's bulk copies are issued one lane at a time, ~60 ns each:
-// one warp alone caps a CTA near 20-40 GB/s).  Producer 0 fetches the page
-// ids five items ahead into an 8-entry ring with cp.async (completion tracked
-// by idfull); both producers release an entry (idempty) after its B rows.
+// kGProducers warps walk the stream and issue alternate slots (a warp issues
+// its bulk copies one lane at a time, ~60 ns each: one warp alone caps a CTA
+// near 20-40 GB/s).  Producer 0 also
+//   - (leader CTA only) claims the cluster's items from the launch counter and
+//     broadcasts each claimed index into every CTA of the cluster;
+//   - stages each item's descriptor (bulk copy) and fetches its page ids three
+//     items ahead into a 4-entry ring with cp.async (idfull); every producer
+//     releases an id entry (idempty) after the item's B rows.
 template <typename T>
-__device__ __forceinline__ void producer(const GroupParams& p, const GSmem& S, int c, int n, int pw, int lane) {
+__device__ __forceinline__ void producer(const GroupParams& p, const GSmem& S, int c, int pw, int lane) {
     constexpr int ES = sizeof(T);
     const T* pool = reinterpret_cast<const T*>(p.pool);
     const int64_t P = p.P;
-    auto fetch = [&](int m) {
-        if (pw != 0 || m >= n) return;
+    const int ns = p.ns;
+    const int C = p.C;
+    const uint32_t SS = uint32_t(p.SS);
+    const bool copy = !(p.dbg & 32);
+    const bool leader = c == 0;
+    int last = 1 << 30;    // index of the first absent item (known to producer 0 once resolved)
+    bool claiming = true;  // leader: claims left to make
+    // leader: claim item m (or learn that none is left) and broadcast the index to the cluster
+    auto broadcast = [&](int m, int j) {
+        const int e = m % kQD;
+        if (m >= kQD) mbar_wait_cluster(&S.qempty[e], ((m / kQD) - 1) & 1);
+        if (lane < C) {
+            st_dsmem(mapa(smem_u32(&S.iq[e]), uint32_t(lane)), j);
+            mbar_arrive_remote(mapa(smem_u32(&S.qfull[e]), uint32_t(lane)));
+        }
+        __syncwarp();
+    };
+    auto claim_done = [&]() {  // the cluster made its last claim; the last cluster resets the counter
+        if (lane == 0 && atomicAdd(p.ctr + 1, 1) == int(gridDim.x) / C - 1) {
+            p.ctr[0] = 0;
+            p.ctr[1] = 0;
+        }
+        __syncwarp();
+    };
+    auto claim = [&](int m) {
+        if (pw != 0 || !leader || !claiming) return;
+        int j = 0;
+        if (lane == 0) j = atomicAdd(p.ctr, 1);
+        j = __shfl_sync(0xffffffffu, j, 0);
+        if (j >= p.n_items) {
+            j = -1;
+            claiming = false;
+        }
+        broadcast(m, j);
+#ifdef SLORA_HANG_DEBUG
+        if (lane == 0 && gridDim.x / C <= 32) printf("CLAIM block %d m %d j %d ctr %p\n", blockIdx.x, m, j, p.ctr);
+#endif
+        if (!claiming) claim_done();
+    };
+    // producer 0: item m's index -> its descriptor, or the stop marker (at and beyond the first
+    // absent item, so that every role's lookahead finds one)
+    auto resolve = [&](int m) {
+        if (pw != 0) return;
+        const int e = m % kQD;
+        int j = -1;
+        if (m <= last) {  // the leader broadcast an index (or -1) for item m
+            mbar_wait_cluster(&S.qfull[e], (m / kQD) & 1);
+            j = S.iq[e];
+            __syncwarp();
+            if (lane == 0) mbar_arrive_remote(mapa(smem_u32(&S.qempty[e]), 0u));
+#ifdef SLORA_HANG_DEBUG
+            if (lane == 0 && gridDim.x / C <= 32) printf("RESOLVE block %d m %d j %d\n", blockIdx.x, m, j);
+#endif
+        }
+        if (m >= kQD) mbar_wait(&S.dempty[e], ((m / kQD) - 1) & 1);
+        if (j >= 0) {
+            if (lane == 0) {
+                mbar_arrive_expect_tx(&S.dfull[e], sizeof(GItem));
+                bulk_g2s(&S.desc[e], p.items + j, sizeof(GItem), &S.dfull[e]);
+            }
+        } else {
+            last = min(last, m);
+            if (lane == 0) {
+                S.desc[e].rank = 0;
+                mbar_arrive(&S.dfull[e]);
+            }
+        }
+        __syncwarp();
+    };
+    auto fetch = [&](int m) {  // page ids of item m (producer 0)
+        if (pw != 0 || m >= last) return;
+        const GItem* it = item_at(S, m);
+        if (!it) return;
         const int e = m % kIdRing;
         if (m >= kIdRing) mbar_wait(&S.idempty[e], ((m / kIdRing) - 1) & 1);
-        const GItem& it = S.desc[m];
-        const int r = it.rank;
-        const int proj = p.proj_ids[it.pi];
-        const int32_t* src = it.tab + int64_t((p.layer * 4 + proj) * 2) * r;  // A ids, then B ids
+        const int r = it->rank;
+        const int proj = p.proj_ids[it->pi];
+        const int32_t* src = it->tab + int64_t((p.layer * 4 + proj) * 2) * r;  // A ids, then B ids
         int32_t* dst = S.ids + e * 128;
         for (int j = lane; j < 2 * r; j += 32) cp_async4(dst + j, src + j);
         cp_async_mbar_arrive(&S.idfull[e]);
     };
-    RingPos rp;
-    int k = 0;  // position in the slot stream
-    const int ns = p.ns;
-    const uint32_t SS = uint32_t(p.SS);
-    const bool copy = !(p.dbg & 32);
-    auto emit = [&](int m, int kind) {
+    int k = 0;             // stream position
+    bool waited = false;   // griddepcontrol.wait done (activation slots may be issued)
+    int ndef = 0;          // deferred activation slots of the first lap
+    int32_t* dq = S.deferq + pw * 16;
+    int32_t* di = S.deferi + pw * 16;
+    // X (kind 0) or Y (kind 1) slot of item m into stream position kk (its slot is free)
+    auto issue_act = [&](int kk, int m, int kind) {
+        const GItem& it = S.desc[m % kQD];
+        const int slot = kk % ns;
+        const int eK = kind ? p.Dc : p.Kc;
+        const uint32_t rb = uint32_t(eK) * ES;
+        const uint32_t rs = rb + 16;
+        if (lane == 0) mbar_arrive_expect_tx(&S.full[slot], uint32_t(it.nt) * rb);
+        __syncwarp();
+        if (lane < it.nt) {
+            const T* src;
+            if (kind == 0) {
+                src = reinterpret_cast<const T*>(p.x) + int64_t(it.tok[lane]) * p.ldx + int64_t(c) * p.Kc;
+            } else {
+                const int proj = p.proj_ids[it.pi];
+                src = reinterpret_cast<const T*>(p.y[proj]) + int64_t(it.tok[lane]) * p.ldy[proj] +
+                      int64_t(c) * p.Dc;
+            }
+            bulk_g2s(S.ring + slot * SS + uint32_t(lane) * rs, src, rb, &S.full[slot]);
+        }
+    };
+    auto flush = [&]() {  // griddepcontrol.wait, then the deferred activation slots
+        pdl_wait();
+        waited = true;
+        for (int q = 0; q < ndef; ++q) issue_act(dq[q], di[q] >> 1, di[q] & 1);
+        ndef = 0;
+    };
+    auto act = [&](int m, int kind) {  // one activation slot at position k
+        if (k % kGProducers == pw) {
+            if (waited) {
+                mbar_wait(&S.empty[k % ns], ((k / ns) & 1) ^ 1);
+                issue_act(k, m, kind);
+            } else if (k < ns) {
+                if (lane == 0) {
+                    dq[ndef] = k;
+                    di[ndef] = m * 2 + kind;
+                }
+                __syncwarp();
+                ++ndef;
+            } else {
+                flush();
+                mbar_wait(&S.empty[k % ns], ((k / ns) & 1) ^ 1);
+                issue_act(k, m, kind);
+            }
+        }
+        ++k;
+    };
+    auto rows = [&](int m, int kind) {  // the item's A (kind 0) or B (kind 1) rows, 8 per slot
         const int e = m % kIdRing;
         mbar_wait(&S.idfull[e], (m / kIdRing) & 1);
-        const GItem& it = S.desc[m];
+        const GItem& it = S.desc[m % kQD];
         const int r = it.rank;
         const int32_t* id = S.ids + e * 128 + (kind ? r : 0);
         const int eK = kind ? p.Dc : p.Kc;
@@ -161,64 +306,80 @@ __device__ __forceinline__ void producer(const GroupParams& p, const GSmem& S, i
         const uint32_t rs = rb + 16;
         const int64_t coff = int64_t(c) * eK;
         for (int j0 = 0; j0 < r; j0 += 8, ++k) {
-            if (k % kGProducers == pw) {
-                const int nr = min(8, r - j0);
-                mbar_wait(&S.empty[rp.slot], (rp.lap & 1) ^ 1);
-                const int pg = lane < nr ? id[j0 + lane] : 0;
-                if (lane == 0) {
-                    if (copy)
-                        mbar_arrive_expect_tx(&S.full[rp.slot], uint32_t(nr) * rb);
-                    else
-                        mbar_arrive(&S.full[rp.slot]);
-                }
-                __syncwarp();
-                if (lane < nr && copy)
-                    bulk_g2s(S.ring + rp.slot * SS + uint32_t(lane) * rs, pool + int64_t(pg) * P + coff, rb,
-                             &S.full[rp.slot]);
-                if (lane == 0 && p.trace && k < 96) GTRACE(160 + k);
+            if (k % kGProducers != pw) continue;
+            if (k >= ns && !waited) flush();  // the ring wraps: the consumers need the deferred slots first
+            const int slot = k % ns;
+            const int nr = min(8, r - j0);
+            mbar_wait(&S.empty[slot], ((k / ns) & 1) ^ 1);
+            const int pg = lane < nr ? id[j0 + lane] : 0;
+            if (lane == 0) {
+                if (copy)
+                    mbar_arrive_expect_tx(&S.full[slot], uint32_t(nr) * rb);
+                else
+                    mbar_arrive(&S.full[slot]);
             }
-            rp.advance(ns);
+            __syncwarp();
+            if (lane < nr && copy)
+                bulk_g2s(S.ring + slot * SS + uint32_t(lane) * rs, pool + int64_t(pg) * P + coff, rb,
+                         &S.full[slot]);
+            if (lane == 0 && p.trace && k < 64) GTRACE(192 + k);
         }
         if (kind) {  // the item's ids are no longer needed by this warp
             __syncwarp();
             if (lane == 0) mbar_arrive(&S.idempty[e]);
         }
     };
-    for (int m = 0; m < 5; ++m) fetch(m);
-    if (lane == 0 && pw == 0) GTRACE(2);
-    emit(0, 0);
-    if (lane == 0 && pw == 0) GTRACE(3);
-    if (n > 1) emit(1, 0);
-    for (int i = 0; i < n; ++i) {
-        if (i + 2 < n) emit(i + 2, 0);
-        emit(i, 1);
-        fetch(i + 5);  // entry (i+5) % 8 == (i-3) % 8: released by both producers after emit(i-3, B)
+    // prologue: claims and descriptors of items 0..2, their page ids
+    for (int m = 0; m < 3; ++m) {
+        claim(m);
+        resolve(m);
     }
+    for (int m = 0; m < 3; ++m) fetch(m);
+    if (lane == 0 && pw == 0) GTRACE(2);
+    for (int m = 0; m < kGDepth; ++m)
+        if (item_at(S, m)) {
+            act(m, 0);
+            rows(m, 0);
+        }
+    if (lane == 0 && pw == 0) GTRACE(3);
+    for (int i = 0; item_at(S, i); ++i) {
+        if (pw == 0) {  // one more item in flight: claim + stage item i+3
+            claim(i + 3);
+            resolve(i + 3);
+        }
+        if (item_at(S, i + kGDepth)) {
+            act(i + kGDepth, 0);
+            rows(i + kGDepth, 0);
+        }
+        rows(i, 1);
+        act(i, 1);
+        fetch(i + 3);  // id entry (i+3) % 4 == (i-1) % 4: released by every producer after rows(i-1, B)
+    }
+    if (!waited) flush();
     if (lane == 0 && pw == 0) GTRACE(4);
 }
 
 // ------------------------------------------------------------ exchange warp
-// v of item i = sum over the group's C partials in slice order, into vbuf[i%2]
-// once all C CTAs have released item i; the group's last reader of item i
-// resets its two counters (self-resetting: no memset between launches).
-__device__ __forceinline__ void exchange(const GroupParams& p, const GSmem& S, int i0, int n, int lane) {
-    for (int i = 0; i < n; ++i) {
+// v of item i = sum over the cluster's C partials in rank order (distributed
+// shared memory), into vbuf[i % 2]; then every owner learns (remote arrive on
+// its pfree) that its partial buffer may be rewritten.
+__device__ __forceinline__ void exchange(const GroupParams& p, const GSmem& S, int lane) {
+    const int C = p.C;
+    for (int i = 0;; ++i) {
+        const GItem* itp = item_at(S, i);
+        if (!itp) break;
+        const int b = i % kNP;
         if (i >= 2) mbar_wait(&S.vempty[i & 1], ((i >> 1) - 1) & 1);
-        const GItem& it = S.desc[i];
-        const int tot = it.nt * it.rank;
-        int* cnt = p.cnt + 2 * (i0 + i);
-        float* vb = S.vbuf + (i & 1) * (kGMaxTok * 64);
+        mbar_wait_cluster(&S.pready[b], (i / kNP) & 1);
+        const int tot = itp->nt * itp->rank;
+        float* vb = S.vbuf + (i & 1) * kVB;
+        const uint32_t local = smem_u32(S.part + b * kVB);
         if (!(p.dbg & 1)) {
-            if (lane == 0)
-                while (ld_acquire(cnt) < p.C) __nanosleep(20);
-            __syncwarp();
-            const float* ws = p.ws + it.ws;
             if ((tot & 3) == 0) {
                 for (int e4 = lane; e4 < (tot >> 2); e4 += 32) {
                     float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll 4
-                    for (int q = 0; q < p.C; ++q) {
-                        const float4 v = ld_cg4(ws + int64_t(q) * tot + 4 * e4);
+                    for (int q = 0; q < C; ++q) {
+                        const float4 v = ld_dsmem4(mapa(local, uint32_t(q)) + 16u * uint32_t(e4));
                         s.x += v.x;
                         s.y += v.y;
                         s.z += v.z;
@@ -229,16 +390,13 @@ __device__ __forceinline__ void exchange(const GroupParams& p, const GSmem& S, i
             } else {
                 for (int e = lane; e < tot; e += 32) {
                     float s = 0.f;
-                    for (int q = 0; q < p.C; ++q) s += ld_cg(ws + int64_t(q) * tot + e);
+                    for (int q = 0; q < C; ++q) s += ld_dsmem(mapa(local, uint32_t(q)) + 4u * uint32_t(e));
                     vb[e] = s;
                 }
             }
-            __syncwarp();
-            if (lane == 0 && atomicAdd(cnt + 1, 1) == p.C - 1) {
-                cnt[0] = 0;
-                cnt[1] = 0;
-            }
         }
+        __syncwarp();
+        if (lane < C) mbar_arrive_remote(mapa(smem_u32(&S.pfree[b]), uint32_t(lane)));
         if (lane == 0) mbar_arrive(&S.vfull[i & 1]);
     }
 }
@@ -276,95 +434,56 @@ __device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t&
                  : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
                  : "r"(addr));
 }
-template <typename T> __device__ __forceinline__ float to_f(T v);
-template <> __device__ __forceinline__ float to_f<__half>(__half v) { return __half2float(v); }
-template <> __device__ __forceinline__ float to_f<__nv_bfloat16>(__nv_bfloat16 v) { return __bfloat162float(v); }
-template <typename T> __device__ __forceinline__ T from_f(float v);
-template <> __device__ __forceinline__ __half from_f<__half>(float v) { return __float2half_rn(v); }
-template <> __device__ __forceinline__ __nv_bfloat16 from_f<__nv_bfloat16>(float v) { return __float2bfloat16_rn(v); }
 
 template <typename T, int KSMAX>
 struct Consumer {
     static constexpr int ES = sizeof(T);
     static constexpr bool kF32 = sizeof(T) == 4;
     using V = Vec16<T>;
-    static constexpr int VE = V::VE;
 
     const GroupParams& p;
     const GSmem& S;
-    const int c, i0, n, tid, warp, lane;
-    RingPos rp;
+    const int c, tid, warp, lane;
+    int k = 0;  // stream position
 
-    __device__ Consumer(const GroupParams& p_, const GSmem& S_, int c_, int i0_, int n_)
-        : p(p_), S(S_), c(c_), i0(i0_), n(n_), tid(threadIdx.x), warp(threadIdx.x >> 5), lane(threadIdx.x & 31) {}
+    __device__ Consumer(const GroupParams& p_, const GSmem& S_, int c_)
+        : p(p_), S(S_), c(c_), tid(threadIdx.x), warp(threadIdx.x >> 5), lane(threadIdx.x & 31) {}
 
-    __device__ __forceinline__ const T* xrow(const GItem& it, int t) const {
-        return reinterpret_cast<const T*>(p.x) + int64_t(it.tok[t]) * p.ldx + int64_t(c) * p.Kc;
-    }
     __device__ __forceinline__ T* yrow(const GItem& it, int t) const {
         const int proj = p.proj_ids[it.pi];
         return reinterpret_cast<T*>(p.y[proj]) + int64_t(it.tok[t]) * p.ldy[proj] + int64_t(c) * p.Dc;
     }
+    __device__ __forceinline__ unsigned char* slot_ptr() const { return S.ring + (k % p.ns) * uint32_t(p.SS); }
+    __device__ __forceinline__ uint32_t slot_u32() const {
+        return smem_u32(S.ring) + uint32_t(k % p.ns) * uint32_t(p.SS);
+    }
     __device__ __forceinline__ void wait_slot() {
-        mbar_wait(&S.full[rp.slot], rp.lap & 1);
-        if (tid == 0 && p.trace) {
-            const int k = int(rp.lap) * p.ns + rp.slot;
-            if (k < 96) GTRACE(64 + k);
-        }
+        if (tid == 0 && p.trace && k < 64) GTRACE(128 + k);
+        mbar_wait(&S.full[k % p.ns], (k / p.ns) & 1);
+        if (tid == 0 && p.trace && k < 64) GTRACE(64 + k);
     }
     __device__ __forceinline__ void release_slot() {
         __syncwarp();
-        if (lane == 0) mbar_arrive(&S.empty[rp.slot]);
-        rp.advance(p.ns);
+        if (lane == 0) mbar_arrive(&S.empty[k % p.ns]);
+        ++k;
     }
 
-    // x fragments of item m for this warp's k-range [warp*KW, (warp+1)*KW): token g = lane/4
-    __device__ __forceinline__ void load_x(int m, uint32_t (&xa)[KSMAX][2]) const {
-        if constexpr (!kF32) {
-            const int KW = p.Kc >> 3, KS = KW >> 4;
-            const int g = lane >> 2, t4 = lane & 3;
-            const T* xr = nullptr;
-            if (m < n) {
-                const GItem& it = S.desc[m];
-                if (g < it.nt && !(p.dbg & 2)) xr = xrow(it, g) + warp * KW + 2 * t4;
-            }
-#pragma unroll
-            for (int ks = 0; ks < KSMAX; ++ks) {
-                xa[ks][0] = (ks < KS && xr) ? ld_u32(xr + 16 * ks) : 0u;
-                xa[ks][1] = (ks < KS && xr) ? ld_u32(xr + 16 * ks + 8) : 0u;
-            }
-        }
-    }
-    // y of item m for the expand epilogue: thread (g, t4) owns token 2*t4 + (g & 1) and the column
-    // pairs warp*CW + 16j + (g & ~1) + {0, 8} (+0, +1) of each m-block j (4-byte accesses)
-    __device__ __forceinline__ T* ypair(const GItem& it) const {
-        const int g = lane >> 2, t4 = lane & 3;
-        const int tok = 2 * t4 + (g & 1);
-        return tok < it.nt ? yrow(it, tok) + warp * (p.Dc >> 3) + (g & ~1) : nullptr;
-    }
-    __device__ __forceinline__ void load_y(int m, uint32_t (&yv)[KSMAX][2]) const {
-        if constexpr (!kF32) {
-            const GItem& it = S.desc[m];
-            const int MB = p.Dc >> 7;
-            const T* yp = (p.dbg & 4) ? nullptr : ypair(it);
-#pragma unroll
-            for (int j = 0; j < KSMAX; ++j) {
-                yv[j][0] = (j < MB && yp) ? ld_u32(yp + 16 * j) : 0u;
-                yv[j][1] = (j < MB && yp) ? ld_u32(yp + 16 * j + 8) : 0u;
-            }
-        }
-    }
-
-    // -- shrink of item m: this CTA's partial v over its K-slice -> workspace, then release.
-    // xa holds item m's x fragments on entry and item m+1's on return.
-    __device__ __forceinline__ void shrink(int m, uint32_t (&xa)[KSMAX][2]) {
-        const GItem& it = S.desc[m];
+    // -- shrink of item m: X slot, then the A slots; this CTA's partial v -> part[m % 3],
+    // then a release-arrive on the pready of every CTA of the cluster
+    __device__ __forceinline__ void shrink(int m, const GItem& it) {
         const int r = it.rank, nt = it.nt;
-        const int nsl = (r + 7) >> 3;
-        float* part = p.ws + it.ws + int64_t(c) * nt * r;
-        const uint32_t rs = uint32_t(p.Kc) * ES + 16;
+        const int nsl = nslot(r);
+        const int b = m % kNP;
+        float* part = S.part + b * kVB;
+        // part[b] was last read (by the cluster) for item m - 3
+        if (m >= kNP) mbar_wait_cluster(&S.pfree[b], ((m / kNP) - 1) & 1);
+        const uint32_t rsx = uint32_t(p.Kc) * ES + 16;
         if constexpr (kF32) {
-            // warp w: row w of each slot, lanes over 16-byte vectors, fixed-order butterfly
+            // the X slot stays until the A rows are done (fp32 x rows are read from it directly)
+            wait_slot();
+            const unsigned char* xs = slot_ptr();
+            const int kx = k;
+            ++k;
             const int nv = p.Kc >> 2;
             for (int s = 0; s < nsl; ++s) {
                 wait_slot();
@@ -373,14 +492,13 @@ struct Consumer {
 #pragma unroll
                 for (int t = 0; t < kGMaxTok; ++t) acc[t] = 0.f;
                 if (warp < nr) {
-                    const float4* arow =
-                        reinterpret_cast<const float4*>(S.ring + rp.slot * uint32_t(p.SS) + uint32_t(warp) * rs);
+                    const float4* arow = reinterpret_cast<const float4*>(slot_ptr() + uint32_t(warp) * rsx);
                     for (int v = lane; v < nv; v += 32) {
                         const float4 a = arow[v];
 #pragma unroll
                         for (int t = 0; t < kGMaxTok; ++t)
                             if (t < nt) {
-                                const float4 xv = reinterpret_cast<const float4*>(xrow(it, t))[v];
+                                const float4 xv = reinterpret_cast<const float4*>(xs + t * rsx)[v];
                                 acc[t] = fmaf(a.x, xv.x, acc[t]);
                                 acc[t] = fmaf(a.y, xv.y, acc[t]);
                                 acc[t] = fmaf(a.z, xv.z, acc[t]);
@@ -399,27 +517,32 @@ struct Consumer {
                     }
                 }
             }
+            __syncwarp();  // release the X slot (position kx)
+            if (lane == 0) mbar_arrive(&S.empty[kx % p.ns]);
         } else {
             const int KW = p.Kc >> 3, KS = KW >> 4;
             const int g = lane >> 2, t4 = lane & 3;
-            uint32_t xc[KSMAX][2];  // this item's fragments; xa is refilled with the next item's now
-#pragma unroll
-            for (int ks = 0; ks < KSMAX; ++ks) {
-                xc[ks][0] = xa[ks][0];
-                xc[ks][1] = xa[ks][1];
-            }
-            load_x(m + 1, xa);
-            // ldmatrix: lanes 8*mi .. 8*mi+7 address row rr of matrix mi = k offset 8*mi (two k-steps per x4)
             const int mi = lane >> 3, rr = lane & 7;
-            const uint32_t rowoff = uint32_t(rr) * rs + uint32_t(warp * KW + mi * 8) * ES;
-            const uint32_t ring = smem_u32(S.ring);
+            // x fragments of this warp's k-range from the X slot: ldmatrix.x4 covers two k-steps
+            // (matrix mi = k offset 8*mi; lanes of absent tokens read 16 zero bytes)
+            uint32_t xa[KSMAX][2];
+            wait_slot();
+            {
+                const bool real = rr < nt;
+                const uint32_t xb = real ? slot_u32() + uint32_t(rr) * rsx + uint32_t(warp * KW + mi * 8) * ES
+                                         : S.zero16;
+                const uint32_t xadv = real ? 32u * ES : 0u;
+#pragma unroll
+                for (int kp = 0; kp < KSMAX / 2; ++kp)
+                    if (2 * kp < KS)
+                        ldsm_x4(xb + uint32_t(kp) * xadv, xa[2 * kp][0], xa[2 * kp][1], xa[2 * kp + 1][0],
+                                xa[2 * kp + 1][1]);
+            }
+            release_slot();
+            const uint32_t rowoff = uint32_t(rr) * rsx + uint32_t(warp * KW + mi * 8) * ES;
             for (int s = 0; s < nsl; ++s) {
                 wait_slot();
-                if (m == 0 && s == 0 && tid == 0) {
-                    GTRACE(10);
-                    GTRACE_ALL(2);
-                }
-                const uint32_t base = ring + uint32_t(rp.slot) * uint32_t(p.SS) + rowoff;
+                const uint32_t base = slot_u32() + rowoff;
                 float d0[4] = {0.f, 0.f, 0.f, 0.f}, d1[4] = {0.f, 0.f, 0.f, 0.f};
                 if (!(p.dbg & 8)) {
 #pragma unroll
@@ -427,12 +550,11 @@ struct Consumer {
                         if (2 * kp < KS) {
                             uint32_t b0, b1, b2, b3;
                             ldsm_x4(base + uint32_t(kp) * 32u * ES, b0, b1, b2, b3);
-                            Mma<T>::run(d0, xc[2 * kp][0], xc[2 * kp][1], b0, b1);
-                            Mma<T>::run(d1, xc[2 * kp + 1][0], xc[2 * kp + 1][1], b2, b3);
+                            Mma<T>::run(d0, xa[2 * kp][0], xa[2 * kp][1], b0, b1);
+                            Mma<T>::run(d1, xa[2 * kp + 1][0], xa[2 * kp + 1][1], b2, b3);
                         }
                 }
                 release_slot();
-                if (p.dbg & 8) continue;
                 // d[0], d[1]: token g, rows 2*t4, 2*t4+1 of the slot (rows >= r: discarded below)
                 float* rb = S.red + (s & 1) * 512 + warp * 64 + g * 8 + 2 * t4;
                 rb[0] = d0[0] + d1[0];
@@ -450,24 +572,21 @@ struct Consumer {
                 }
             }
         }
-        bar_sync(1, kGConsumers * 32);  // every partial of the item is written
-        if (tid == 0) {
-            __threadfence();
-            red_release_add(p.cnt + 2 * (i0 + m), 1);
-        }
+        bar_sync(1, kGConsumers * 32);  // every partial of the item is in part[b]
+        if (tid < p.C) mbar_arrive_remote(mapa(smem_u32(&S.pready[b]), uint32_t(tid)));
     }
 
-    // -- expand of item m over this CTA's column slice (v of the item in vbuf[m % 2]);
-    // yv: the item's y pairs (load_y)
-    __device__ __forceinline__ void expand(int m, const uint32_t (&yv)[KSMAX][2]) {
-        const GItem& it = S.desc[m];
+    // -- expand of item m over this CTA's column slice: the B slots, then the Y slot
+    // (v of the item in vbuf[m % 2])
+    __device__ __forceinline__ void expand(int m, const GItem& it) {
         const int r = it.rank, nt = it.nt;
-        const float* vb = S.vbuf + (m & 1) * (kGMaxTok * 64);
+        const float* vb = S.vbuf + (m & 1) * kVB;
         const uint32_t rs = uint32_t(p.Dc) * ES + 16;
-        const int nsl = (r + 7) >> 3;
+        const int nsl = nslot(r);
         const float scale = it.scale;
         if constexpr (kF32) {
             // thread = (16-byte column vector, token group), FFMA over the rank rows
+            constexpr int VE = V::VE;
             const int nv = p.Dc / VE;
             const int tpv = max(1, (kGConsumers * 32) / nv);
             const bool active = tid < nv * tpv;
@@ -475,43 +594,44 @@ struct Consumer {
             constexpr int TT = kGMaxTok;
             float acc[TT][VE];
 #pragma unroll
-            for (int k = 0; k < TT; ++k)
+            for (int q = 0; q < TT; ++q)
 #pragma unroll
-                for (int e = 0; e < VE; ++e) acc[k][e] = 0.f;
+                for (int e = 0; e < VE; ++e) acc[q][e] = 0.f;
             for (int s = 0; s < nsl; ++s) {
                 wait_slot();
                 const int nr = min(8, r - 8 * s);
                 if (active && !(p.dbg & 16)) {
-                    const unsigned char* sb = S.ring + rp.slot * uint32_t(p.SS) + cv * 16;
+                    const unsigned char* sb = slot_ptr() + cv * 16;
                     for (int jj = 0; jj < nr; ++jj) {
-                        float b[VE];
-                        V::to_f32(*reinterpret_cast<const uint4*>(sb + jj * rs), b);
+                        float bf[VE];
+                        V::to_f32(*reinterpret_cast<const uint4*>(sb + jj * rs), bf);
 #pragma unroll
-                        for (int k = 0; k < TT; ++k) {
-                            const int t = tg + k * tpv;
+                        for (int q = 0; q < TT; ++q) {
+                            const int t = tg + q * tpv;
                             if (t < nt) {
                                 const float vv = vb[t * r + 8 * s + jj];
 #pragma unroll
-                                for (int e = 0; e < VE; ++e) acc[k][e] = fmaf(vv, b[e], acc[k][e]);
+                                for (int e = 0; e < VE; ++e) acc[q][e] = fmaf(vv, bf[e], acc[q][e]);
                             }
                         }
                     }
                 }
                 release_slot();
             }
-            if (!active) return;
+            wait_slot();  // Y slot
+            if (active)
 #pragma unroll
-            for (int k = 0; k < TT; ++k) {
-                const int t = tg + k * tpv;
-                if (t < nt) {
-                    T* yp = yrow(it, t) + cv * VE;
-                    float yf[VE];
-                    V::to_f32(*reinterpret_cast<const uint4*>(yp), yf);
+                for (int q = 0; q < TT; ++q) {
+                    const int t = tg + q * tpv;
+                    if (t < nt) {
+                        float yf[VE];
+                        V::to_f32(*reinterpret_cast<const uint4*>(slot_ptr() + t * rs + cv * 16), yf);
 #pragma unroll
-                    for (int e = 0; e < VE; ++e) yf[e] = yf[e] + scale * acc[k][e];
-                    *reinterpret_cast<uint4*>(yp) = V::from_f32(yf);
+                        for (int e = 0; e < VE; ++e) yf[e] = yf[e] + scale * acc[q][e];
+                        *reinterpret_cast<uint4*>(yrow(it, t) + cv * VE) = V::from_f32(yf);
+                    }
                 }
-            }
+            release_slot();
         } else {
             // D[col][tok] over this warp's columns [warp*CW, (warp+1)*CW): m-blocks of 16 columns
             using MF = Mma8<T>;
@@ -521,8 +641,7 @@ struct Consumer {
             float acc[KSMAX][4];
 #pragma unroll
             for (int j = 0; j < KSMAX; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
-            const uint32_t ring = smem_u32(S.ring);
-            // ldmatrix.trans: lanes 8*mi..8*mi+7 address rank row rr, columns +8*mi of a 32-column pair of m-blocks
+            // ldmatrix.trans: lanes 8*mi..8*mi+7 address rank row rr, columns +8*mi of a 32-column pair
             const uint32_t laneoff = uint32_t(rr) * rs + uint32_t(warp * CW + mi * 8) * ES;
             const bool math = !(p.dbg & 16);
             for (int s = 0; s < nsl; ++s) {
@@ -538,7 +657,7 @@ struct Consumer {
                     const uint32_t bl = MF::pack(v0 - hf.x, v1 - hf.y);
                     // rows >= nr of a partial slot hold stale bytes: zero their A-operand halves
                     const uint32_t keep = 2 * t4 + 1 < nr ? 0xffffffffu : (2 * t4 < nr ? 0x0000ffffu : 0u);
-                    const uint32_t base = ring + uint32_t(rp.slot) * uint32_t(p.SS) + laneoff;
+                    const uint32_t base = slot_u32() + laneoff;
 #pragma unroll
                     for (int q = 0; q < KSMAX / 2; ++q)
                         if (2 * q < MB) {
@@ -556,50 +675,62 @@ struct Consumer {
                 }
                 release_slot();
             }
-            if (!math) return;
             // acc[j]: columns warp*CW + 16j + g (c0: token 2t4, c1: 2t4+1) and +8 (c2, c3).  One
             // exchange with lane ^ 4 (column g ^ 1) turns them into column pairs of one token:
             // even g keeps token 2t4 (columns g, g+1), odd g token 2t4+1 (columns g-1, g).
-            const bool odd = g & 1;
-            T* yp = ypair(it);
+            wait_slot();  // Y slot: the tokens' y row slices
+            if (math) {
+                const bool odd = g & 1;
+                const int tok = 2 * t4 + (g & 1);
+                const int col = warp * CW + (g & ~1);
+                const unsigned char* ys = slot_ptr() + uint32_t(tok) * rs + uint32_t(col) * ES;
+                T* yp = tok < nt ? yrow(it, tok) + col : nullptr;
 #pragma unroll
-            for (int jm = 0; jm < KSMAX; ++jm)
-                if (jm < MB) {
-                    const float s0 = __shfl_xor_sync(0xffffffffu, odd ? acc[jm][0] : acc[jm][1], 4);
-                    const float s2 = __shfl_xor_sync(0xffffffffu, odd ? acc[jm][2] : acc[jm][3], 4);
-                    const float lo0 = odd ? s0 : acc[jm][0], hi0 = odd ? acc[jm][1] : s0;
-                    const float lo8 = odd ? s2 : acc[jm][2], hi8 = odd ? acc[jm][3] : s2;
-                    if (yp) {
-                        const float2 y0 = MF::unpack(yv[jm][0]);
-                        const float2 y8 = MF::unpack(yv[jm][1]);
-                        *reinterpret_cast<uint32_t*>(yp + 16 * jm) = MF::pack(y0.x + scale * lo0, y0.y + scale * hi0);
-                        *reinterpret_cast<uint32_t*>(yp + 16 * jm + 8) =
-                            MF::pack(y8.x + scale * lo8, y8.y + scale * hi8);
+                for (int jm = 0; jm < KSMAX; ++jm)
+                    if (jm < MB) {
+                        const float s0 = __shfl_xor_sync(0xffffffffu, odd ? acc[jm][0] : acc[jm][1], 4);
+                        const float s2 = __shfl_xor_sync(0xffffffffu, odd ? acc[jm][2] : acc[jm][3], 4);
+                        const float lo0 = odd ? s0 : acc[jm][0], hi0 = odd ? acc[jm][1] : s0;
+                        const float lo8 = odd ? s2 : acc[jm][2], hi8 = odd ? acc[jm][3] : s2;
+                        if (yp) {
+                            const float2 y0 = MF::unpack(*reinterpret_cast<const uint32_t*>(ys + 16 * jm * ES));
+                            const float2 y8 =
+                                MF::unpack(*reinterpret_cast<const uint32_t*>(ys + (16 * jm + 8) * ES));
+                            *reinterpret_cast<uint32_t*>(yp + 16 * jm) =
+                                MF::pack(y0.x + scale * lo0, y0.y + scale * hi0);
+                            *reinterpret_cast<uint32_t*>(yp + 16 * jm + 8) =
+                                MF::pack(y8.x + scale * lo8, y8.y + scale * hi8);
+                        }
                     }
-                }
+            }
+            release_slot();
         }
     }
 
     __device__ __forceinline__ void run() {
-        uint32_t xa[KSMAX][2];  // x fragments of the next item to shrink
-        uint32_t yv[KSMAX][2];  // y pairs of the item being expanded
-        load_x(0, xa);
-        for (int m = 0; m < min(n, kGDepth); ++m) shrink(m, xa);
+        for (int m = 0; m < kGDepth; ++m)
+            if (const GItem* it = item_at(S, m)) shrink(m, *it);
         if (tid == 0) GTRACE(16);
-        for (int i = 0; i < n; ++i) {
-            if (i + kGDepth < n) shrink(i + kGDepth, xa);
-            if (tid == 0) GTRACE(17 + 3 * i);
-            load_y(i, yv);  // in flight during the wait for v
+        int i = 0;
+        for (;; ++i) {
+            const GItem* it = item_at(S, i);
+            if (!it) break;
+            if (const GItem* nx = item_at(S, i + kGDepth)) shrink(i + kGDepth, *nx);
+            if (tid == 0 && i < 15) GTRACE(17 + 3 * i);
             mbar_wait(&S.vfull[i & 1], (i >> 1) & 1);
-            if (tid == 0) GTRACE(18 + 3 * i);
-            expand(i, yv);
+            if (tid == 0 && i < 15) GTRACE(18 + 3 * i);
+            expand(i, *it);
             __syncwarp();
-            if (lane == 0) mbar_arrive(&S.vempty[i & 1]);
-            if (tid == 0) GTRACE(19 + 3 * i);
+            if (lane == 0) {
+                mbar_arrive(&S.vempty[i & 1]);
+                mbar_arrive(&S.dempty[i % kQD]);
+            }
+            if (tid == 0 && i < 15) GTRACE(19 + 3 * i);
         }
         if (tid == 0) {
             GTRACE(63);
-            GTRACE_ALL(3);
+            GTRACE_ALL(2, i);
+            GTRACE_ALL(3, gtimer());
         }
     }
 };
@@ -609,15 +740,12 @@ __global__ void __launch_bounds__(kGThreads, 2) mbgmv_group_kernel(const __grid_
     extern __shared__ __align__(128) unsigned char smem[];
     const GSmem S = carve(smem);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int C = p.C;
-    const int g = blockIdx.x / C, c = blockIdx.x - g * C;
-    const int i0 = p.goff[g], n = p.goff[g + 1] - i0;
+    const int C = p.C, c = int(cluster_ctarank());
     if (threadIdx.x == 0) {
         for (int s = 0; s < kGMaxSlots; ++s) {
             mbar_init(&S.full[s], 1);
             mbar_init(&S.empty[s], kGConsumers);
         }
-        mbar_init(S.dbar, 1);
         for (int b = 0; b < 2; ++b) {
             mbar_init(&S.vfull[b], 1);
             mbar_init(&S.vempty[b], kGConsumers);
@@ -626,39 +754,39 @@ __global__ void __launch_bounds__(kGThreads, 2) mbgmv_group_kernel(const __grid_
             mbar_init(&S.idfull[b], 32);
             mbar_init(&S.idempty[b], kGProducers);
         }
+        for (int b = 0; b < kNP; ++b) {
+            mbar_init(&S.pready[b], C);
+            mbar_init(&S.pfree[b], C);
+        }
+        for (int b = 0; b < kQD; ++b) {
+            mbar_init(&S.qfull[b], 1);
+            mbar_init(&S.qempty[b], C);
+            mbar_init(&S.dfull[b], 1);
+            mbar_init(&S.dempty[b], kGConsumers);
+        }
         fence_mbar_init();
     }
-    __syncthreads();
-    pdl_trigger();  // the next launch may start its prologue (weights only)
+    if (threadIdx.x < 16) reinterpret_cast<uint32_t*>(smem + 704)[threadIdx.x] = 0u;
+    cluster_sync();  // every CTA's barriers exist before any remote arrive
+    pdl_trigger();   // the next launch may start its prologue (weights only)
     if (threadIdx.x == 0) {
         GTRACE(0);
-        GTRACE_ALL(0);
+        GTRACE_ALL(0, gtimer());
     }
-    if (n <= 0) return;
     if (warp >= kGConsumers && warp < kGConsumers + kGProducers) {
-        const int pw = warp - kGConsumers;
-        if (pw == 0 && lane == 0) {
-            mbar_arrive_expect_tx(S.dbar, uint32_t(n) * sizeof(GItem));
-            bulk_g2s(S.desc, p.items + i0, uint32_t(n) * sizeof(GItem), S.dbar);
-        }
-        mbar_wait(S.dbar, 0);
-        if (pw == 0 && lane == 0) GTRACE(1);
-        producer<T>(p, S, c, n, pw, lane);
+        producer<T>(p, S, c, warp - kGConsumers, lane);
     } else if (warp == kGConsumers + kGProducers) {
-        pdl_wait();  // the workspace and the counters belong to the previous kernel until here
-        mbar_wait(S.dbar, 0);
-        exchange(p, S, i0, n, lane);
+        exchange(p, S, lane);
     } else {
-        pdl_wait();  // x, y belong to the previous kernel until here
+        pdl_wait();  // y stores must follow the previous kernel
         if (threadIdx.x == 0) {
             GTRACE(8);
-            GTRACE_ALL(1);
+            GTRACE_ALL(1, gtimer());
         }
-        mbar_wait(S.dbar, 0);
-        if (threadIdx.x == 0) GTRACE(9);
-        Consumer<T, KSMAX> cons(p, S, c, i0, n);
+        Consumer<T, KSMAX> cons(p, S, c);
         cons.run();
     }
+    cluster_sync();  // no CTA leaves while a peer may still read its partials or arrive on its barriers
 }
 
 template <typename T, int KSMAX>
@@ -685,8 +813,30 @@ cudaError_t configure_mbgmv_group() {
     for (const void* k : ks) {
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         if (e) return e;
+        e = cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        if (e) return e;
     }
     return cudaSuccess;
+}
+
+int mbgmv_group_max_clusters(int dtype, int C, size_t smem) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(unsigned(C));
+    cfg.blockDim = dim3(kGThreads);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = unsigned(C);
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, group_kernel_for(dtype, 8), &cfg) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
 }
 
 cudaError_t launch_mbgmv_group(const GroupParams& p, int dtype, int grid, size_t smem, cudaStream_t s) {
@@ -697,8 +847,13 @@ cudaError_t launch_mbgmv_group(const GroupParams& p, int dtype, int grid, size_t
     cfg.blockDim = dim3(kGThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     int na = 0;
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = unsigned(p.C);
+    attr[na].val.clusterDim.y = 1;
+    attr[na].val.clusterDim.z = 1;
+    ++na;
     if (pdl_on()) {
         attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
         attr[na].val.programmaticStreamSerializationAllowed = 1;

@@ -50,7 +50,9 @@ def main():
     raw = W.pool.debug_trace().reshape(-1).astype(np.int64)
     tr = np.stack([raw[0:4096].reshape(16, 256), raw[8192:8192 + 4096].reshape(16, 256)])
     allc = np.stack([raw[4096:4096 + 2048].reshape(512, 4), raw[8192 + 4096:8192 + 4096 + 2048].reshape(512, 4)])
-    t0 = tr[0][tr[0] > 0].min()
+    for a in allc:  # column 2 holds item counts, not timestamps
+        a[:, 2] = np.where(a[:, 0] > 0, a[:, 2], 0)
+    t0 = allc[0][:, 0][allc[0][:, 0] > 0].min()
     for call, arr in (("qkv", tr[0]), ("o", tr[1])):
         print(f"== {call} launch of layer {os.environ.get('SLORA_TRACE_LAYER', '16')} (us after qkv start)")
         for cta in range(16):
@@ -58,19 +60,24 @@ def main():
             print(f"cta{cta:2d} " + " ".join(f"{name(e)}={t:.2f}" for e, t in sorted(ev, key=lambda z: z[1])))
         a = allc[0 if call == "qkv" else 1]
         live = a[:, 0] > 0
-        rel = (a[live] - t0) / 1e3
+        rel = (a[live].astype(np.float64) - t0) / 1e3
         if rel.size:
             q = lambda col: np.percentile(rel[:, col], [0, 10, 50, 90, 100]).round(2).tolist()
-            print(f"all {int(live.sum())} CTAs: start {q(0)} pdl {q(1)} slot0 {q(2)} end {q(3)}")
+            nit = a[live][:, 2]
+            print(f"all {int(live.sum())} CTAs: start {q(0)} pdl {q(1)} end {q(3)} "
+                  f"items/CTA min {nit.min()} median {int(np.median(nit))} max {nit.max()}")
             late = np.argsort(-rel[:, 3])[:12]
             idx = np.nonzero(live)[0]
-            print("latest CTAs (id, start, slot0, end): " +
-                  " ".join(f"({idx[i]},{rel[i,0]:.1f},{rel[i,2]:.1f},{rel[i,3]:.1f})" for i in late))
-        for cta in range(4):
-            iss = [(arr[cta, 160 + k] - t0) / 1e3 for k in range(96) if arr[cta, 160 + k] > 0]
-            rdy = [(arr[cta, 64 + k] - t0) / 1e3 for k in range(96) if arr[cta, 64 + k] > 0]
-            print(f"cta{cta} slots issued: " + " ".join(f"{t:.2f}" for t in iss))
-            print(f"cta{cta} slots ready : " + " ".join(f"{t:.2f}" for t in rdy))
+            print("latest CTAs (id, start, end, items): " +
+                  " ".join(f"({idx[i]},{rel[i,0]:.1f},{rel[i,3]:.1f},{nit[i]})" for i in late))
+        for cta in range(2):
+            print(f"cta{cta} slot k: issued (weights) / consumer waits from / consumer got it (us)")
+            for k in range(64):
+                w, g, i = arr[cta, 128 + k], arr[cta, 64 + k], arr[cta, 192 + k]
+                if g <= 0:
+                    continue
+                f = lambda v: f"{(v - t0) / 1e3:7.2f}" if v > 0 else "      -"
+                print(f"  k={k:2d} issued {f(i)} wait {f(w)} got {f(g)}  stall {(g - w) / 1e3:5.2f}")
 
 
 if __name__ == "__main__":
