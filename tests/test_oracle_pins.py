@@ -231,3 +231,63 @@ def test_memory_optimality(N):
     per, total = tpe.shard_elements(N, 4096, 4096, 64)
     assert sum(per) == total
     assert all(p * N == total for p in per)
+
+
+def _ieee_value(bits, ebits, mbits):
+    """IEEE-754 binary value of a bit pattern, from the definition
+    (sign, biased exponent, fraction; subnormals; inf/nan), as a Fraction or
+    float('inf')/-inf.  Independent of numpy's views."""
+    sign = -1 if bits >> (ebits + mbits) & 1 else 1
+    e = bits >> mbits & ((1 << ebits) - 1)
+    m = bits & ((1 << mbits) - 1)
+    bias = (1 << (ebits - 1)) - 1
+    if e == (1 << ebits) - 1:
+        return sign * float("inf") if m == 0 else float("nan")
+    if e == 0:
+        return sign * Fraction(m, 1 << mbits) * Fraction(2) ** (1 - bias)
+    return sign * (1 + Fraction(m, 1 << mbits)) * Fraction(2) ** (e - bias)
+
+
+@pytest.mark.parametrize("bits,expect", [(0x3F80, 1.0), (0xC040, -3.0), (0x0001, 2.0 ** -133),
+                                         (0x7F7F, 3.3895313892515355e38), (0x4049, 3.140625),
+                                         (0x8000, -0.0), (0x0080, 2.0 ** -126)])
+def test_to_f64_bf16_bit_patterns(bits, expect):
+    """oracle.to_f64 decodes bf16 storage (uint16 bit patterns) exactly: pinned
+    to hand-derived values and to the IEEE definition with 8 exponent and 7
+    fraction bits.  Catches a wrong shift (<< 15 / << 17), a byte swap, or
+    decoding as fp16."""
+    got = oracle.to_f64(np.array([bits], np.uint16), "bf16")[0]
+    assert got == expect and np.signbit(got) == np.signbit(expect)
+    assert Fraction(got) == _ieee_value(bits, 8, 7)
+
+
+def test_to_f64_bf16_sampled_patterns_against_definition():
+    """Every 97th of the 65536 bf16 patterns (all exponents, signs, subnormals,
+    inf/nan) decodes to the IEEE definition, checked with exact rationals."""
+    pats = np.arange(1 << 16, dtype=np.uint32).astype(np.uint16)
+    with np.errstate(invalid="ignore"):  # nan patterns
+        got = oracle.to_f64(pats, "bf16")
+    for b in range(0, 1 << 16, 97):  # a spread sample checked with exact rationals
+        v = _ieee_value(b, 8, 7)
+        if isinstance(v, float):
+            assert np.isinf(got[b]) if not np.isnan(v) else np.isnan(got[b])
+        else:
+            assert Fraction(got[b]) == v, hex(b)
+
+
+@pytest.mark.parametrize("bits", [0x3C00, 0x0001, 0x7BFF, 0xC200, 0x0400])
+def test_to_f64_f16_bit_patterns(bits):
+    got = oracle.to_f64(np.array([bits], np.uint16).view(np.float16), "f16")[0]
+    assert Fraction(got) == _ieee_value(bits, 5, 10)
+
+
+def test_bf16_round_to_nearest_even_ties():
+    """synth.round_to (the storage rounding both sides read) rounds fp32 to
+    bf16 to nearest, ties to even: 1 + 2^-8 is halfway between 1 (even
+    fraction 0) and 1 + 2^-7 (odd) -> 1; 1 + 3*2^-8 is halfway between
+    1 + 2^-7 (odd) and 1 + 2^-6 (even) -> 1 + 2^-6; just above a tie rounds up."""
+    from synth import workload as wl
+    xs = np.array([1 + 2 ** -8, 1 + 3 * 2 ** -8, 1 + 2 ** -8 + 2 ** -20, -(1 + 2 ** -8)], np.float32)
+    b = wl.round_to(xs, "bf16")
+    assert [int(v) for v in b] == [0x3F80, 0x3F82, 0x3F81, 0xBF80]
+    assert list(oracle.to_f64(b, "bf16")) == [1.0, 1 + 2 ** -6, 1 + 2 ** -7, -1.0]
