@@ -71,7 +71,8 @@ typedef enum {
     SLORA_ERR_TOKEN_COUNT_NOT_ONE = 12, /* decode-only call on a multi-token segment */
     SLORA_ERR_INDIVISIBLE = 13,       /* IndivisibleDimension               */
     SLORA_ERR_CUDA = 14,
-    SLORA_ERR_NO_DEVICE = 15          /* device call on a bookkeeping-only pool     */
+    SLORA_ERR_NO_DEVICE = 15,         /* device call on a bookkeeping-only pool     */
+    SLORA_ERR_NCCL = 16               /* NCCL missing, or an NCCL call failed       */
 } slora_status;
 
 const char* slora_status_string(slora_status s);
@@ -235,6 +236,63 @@ slora_status slora_lora_shrink(slora_pool_t pool, slora_batch_t batch, int32_t l
 slora_status slora_lora_expand(slora_pool_t pool, slora_batch_t batch, int32_t layer,
                                uint32_t proj_mask, const float* v, int32_t v_blocks,
                                void* const y[4], const int64_t ldy[4], void* stream);
+
+/* ---------------------------------------------------------------- a6/a8 --
+ * Tensor-parallel LoRA (Fig. lora_tp; readings R3/R4/R13/R14):
+ * N ranks, one process per GPU, each with a pool created with tp_size = N and
+ * its own tp_rank.  The library owns an NCCL communicator (NCCL is loaded at
+ * run time with dlopen("libnccl.so.2"), so a process that already loaded
+ * torch's NCCL shares it) and carries the two exchange steps between its
+ * shrink and expand kernels, on the caller's stream, capturable in a CUDA
+ * graph.  The exchanged intermediate is fp32.
+ *
+ * slora_tp_unique_id: ncclGetUniqueId into id_out (SLORA_TP_ID_BYTES bytes).
+ *   Rank 0 calls it; the bytes reach the other ranks by any channel (e.g. a
+ *   torch.distributed broadcast).
+ * slora_tp_init: ncclCommInitRank(size, id, rank) on the pool's device.
+ *   rank/size must equal the pool's tp_rank/tp_size; size 1 is allowed (the
+ *   collectives become one-rank NCCL calls).  Errors: INVALID_ARG, NO_DEVICE,
+ *   NCCL.  The communicator lives until slora_pool_destroy.
+ *   The exchange buffers (fp32, library-owned) are sized by every later
+ *   slora_batch_prepare: prepare after init.
+ * slora_tp_lora_qkv (the q/k/v projections as "W1"): for p in q,k,v
+ *     v_k   = x A1_{k,p}                 (fp32, T x r/N per token, shrink)
+ *     v     = all_gather_k(v_k)          ONE ncclAllGather of the three
+ *                                        projections' shards (reading R14)
+ *     y_p  += scale * v B1_{k,p}         (expand; y_p is this rank's T x H/N
+ *                                        column shard of the q/k/v output)
+ *   x: T x H (replicated), stride ldx; y[0..2]: T x H/N, strides ldy[0..2].
+ * slora_tp_lora_o (the o projection as "W2", reading R13):
+ *     u_k   = z_k A2_k                   (fp32 partial over this rank's H/N
+ *                                        input rows, shrink)
+ *     u     = all_reduce_sum(u_k)        ncclAllReduce
+ *     base[:, k*H/N:(k+1)*H/N] += scale * u B2_k
+ *   z: this rank's T x H/N slice of the attention output (stride ldz);
+ *   base: this rank's T x H partial sum of the base o projection (stride
+ *   ld_base).  The LoRA output is folded into column slice k, so the base
+ *   layer's own all-reduce (the caller's) then carries base + LoRA.
+ * Both: errors INVALID_ARG (no communicator, tp_size mismatch), SHAPE
+ *   (exchange buffers smaller than the batch: prepare after init), CUDA, NCCL.
+ * slora_tp_get_stats: per-device element counts taken from the count
+ *   arguments passed to NCCL, with the ring schedule's per-device volumes
+ *   (all-gather: (N-1) * sendcount sent; all-reduce: 2(N-1)/N * count sent),
+ *   which equal P:337's 3(N-1)*NR/N and 2(N-1)*NR/N per layer. */
+#define SLORA_TP_ID_BYTES 128
+typedef struct {
+    int64_t allgather_calls;
+    int64_t allgather_send_elems;  /* per device, fp32 elements */
+    int64_t allgather_recv_elems;
+    int64_t allreduce_calls;
+    int64_t allreduce_count;       /* sum of the count arguments */
+    int64_t allreduce_send_elems;  /* per device, ring schedule: 2(N-1)/N * count */
+} slora_tp_stats;
+slora_status slora_tp_unique_id(void* id_out);
+slora_status slora_tp_init(slora_pool_t pool, const void* id, int32_t rank, int32_t size);
+slora_status slora_tp_lora_qkv(slora_pool_t pool, slora_batch_t batch, int32_t layer, const void* x,
+                               int64_t ldx, void* const y[3], const int64_t ldy[3], void* stream);
+slora_status slora_tp_lora_o(slora_pool_t pool, slora_batch_t batch, int32_t layer, const void* z,
+                             int64_t ldz, void* base_partial, int64_t ld_base, void* stream);
+slora_status slora_tp_get_stats(slora_pool_t pool, slora_tp_stats* out);
 
 /* Wait for `stream` and surface any deferred CUDA error. */
 slora_status slora_sync(slora_pool_t pool, void* stream);

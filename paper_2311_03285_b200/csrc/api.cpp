@@ -25,6 +25,9 @@
 #include "../../include/slora.h"
 #include "slora_internal.h"
 
+#include <dlfcn.h>
+#include <nccl.h>  // types only: NCCL is loaded at run time (dlopen), see slora_tp_init
+
 #include <cudaTypedefs.h>
 
 namespace slora {
@@ -74,11 +77,51 @@ extern "C" const char* slora_status_string(slora_status s) {
         case SLORA_ERR_INDIVISIBLE: return "SLORA_ERR_INDIVISIBLE";
         case SLORA_ERR_CUDA: return "SLORA_ERR_CUDA";
         case SLORA_ERR_NO_DEVICE: return "SLORA_ERR_NO_DEVICE";
+        case SLORA_ERR_NCCL: return "SLORA_ERR_NCCL";
     }
     return "SLORA_ERR_UNKNOWN";
 }
 extern "C" const char* slora_last_error(void) { return g_err.c_str(); }
 extern "C" int64_t slora_launch_count(void) { return slora::launch_count(); }
+
+// -------------------------------------------------------------------- NCCL
+// NCCL is loaded on first use with dlopen("libnccl.so.2"): in a process that
+// already loaded torch's NCCL this returns that same library (one NCCL per
+// process), and the C ABI works without NCCL for single-GPU use.
+namespace {
+struct NcclApi {
+    bool tried = false, ok = false;
+    std::string why;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                              cudaStream_t) = nullptr;
+    const char* (*GetErrorString)(ncclResult_t) = nullptr;
+};
+NcclApi& nccl() {
+    static NcclApi api;
+    if (api.tried) return api;
+    api.tried = true;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+        api.why = dlerror() ? dlerror() : "dlopen libnccl.so.2 failed";
+        return api;
+    }
+    auto sym = [&](const char* n) { return dlsym(h, n); };
+    api.GetUniqueId = reinterpret_cast<decltype(api.GetUniqueId)>(sym("ncclGetUniqueId"));
+    api.CommInitRank = reinterpret_cast<decltype(api.CommInitRank)>(sym("ncclCommInitRank"));
+    api.CommDestroy = reinterpret_cast<decltype(api.CommDestroy)>(sym("ncclCommDestroy"));
+    api.AllGather = reinterpret_cast<decltype(api.AllGather)>(sym("ncclAllGather"));
+    api.AllReduce = reinterpret_cast<decltype(api.AllReduce)>(sym("ncclAllReduce"));
+    api.GetErrorString = reinterpret_cast<decltype(api.GetErrorString)>(sym("ncclGetErrorString"));
+    api.ok = api.GetUniqueId && api.CommInitRank && api.CommDestroy && api.AllGather && api.AllReduce &&
+             api.GetErrorString;
+    if (!api.ok) api.why = "libnccl.so.2 lacks a required symbol";
+    return api;
+}
+}  // namespace
 
 // -------------------------------------------------------------------- pool
 namespace {
@@ -211,6 +254,13 @@ struct slora_pool {
     int64_t ws_region = 0;            // floats per workspace region: ring v, warp-task v, MBGMM v (kMgKsplit parts)
     uint64_t launch_seq = 0;
     int sms = 148;
+    // tensor parallelism (slora_tp_*): the library's NCCL communicator and fp32 exchange buffers
+    ncclComm_t tp_comm = nullptr;
+    float* tp_vloc = nullptr;          // q/k/v shrink output of this rank: 3 * NR / N
+    float* tp_vall = nullptr;          // all-gathered q/k/v intermediate: 3 * NR
+    float* tp_u = nullptr;             // o partial / all-reduced intermediate: NR
+    int64_t tp_cap = 0;                // NR the buffers hold
+    slora_tp_stats tp_stats{};
     int32_t* g_ctr = nullptr;          // MBGMV cluster kernel: claim counters, kGCtrSlots pairs (zeroed once)
     uint64_t g_seq = 0;                // rotating counter slot of the next launch
 
@@ -280,6 +330,11 @@ struct slora_batch {
     cudaEvent_t upload_ev = nullptr;
     bool upload_pending = false;
 };
+
+static void tp_release(slora_pool* p) {
+    if (p->tp_comm && nccl().ok) nccl().CommDestroy(p->tp_comm);
+    p->tp_comm = nullptr;
+}
 
 static slora_status check_pool(slora_pool_t p) {
     if (!p) return fail(SLORA_ERR_INVALID_ARG, "null pool");
@@ -400,8 +455,12 @@ extern "C" slora_status slora_pool_destroy(slora_pool_t p) {
         if (p->ws_dev) cudaFree(p->ws_dev);
         if (p->xg_dev) cudaFree(p->xg_dev);
         if (p->g_ctr) cudaFree(p->g_ctr);
+        if (p->tp_vloc) cudaFree(p->tp_vloc);
+        if (p->tp_vall) cudaFree(p->tp_vall);
+        if (p->tp_u) cudaFree(p->tp_u);
         if (p->trace_dev) cudaFree(p->trace_dev);
     }
+    tp_release(p);
     delete p;
     return ok();
 }
@@ -1380,6 +1439,16 @@ extern "C" slora_status slora_batch_prepare(slora_batch_t b, const int64_t* tok_
         p->ws_stride = st;
         p->ws_region = ws_need;
     }
+    // tensor-parallel exchange buffers (slora_tp_*): 3*NR/N, 3*NR and NR fp32
+    if (p->tp_comm && b->NR > p->tp_cap) {
+        const int64_t cap = b->NR * 2;
+        for (float** buf : {&p->tp_vloc, &p->tp_vall, &p->tp_u})
+            if (*buf) CUDA_TRY(cudaFreeAsync(*buf, s));
+        CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&p->tp_vloc), sizeof(float) * size_t(3 * cap), s));
+        CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&p->tp_vall), sizeof(float) * size_t(3 * cap), s));
+        CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&p->tp_u), sizeof(float) * size_t(cap), s));
+        p->tp_cap = cap;
+    }
     // eager descriptors for the usual calls (q/k/v together, o alone)
     slora_status st2 = SLORA_OK;
     if (b->adapted > 0) {
@@ -1755,6 +1824,102 @@ extern "C" slora_status slora_lora_expand(slora_pool_t p, slora_batch_t b, int32
         q.ldy[pj] = ldy[pj];
     }
     return launch(p, 3, q, stream);
+}
+
+// ---------------------------------------------------------- a6/a8: TP
+extern "C" slora_status slora_tp_unique_id(void* id_out) {
+    if (!id_out) return fail(SLORA_ERR_INVALID_ARG, "null id_out");
+    static_assert(sizeof(ncclUniqueId) == SLORA_TP_ID_BYTES, "ncclUniqueId size");
+    NcclApi& n = nccl();
+    if (!n.ok) return fail(SLORA_ERR_NCCL, "NCCL unavailable: %s", n.why.c_str());
+    ncclUniqueId id;
+    const ncclResult_t r = n.GetUniqueId(&id);
+    if (r != ncclSuccess) return fail(SLORA_ERR_NCCL, "ncclGetUniqueId: %s", n.GetErrorString(r));
+    memcpy(id_out, &id, sizeof(id));
+    return ok();
+}
+
+extern "C" slora_status slora_tp_init(slora_pool_t p, const void* id, int32_t rank, int32_t size) {
+    if (check_pool(p) || !id) return fail(SLORA_ERR_INVALID_ARG, "null argument");
+    if (!p->dev) return fail(SLORA_ERR_NO_DEVICE, "bookkeeping-only pool");
+    if (size != p->cfg.tp_size || rank != p->cfg.tp_rank)
+        return fail(SLORA_ERR_INVALID_ARG, "rank/size %d/%d differ from the pool's tp_rank/tp_size %d/%d", rank, size,
+                    p->cfg.tp_rank, p->cfg.tp_size);
+    if (p->tp_comm) return fail(SLORA_ERR_INVALID_ARG, "communicator already initialized");
+    NcclApi& n = nccl();
+    if (!n.ok) return fail(SLORA_ERR_NCCL, "NCCL unavailable: %s", n.why.c_str());
+    CUDA_TRY(cudaSetDevice(p->cfg.device));
+    ncclUniqueId uid;
+    memcpy(&uid, id, sizeof(uid));
+    const ncclResult_t r = n.CommInitRank(&p->tp_comm, size, uid, rank);
+    if (r != ncclSuccess) {
+        p->tp_comm = nullptr;
+        return fail(SLORA_ERR_NCCL, "ncclCommInitRank: %s", n.GetErrorString(r));
+    }
+    return ok();
+}
+
+namespace {
+slora_status tp_checks(slora_pool* p, slora_batch* b) {
+    if (!p || !b) return fail(SLORA_ERR_INVALID_ARG, "null pool/batch");
+    if (!p->tp_comm) return fail(SLORA_ERR_INVALID_ARG, "no communicator: call slora_tp_init first");
+    if (b->adapted > 0 && b->NR > p->tp_cap)
+        return fail(SLORA_ERR_SHAPE, "exchange buffers hold NR=%lld < %lld: prepare the batch after slora_tp_init",
+                    (long long)p->tp_cap, (long long)b->NR);
+    return SLORA_OK;
+}
+}  // namespace
+
+extern "C" slora_status slora_tp_lora_qkv(slora_pool_t p, slora_batch_t b, int32_t layer, const void* x,
+                                          int64_t ldx, void* const y[3], const int64_t ldy[3], void* stream) {
+    slora_status st = tp_checks(p, b);
+    if (st) return st;
+    if (b->adapted == 0) return ok();
+    if (!y || !ldy) return fail(SLORA_ERR_INVALID_ARG, "null y");
+    const int N = p->N();
+    int64_t n_loc = 0;
+    if ((st = slora_lora_v_elems(b, 0x7, N, &n_loc))) return st;
+    if ((st = slora_lora_shrink(p, b, layer, 0x7, x, ldx, p->tp_vloc, stream))) return st;
+    NcclApi& n = nccl();
+    const ncclResult_t r = n.AllGather(p->tp_vloc, p->tp_vall, size_t(n_loc), ncclFloat, p->tp_comm,
+                                       static_cast<cudaStream_t>(stream));
+    if (r != ncclSuccess) return fail(SLORA_ERR_NCCL, "ncclAllGather: %s", n.GetErrorString(r));
+    p->tp_stats.allgather_calls += 1;
+    p->tp_stats.allgather_send_elems += int64_t(N - 1) * n_loc;  // this rank's shard to each of N-1 peers
+    p->tp_stats.allgather_recv_elems += int64_t(N - 1) * n_loc;
+    void* ys[4] = {y[0], y[1], y[2], nullptr};
+    const int64_t lds[4] = {ldy[0], ldy[1], ldy[2], 0};
+    return slora_lora_expand(p, b, layer, 0x7, p->tp_vall, N, ys, lds, stream);
+}
+
+extern "C" slora_status slora_tp_lora_o(slora_pool_t p, slora_batch_t b, int32_t layer, const void* z, int64_t ldz,
+                                        void* base_partial, int64_t ld_base, void* stream) {
+    slora_status st = tp_checks(p, b);
+    if (st) return st;
+    if (b->adapted == 0) return ok();
+    if (!base_partial || ld_base < p->cfg.hidden) return fail(SLORA_ERR_INVALID_ARG, "base partial / stride");
+    const int N = p->N();
+    int64_t n_u = 0;
+    if ((st = slora_lora_v_elems(b, 0x8, 1, &n_u))) return st;
+    if ((st = slora_lora_shrink(p, b, layer, 0x8, z, ldz, p->tp_u, stream))) return st;
+    NcclApi& n = nccl();
+    const ncclResult_t r = n.AllReduce(p->tp_u, p->tp_u, size_t(n_u), ncclFloat, ncclSum, p->tp_comm,
+                                       static_cast<cudaStream_t>(stream));
+    if (r != ncclSuccess) return fail(SLORA_ERR_NCCL, "ncclAllReduce: %s", n.GetErrorString(r));
+    p->tp_stats.allreduce_calls += 1;
+    p->tp_stats.allreduce_count += n_u;
+    p->tp_stats.allreduce_send_elems += 2 * int64_t(N - 1) * n_u / N;  // ring: reduce-scatter + all-gather
+    // fold (reading R13): the expand writes column slice k of the base partial sum
+    void* ys[4] = {nullptr, nullptr, nullptr,
+                   static_cast<uint8_t*>(base_partial) + size_t(int64_t(p->cfg.tp_rank) * p->P) * p->es};
+    const int64_t lds[4] = {0, 0, 0, ld_base};
+    return slora_lora_expand(p, b, layer, 0x8, p->tp_u, 1, ys, lds, stream);
+}
+
+extern "C" slora_status slora_tp_get_stats(slora_pool_t p, slora_tp_stats* out) {
+    if (check_pool(p) || !out) return fail(SLORA_ERR_INVALID_ARG, "null argument");
+    *out = p->tp_stats;
+    return ok();
 }
 
 extern "C" slora_status slora_sync(slora_pool_t p, void* stream) {

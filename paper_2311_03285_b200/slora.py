@@ -25,8 +25,9 @@ STATUS = {
     0: "OK", 1: "INVALID_ARG", 2: "SHAPE", 3: "OUT_OF_PAGES", 4: "ALREADY_RESIDENT",
     5: "NOT_RESIDENT", 6: "PINNED", 7: "NOT_PINNED", 8: "STALE_HANDLE", 9: "FREE_PAGE_READ",
     10: "NONRESIDENT_ADAPTER", 11: "SEGMENT_OVERLAP", 12: "TOKEN_COUNT_NOT_ONE", 13: "INDIVISIBLE",
-    14: "CUDA", 15: "NO_DEVICE",
+    14: "CUDA", 15: "NO_DEVICE", 16: "NCCL",
 }
+TP_ID_BYTES = 128
 
 
 class SloraError(RuntimeError):
@@ -55,6 +56,12 @@ class BatchInfo(ctypes.Structure):
     _fields_ = [("T", ctypes.c_int32), ("adapted_tokens", ctypes.c_int32), ("segments", ctypes.c_int32),
                 ("sum_rank_tokens", ctypes.c_int64), ("weight_bytes_per_proj", ctypes.c_int64),
                 ("mbgmm_segments", ctypes.c_int32)]
+
+
+class TPStats(ctypes.Structure):
+    _fields_ = [("allgather_calls", ctypes.c_int64), ("allgather_send_elems", ctypes.c_int64),
+                ("allgather_recv_elems", ctypes.c_int64), ("allreduce_calls", ctypes.c_int64),
+                ("allreduce_count", ctypes.c_int64), ("allreduce_send_elems", ctypes.c_int64)]
 
 
 _VP = ctypes.c_void_p
@@ -88,6 +95,11 @@ SIGNATURES = {
     "slora_lora_prefetch_next": [_VP, _VP, _I32, _U32],
     "slora_lora_shrink": [_VP, _VP, _I32, _U32, _VP, _I64, _VP, _VP],
     "slora_lora_expand": [_VP, _VP, _I32, _U32, _VP, _I32, ctypes.POINTER(_VP), _PI64, _VP],
+    "slora_tp_unique_id": [_VP],
+    "slora_tp_init": [_VP, _VP, _I32, _I32],
+    "slora_tp_lora_qkv": [_VP, _VP, _I32, _VP, _I64, ctypes.POINTER(_VP), _PI64, _VP],
+    "slora_tp_lora_o": [_VP, _VP, _I32, _VP, _I64, _VP, _I64, _VP],
+    "slora_tp_get_stats": [_VP, ctypes.POINTER(TPStats)],
     "slora_sync": [_VP, _VP],
     "slora_debug_trace": [_VP, _PI64, _I32],
 }
@@ -140,6 +152,13 @@ def _stream(s) -> int:
     if isinstance(s, int):
         return s
     return int(s.cuda_stream)
+
+
+def tp_unique_id() -> bytes:
+    """ncclGetUniqueId (rank 0); broadcast the bytes to the other ranks."""
+    buf = ctypes.create_string_buffer(TP_ID_BYTES)
+    _check(lib().slora_tp_unique_id(buf))
+    return buf.raw
 
 
 def mask_of(projs) -> int:
@@ -195,6 +214,18 @@ class Pool:
         ptr = None
         if host_w is not None:
             host_w = np.ascontiguousarray(host_w)
+            # the library reads exactly this many bytes of the pool's element type from the pointer
+            want_item = ESIZE[self.dtype]
+            kind_ok = (host_w.dtype == np.float32 if self.dtype == "f32" else
+                       host_w.dtype == np.float16 if self.dtype == "f16" else
+                       host_w.dtype in (np.uint16, np.int16))
+            need = self.num_layers * 4 * 2 * self.hidden * rank * want_item
+            if self.device < 0:
+                pass  # bookkeeping-only pool: the library refuses host weights (NO_DEVICE)
+            elif not kind_ok or host_w.itemsize != want_item:
+                raise ValueError(f"host_w dtype {host_w.dtype} does not match the pool dtype {self.dtype}")
+            elif host_w.nbytes != need:
+                raise ValueError(f"host_w holds {host_w.nbytes} bytes, the canonical layout needs {need}")
             ptr = host_w.ctypes.data
         _check(lib().slora_adapter_load(self.h, adapter_id, rank, ptr, scale, _stream(stream),
                                         ctypes.byref(slot)))
@@ -256,6 +287,17 @@ class Pool:
     def sync(self, stream=None) -> None:
         _check(lib().slora_sync(self.h, _stream(stream)))
 
+    # -------------------------------------------------------------- a6/a8
+    def tp_init(self, unique_id: bytes, rank: int, size: int) -> None:
+        """Create the library's NCCL communicator (all ranks, same id)."""
+        buf = ctypes.create_string_buffer(bytes(unique_id), TP_ID_BYTES)
+        _check(lib().slora_tp_init(self.h, buf, rank, size))
+
+    def tp_stats(self) -> dict:
+        r = TPStats()
+        _check(lib().slora_tp_get_stats(self.h, ctypes.byref(r)))
+        return {f: getattr(r, f) for f, _ in TPStats._fields_}
+
     def debug_trace(self) -> np.ndarray:
         """[16 CTAs, 1024 events] globaltimer ns of the last traced launches."""
         out = np.zeros(16 * 1024, np.int64)
@@ -316,6 +358,17 @@ class Batch:
     def shrink(self, layer: int, projs, x, ldx: int, v, stream=None) -> None:
         _check(lib().slora_lora_shrink(self.pool.h, self.h, layer, mask_of(projs), _ptr(x), ldx, _ptr(v),
                                        _stream(stream)))
+
+    def tp_qkv(self, layer: int, x, ldx: int, ys, ldys, stream=None) -> None:
+        """TP q/k/v: shrink -> NCCL all-gather -> expand into the three column shards."""
+        yp = (_VP * 3)(*[_ptr(y) or None for y in ys])
+        ld = (_I64 * 3)(*ldys)
+        _check(lib().slora_tp_lora_qkv(self.pool.h, self.h, layer, _ptr(x), ldx, yp, ld, _stream(stream)))
+
+    def tp_o(self, layer: int, z, ldz: int, base_partial, ld_base: int, stream=None) -> None:
+        """TP o: shrink -> NCCL all-reduce -> expand into column slice k of the base partial."""
+        _check(lib().slora_tp_lora_o(self.pool.h, self.h, layer, _ptr(z), ldz, _ptr(base_partial), ld_base,
+                                     _stream(stream)))
 
     def expand(self, layer: int, projs, v, v_blocks: int, ys, ldys, stream=None) -> None:
         yp, ld = self._ys(ys, ldys)

@@ -102,3 +102,31 @@ class TPLoraLayer:
         P = base_partial.shape[1] // self.N
         y_slice = base_partial[:, self.rank * P:(self.rank + 1) * P]
         self.ops.expand(layer, "o", u, 1, [None, None, None, y_slice], [0, 0, 0, ld_base], stream)
+
+
+class LibraryTP:
+    """S-LoRA TP through the C ABI (slora_tp_*): the library's own NCCL
+    communicator carries the all-gather and the all-reduce between its shrink
+    and expand kernels, on the caller's stream (graph-capturable).
+    torch.distributed only bootstraps it: rank 0 draws the NCCL unique id and
+    broadcasts the 128 bytes (include/slora.h a6/a8)."""
+
+    def __init__(self, pool, group=None):
+        from .slora import tp_unique_id
+        self.pool = pool
+        self.N, self.rank = pool.tp_size, pool.tp_rank
+        uid = tp_unique_id() if self.rank == 0 else None
+        if self.N > 1:
+            obj = [uid]
+            dist.broadcast_object_list(obj, src=0, group=group)
+            uid = obj[0]
+        pool.tp_init(uid, self.rank, self.N)
+
+    def qkv(self, batch, layer, x, ldx, y_shards, ld_y, stream=None):
+        batch.tp_qkv(layer, x, ldx, list(y_shards), list(ld_y), stream)
+
+    def o(self, batch, layer, z_shard, ldz, base_partial, ld_base, stream=None):
+        batch.tp_o(layer, z_shard, ldz, base_partial, ld_base, stream)
+
+    def stats(self):
+        return self.pool.tp_stats()

@@ -152,3 +152,35 @@ def test_batch_grouping_counts():
     assert info["segments"] == len(set(used))
     assert info["sum_rank_tokens"] == sum(ranks[a] for a in used)
     assert info["weight_bytes_per_proj"] == sum(ranks[a] * 2 * 64 * 2 for a in set(used))
+
+
+def test_adapter_load_validates_host_buffer():
+    """The binding checks the host buffer before the library reads from it
+    (ADVICE r01): wrong element type or wrong size raise ValueError."""
+    import paper_2311_03285_b200.slora as sl2
+    p = sl2.Pool.__new__(sl2.Pool)  # a device pool's attributes without creating one
+    p.dtype, p.num_layers, p.hidden, p.device, p.h = "f16", 1, 64, 0, None
+    good = np.zeros(1 * 4 * 2 * 64 * 4, np.float16)
+    with pytest.raises(ValueError):
+        p.adapter_load(1, 4, good.astype(np.float32))  # wider dtype
+    with pytest.raises(ValueError):
+        p.adapter_load(1, 4, good[:-1])                 # undersized
+
+
+def test_tp_entry_points_refuse_without_device_or_communicator():
+    """slora_tp_* on a bookkeeping pool: NO_DEVICE for init; the TP compute
+    calls need a communicator first (INVALID_ARG), before any CUDA work."""
+    c, _ = mk(1000, hidden=64, L=1, max_ad=8)
+    with pytest.raises(sl.SloraError) as e:
+        c.tp_init(bytes(128), 0, 1)
+    assert e.value.name == "NO_DEVICE"
+    c.adapter_load(1, 4)
+    b = sl.Batch(c)
+    b.prepare(np.array([1, 1], np.int64))
+    with pytest.raises(sl.SloraError) as e:
+        b.tp_qkv(0, 0, 64, [0, 0, 0], [64] * 3)
+    assert e.value.name == "INVALID_ARG"
+    with pytest.raises(sl.SloraError) as e:
+        b.tp_o(0, 0, 64, 0, 64)
+    assert e.value.name == "INVALID_ARG"
+    assert c.tp_stats()["allgather_calls"] == 0
