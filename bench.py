@@ -4,16 +4,19 @@
 
 One STEP = one pass of the whole hot path over one synthetic batch:
   a4 batch descriptor (slora_batch_prepare: group by adapter, pack units,
-     upload), then for each of the model's 32 layers
+     upload), then for each of the model's layers
   a5+a7 q/k/v fused shrink->expand (one launch) and o fused shrink->expand
-     (one launch) -- on N > 1 GPUs the split shrink -> NCCL all-gather /
-     all-reduce -> expand of S-LoRA TP (a6, a8 fold into the base partial).
+     (one launch) -- on N > 1 GPUs the library's TP calls (slora_tp_lora_qkv:
+     shrink -> NCCL all-gather -> expand; slora_tp_lora_o: shrink -> NCCL
+     all-reduce -> expand into the base partial, a6 + a8 fold).
 value = adapted tokens x layers / step time (LoRA-layer tokens/s, i.e.
 T / per-layer LoRA time), whole job.  Default workload: BASELINE configs[2]
 decode (Llama-7B h=4096, 2000 adapters, ranks {64,32,16,8} round-robin,
 Zipf alpha=1, decode batch 64, fp16) -- the north_star's ">= 70% of HBM"
-target.  Weights of 32 layers (~3 GB) rotate through the timed region, far
-larger than the 126 MB L2 (no flush needed; stated in config).
+target.  Weights of 32 layers (~3.5 GB) rotate through the timed region, far
+larger than the 126 MB L2 (no flush needed; stated in config).  The line also
+nests the other BASELINE configs measured the same way ("secondary"), each
+with its own roofline, and the two NEXT-2 ablations ("ablations").
 
 --impl reference: the fp64 CPU oracle (oracle/), timed on host cores on a
 bounded sample of the same workload (the tier's reference arm).
@@ -45,10 +48,11 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default=None, help="c1 | c2 | c2-mixed | c3 | c4 (default: c2, or tp preset)")
+    ap.add_argument("--workload", default=None, help="c1 | c2 | c2-mixed | c3 | c4 (default: c2)")
     ap.add_argument("--layers", type=int, default=None)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-secondary", action="store_true", help="skip the nested secondary configs / ablations")
     ap.add_argument("--profile-steps", type=int, default=0, help="untimed steps only (for ncu)")
     ap.add_argument("--no-graph", action="store_true", help="eager launches instead of a CUDA graph replay")
     return ap.parse_args()
@@ -122,32 +126,28 @@ class ClockSampler:
 
 # ------------------------------------------------------------------ setup
 class Workload:
-    def __init__(self, cfg, layers, tp, rank, device, stream):
+    def __init__(self, cfg, layers, tp, rank, device, stream, order=None, kv_tokens=16, tp_path=None):
         import torch
         from paper_2311_03285_b200 import Batch, Pool
         self.cfg, self.L, self.N, self.k = cfg, layers, tp, rank
-        # next-call L2 prefetch hints (slora_lora_prefetch_next), single GPU
-        # (SLORA_BENCH_L2PF: "o" = the q/k/v launch prefetches the o call, "qkv" = the o
-        # launch prefetches the next layer's q/k/v, "both", "0" = none)
-        pf = os.environ.get("SLORA_BENCH_L2PF", "0") if tp == 1 else "0"
-        self.pf_o, self.pf_qkv = pf in ("o", "both", "1"), pf in ("qkv", "both", "1")
-        self.l2pf = pf if (self.pf_o or self.pf_qkv) else None
+        # the TP calls (slora_tp_*) serve the layers when N > 1, or on one GPU with SLORA_BENCH_TP=1
+        self.tp_path = (tp > 1) if tp_path is None else tp_path
         self.batch = wl.make_batch(cfg)
         b = self.batch
         self.T, self.H = b.T, cfg.hidden
         self.P = self.H // tp
         es = wl.elem_bytes(cfg.dtype)
         need = sum(layers * 8 * r for r in b.ranks.values())
-        kv_tokens = 16  # KV pages of every request interleaved with adapter pages
+        # KV pages of every request interleaved with adapter pages; order: page placement
         kv_pages = 2 * kv_tokens * layers * len(b.requests)
+        order = order or os.environ.get("SLORA_BENCH_ORDER", "shuffle")
         self.pool = Pool(self.H, layers, need + kv_pages + 64, dtype=cfg.dtype, device=device, tp_size=tp,
-                         tp_rank=rank, order=os.environ.get("SLORA_BENCH_ORDER", "shuffle"), seed=1234 + rank,
-                         max_adapters=max(256, len(b.ranks) + 8))
+                         tp_rank=rank, order=order, seed=1234 + rank, max_adapters=max(256, len(b.ranks) + 8))
         rid = 0
         reqs = list(b.requests)
         load_s, load_bytes = 0.0, 0
         for i, a in enumerate(b.unique):
-            if rid < len(reqs):
+            if rid < len(reqs) and kv_tokens:
                 self.pool.kv_alloc(rid, kv_tokens)
                 rid += 1
             host = wl.adapter_host_buffer(cfg, a, layers)
@@ -162,10 +162,14 @@ class Workload:
         self.load = {"adapters": len(b.unique), "bytes": int(load_bytes), "ms": round(1e3 * load_s, 3),
                      "GBps": round(load_bytes / max(load_s, 1e-9) / 1e9, 2),
                      "note": "full (unsharded) host tensors of all layers; this rank copies its 1/N shard"}
-        while rid < len(reqs):
+        while rid < len(reqs) and kv_tokens:
             self.pool.kv_alloc(rid, kv_tokens)
             rid += 1
         torch.cuda.synchronize()
+        self.tpl = None
+        if self.tp_path:  # the library's NCCL communicator (bootstrapped over torch.distributed)
+            from paper_2311_03285_b200.tp import LibraryTP
+            self.tpl = LibraryTP(self.pool)
         self.dbatch = Batch(self.pool)
         self.dbatch.prepare(b.token_adapter, stream=stream)
         # a4: batch descriptor (grouping, work lists, LPT schedule, upload), host time per prepare
@@ -181,7 +185,7 @@ class Workload:
         g = torch.Generator(device=dev).manual_seed(5 + rank)
         # activations resident in HBM: x per layer, y per (layer, proj)
         self.x = torch.randn((layers, self.T, self.H), generator=g, device=dev).to(td)
-        if tp == 1:
+        if not self.tp_path:
             self.y = torch.randn((layers, 4, self.T, self.H), generator=g, device=dev).to(td)
         else:
             self.y = torch.randn((layers, 3, self.T, self.P), generator=g, device=dev).to(td)
@@ -204,10 +208,20 @@ class Workload:
 
     graph = None
 
+    def close(self):
+        import torch
+        self.graph = None
+        self.dbatch.close()
+        self.pool.close()
+        del self.x, self.y
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
+
     def capture(self, stream):
-        """Capture the layer sequence (launches only) into a CUDA graph; the
-        per-step batch_prepare stays outside (host work + descriptor upload),
-        as in a serving loop that replays a decode graph every iteration."""
+        """Capture the layer sequence (launches + the library's NCCL calls)
+        into a CUDA graph; the per-step batch_prepare stays outside (host work
+        + descriptor upload), as in a serving loop that replays a decode graph
+        every iteration."""
         import torch
         self.dbatch.prepare(self.batch.token_adapter, stream=stream)
         torch.cuda.synchronize()
@@ -218,48 +232,135 @@ class Workload:
         torch.cuda.synchronize()
         self.graph = g
 
-    def step(self, stream, events=None, tpl=None):
+    def step(self, stream, events=None):
         """One step: prepare + all layers.  events: list to append
         (start, end, kind) CUDA event pairs around each launch."""
         b = self.dbatch
         b.prepare(self.batch.token_adapter, stream=stream)
-        if self.graph is not None and events is None and tpl is None:
+        if self.graph is not None and events is None:
             self.graph.replay()
             return
-        self.layers(stream, events, tpl)
+        self.layers(stream, events)
 
-    def layers(self, stream, events=None, tpl=None):
+    def layers(self, stream, events=None):
         import torch
         b = self.dbatch
         H, P = self.H, self.P
         for l in range(self.L):
-            if self.N == 1:
+            e0 = torch.cuda.Event(enable_timing=True) if events is not None else None
+            if e0:
+                e0.record(stream)
+            if not self.tp_path:
                 ys = [self.y[l, p] for p in range(4)]
-                e0 = torch.cuda.Event(enable_timing=True) if events is not None else None
-                if e0: e0.record(stream)
-                if self.pf_o:  # the q/k/v launch pulls the o call's pages into L2
-                    b.prefetch_next(l, "o")
                 b.apply(l, "qkv", self.x[l], H, ys, [H] * 4, stream=stream)
-                if e0:
-                    e1 = torch.cuda.Event(enable_timing=True); e1.record(stream)
-                    e2 = torch.cuda.Event(enable_timing=True); e2.record(stream)
-                if self.pf_qkv and l + 1 < self.L:  # the o launch pulls the next layer's q/k/v pages
-                    b.prefetch_next(l + 1, "qkv")
-                b.apply(l, "o", self.x[l], H, ys, [H] * 4, stream=stream)
-                if e0:
-                    e3 = torch.cuda.Event(enable_timing=True); e3.record(stream)
-                    events.append((e0, e1, "qkv"))
-                    events.append((e2, e3, "o"))
             else:
-                tpl.qkv(l, self.x[l], H, [self.y[l, p] for p in range(3)], [P, P, P], stream=stream)
-                tpl.o(l, self.z[l], P, self.base[l], H, stream=stream)
+                self.tpl.qkv(b, l, self.x[l], H, [self.y[l, p] for p in range(3)], [P, P, P], stream=stream)
+            if e0:
+                e1 = torch.cuda.Event(enable_timing=True); e1.record(stream)
+                e2 = torch.cuda.Event(enable_timing=True); e2.record(stream)
+            if not self.tp_path:
+                b.apply(l, "o", self.x[l], H, ys, [H] * 4, stream=stream)
+            else:
+                self.tpl.o(b, l, self.z[l], P, self.base[l], H, stream=stream)
+            if e0:
+                e3 = torch.cuda.Event(enable_timing=True); e3.record(stream)
+                events.append((e0, e1, "qkv"))
+                events.append((e2, e3, "o"))
+
+
+def timed_steps(W, stream, steps, ws):
+    """K steps bracketed by barrier + synchronize; per-step CUDA events on the
+    launching stream (between steps: the prepare is part of a step).  Returns
+    (mean ms, per-step ms list), max over ranks for the mean."""
+    import torch
+    import torch.distributed as dist
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
+    ev[0].record(stream)
+    for i in range(steps):
+        W.step(stream)
+        ev[i + 1].record(stream)
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    per = [ev[i].elapsed_time(ev[i + 1]) for i in range(steps)]
+    ms = ev[0].elapsed_time(ev[steps]) / steps
+    if ws > 1:
+        tt = torch.tensor([ms], device=f"cuda:{torch.cuda.current_device()}")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt.item())
+    return ms, per
+
+
+def roofline_of(W, ms, stream, serialized=True):
+    """Roofline of the step: algorithmic bytes / time per step (the launches
+    run back to back, prepare included: a conservative average launch
+    duration); serialized per-launch durations from a separate pass."""
+    import torch
+    peaks, peak_kind = measured_peaks()
+    bytes_step = (W.bytes_qkv + W.bytes_o) * W.L
+    achieved = bytes_step / (ms / 1e3) / 1e9
+    r = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
+         "frac": round(achieved / peaks["hbm_gbs"], 4),
+         "peak_source": f"{peak_kind} copy bandwidth (MEASURED_PEAKS.json hbm_gbs)",
+         "alg_bytes_per_launch": {"qkv": W.bytes_qkv, "o": W.bytes_o},
+         "avg_launch_us_in_step": round(1e3 * ms / (2 * W.L), 2),
+         "frac_of_8TBs_spec": round(achieved / 8000.0, 4)}
+    if serialized:
+        events = []
+        for _ in range(3):
+            W.step(stream, events=events)
+        torch.cuda.synchronize()
+        dur = {"qkv": [], "o": []}
+        for a, b, kind in events:
+            dur[kind].append(a.elapsed_time(b))
+        r["serialized_launch_us"] = {"qkv": round(1e3 * float(np.mean(dur["qkv"])), 2),
+                                     "o": round(1e3 * float(np.mean(dur["o"])), 2)}
+        r["serialized_kernel_ms_per_step"] = round((sum(dur["qkv"]) + sum(dur["o"])) / 3, 4)
+    return r
+
+
+def measure(name, layers, steps, warmup, stream, graph=True):
+    """A secondary config measured like the headline (graph replay, events)."""
+    import torch
+    cfg = wl.CONFIGS[name]
+    W = Workload(cfg, layers, 1, 0, torch.cuda.current_device(), stream)
+    for _ in range(max(3, warmup)):
+        W.step(stream)
+    if graph:
+        W.capture(stream)
+        for _ in range(2):
+            W.step(stream)
+    ms, per = timed_steps(W, stream, steps, 1)
+    out = {"workload": cfg.name, "dtype": cfg.dtype, "hidden": cfg.hidden, "layers": layers, "tokens": W.T,
+           "adapted_tokens": W.Tad, "unique_adapters": len(W.batch.ranks),
+           "ms_per_step": round(ms, 4), "value": round(W.Tad * layers / (ms / 1e3), 1), "unit": UNIT,
+           "p10_p50_p90_ms": [round(float(v), 4) for v in np.percentile(per, [10, 50, 90])],
+           "mbgmm_segments": W.dbatch.info()["mbgmm_segments"],
+           "roofline": roofline_of(W, ms, stream, serialized=False)}
+    W.close()
+    return out
+
+
+def traffic_record(cfg_name):
+    """Measured DRAM bytes per launch of the hot kernel: a STATIC record from
+    the committed ncu capture (profiles/ncu_summary.json), not this run."""
+    try:
+        prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json")))
+        if prof.get("workload") == cfg_name:
+            return {"per_launch_bytes": prof.get("dram_bytes_per_launch"), "source":
+                    "static: profiles/ncu_summary.json (ncu --set full of one layer, committed)"}
+    except Exception:
+        pass
+    return None
 
 
 def run_ours(args):
     import torch
     import torch.distributed as dist
     from paper_2311_03285_b200 import launch_count
-    from paper_2311_03285_b200.tp import LibraryOps, TPLoraLayer
 
     ws, rank, local = dist_env()
     if ws > 1 and not dist.is_initialized():
@@ -271,28 +372,28 @@ def run_ours(args):
     if name == "c0":
         layers = 1
     stream = torch.cuda.current_stream()
-    W = Workload(cfg, layers, ws, rank, local, stream)
-    tpl = None
-    if ws > 1:
-        tpl = TPLoraLayer(LibraryOps(W.dbatch), device=f"cuda:{local}")
-        tpl.buffers_for()
+    tp_path = ws > 1 or os.environ.get("SLORA_BENCH_TP") == "1"
+    W = Workload(cfg, layers, ws, rank, local, stream, tp_path=tp_path)
     if args.profile_steps:
         for _ in range(args.profile_steps):
-            W.step(stream, tpl=tpl)
+            W.step(stream)
         torch.cuda.synchronize()
         return
     warm = max(3, args.warmup)
     for _ in range(warm):
-        W.step(stream, tpl=tpl)
+        W.step(stream)
     torch.cuda.synchronize()
-    # host enqueue cost of one eager step (Python + ctypes + launches)
+    # host enqueue cost of one eager step (Python + ctypes + launches); under TP also the exchange
+    # of one step as counted by the library from its NCCL call arguments (graph replays bypass the host)
+    tp0 = W.tpl.stats() if W.tpl else None
     lc0 = launch_count()
     th0 = time.perf_counter()
-    W.step(stream, tpl=tpl)
+    W.step(stream)
     host_ms = (time.perf_counter() - th0) * 1e3
     launches_per_step = launch_count() - lc0
+    tp1 = W.tpl.stats() if W.tpl else None
     torch.cuda.synchronize()
-    use_graph = ws == 1 and not args.no_graph
+    use_graph = not args.no_graph
     if use_graph:
         W.capture(stream)
         for _ in range(2):
@@ -307,62 +408,15 @@ def run_ours(args):
     # per-launch events inside (they would serialize the programmatic
     # dependent launches); per-launch durations come from a separate pass.
     n0 = launch_count()
-    torch.cuda.synchronize()
-    if ws > 1:
-        dist.barrier()
-    t0 = torch.cuda.Event(enable_timing=True)
-    t1 = torch.cuda.Event(enable_timing=True)
-    t0.record(stream)
-    for _ in range(args.steps):
-        W.step(stream, tpl=tpl)
-    t1.record(stream)
-    torch.cuda.synchronize()
-    if ws > 1:
-        dist.barrier()
+    ms, per = timed_steps(W, stream, args.steps, ws)
     launches = launch_count() - n0
     ck = clocks.stop()
-    ms = t0.elapsed_time(t1) / args.steps
-    if ws > 1:
-        tt = torch.tensor([ms], device=f"cuda:{local}")
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        ms = float(tt.item())
     tokens_step = W.Tad * layers
-    value = tokens_step / (ms / 1e3)
-    peaks, peak_kind = measured_peaks()
-    roofline = None
-    if ws == 1:
-        # serialized per-launch durations (separate, untimed pass)
-        events = []
-        for _ in range(3):
-            W.step(stream, events=events, tpl=tpl)
-        torch.cuda.synchronize()
-        dur = {"qkv": [], "o": []}
-        for a, b, kind in events:
-            dur[kind].append(a.elapsed_time(b))
-        ser_ms = (sum(dur["qkv"]) + sum(dur["o"])) / 3
-        # achieved: algorithmic bytes of the step's launches / the timed
-        # region's time per step (launches back to back, prepare included:
-        # a conservative average launch duration)
-        bytes_step = (W.bytes_qkv + W.bytes_o) * layers
-        kern_ms = ms
-        achieved = bytes_step / (kern_ms / 1e3) / 1e9
-        traffic = None
-        try:
-            prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_summary.json")))
-            if prof.get("workload") == cfg.name:
-                traffic = prof.get("dram_bytes_per_launch")
-        except Exception:
-            pass
-        roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                    "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": traffic,
-                    "peak_source": f"{peak_kind} copy bandwidth (MEASURED_PEAKS.json hbm_gbs)",
-                    "kernel": f"mbgmv_kernel<{cfg.dtype}, kFused> (persistent warp-specialized gather-shrink-expand)",
-                    "alg_bytes_per_launch": {"qkv": W.bytes_qkv, "o": W.bytes_o},
-                    "avg_launch_us_in_step": round(1e3 * ms / (2 * layers), 2),
-                    "serialized_launch_us": {"qkv": round(1e3 * float(np.mean(dur["qkv"])), 2),
-                                             "o": round(1e3 * float(np.mean(dur["o"])), 2)},
-                    "serialized_kernel_ms_per_step": round(ser_ms, 4),
-                    "frac_of_8TBs_spec": round(achieved / 8000.0, 4)}
+    value = tokens_step / (ms / 1e3)  # TP: the N ranks serve the same tokens together (strong scaling)
+    roofline = roofline_of(W, ms, stream)
+    roofline["kernel"] = (f"mbgmv_kernel<{cfg.dtype}, kFused> (persistent warp-specialized gather-shrink-expand)"
+                          if not tp_path else f"mbgmv_kernel<{cfg.dtype}, kShrink/kExpand> + NCCL (per GPU)")
+    roofline["traffic"] = traffic_record(cfg.name) if not tp_path else None
     out = {"metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": ws, "steps": args.steps,
            "warmup": warm, "ms_per_step": round(ms, 4), "higher_is_better": True,
            "scaling": "strong", "vs_baseline": None, "dtype": cfg.dtype,
@@ -373,19 +427,40 @@ def run_ours(args):
                       "projections": "q,k,v,o", "parallelism": f"tp{ws}",
                       "l2": "inputs larger than L2 (adapter pages of all layers ~%.2f GB rotate)" %
                             (layers * (W.bytes_qkv + W.bytes_o) / 1e9),
-                      "step": "batch_prepare + layers x (qkv apply, o apply)",
-                      "launch": "CUDA graph replay of the layer launches (PDL edges); prepare per step"
-                      if use_graph else "eager launches",
-                      "l2_prefetch_next_call": W.l2pf},
+                      "step": "batch_prepare + layers x (qkv, o)" + (" through slora_tp_lora_qkv/_o" if tp_path
+                                                                     else " fused applies"),
+                      "launch": "CUDA graph replay of the layer launches (PDL edges; TP: with the library's "
+                                "NCCL calls); prepare per step" if use_graph else "eager launches"},
+           "p10_p50_p90_ms": [round(float(v), 4) for v in np.percentile(per, [10, 50, 90])],
            "gpu_launches": int(launches_per_step * args.steps if use_graph else launches),
            "host_enqueue_ms_eager_step": round(host_ms, 3), "clocks": ck,
-           "batch_prepare_host_us": W.prepare_us, "adapter_load": W.load}
-    if roofline:
-        out["roofline"] = roofline
-    if ws == 1 and not args.no_e2e:
+           "batch_prepare_host_us": W.prepare_us, "adapter_load": W.load, "roofline": roofline}
+    if W.tpl:
+        st = {k: tp1[k] - tp0[k] for k in tp1}
+        NR = sum(W.batch.ranks[a] for a in W.batch.token_adapter if a >= 0)
+        out["tp_exchange_per_step"] = dict(st, P337_allgather_elems=3 * (ws - 1) * NR // ws * layers,
+                                           P337_allreduce_elems=2 * (ws - 1) * NR // ws * layers,
+                                           source="counts from the arguments passed to ncclAllGather/"
+                                                  "ncclAllReduce (slora_tp_get_stats)")
+    if not args.no_e2e:
         out["e2e"] = run_e2e(W, stream, max(3, args.steps // 2))
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        out["cpu_baseline"] = cpu_baseline(cfg, W.batch, budget_s=10.0)
+        out["cpu_baseline"] = cpu_baseline(cfg, W.batch, budget_s=8.0)
+    W.close()
+    if ws == 1 and not tp_path and not args.no_secondary and name == "c2":
+        sec = {}
+        for sname, sl in (("c2-mixed", 32), ("c1", 32), ("c4", 8)):
+            try:
+                sec[sname] = measure(sname, sl, 10, 3, stream)
+            except Exception as e:  # reported, never silently dropped
+                sec[sname] = {"error": f"{type(e).__name__}: {e}"}
+        sec["c4"]["note"] = "70B shapes unsharded on one GPU (the TP8 config's N=1 point); 8 layers (670 MB of " \
+                            "adapter pages rotate, >> L2)"
+        out["secondary"] = sec
+        try:
+            out["ablations"] = run_ablations(stream)
+        except Exception as e:
+            out["ablations"] = {"error": f"{type(e).__name__}: {e}"}
     if rank == 0:
         print(json.dumps(out), flush=True)
     if ws > 1:
@@ -393,23 +468,33 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def run_ablations(stream):
+    """NEXT-2: the S-LoRA-bmm and no-unify-mem kernel-level
+    ablations, timed on the C2 decode batch (bench_ablations.py)."""
+    import bench_ablations
+    return bench_ablations.run(stream)
+
+
 def run_e2e(W, stream, steps):
     """Same metric through the public API with HOST buffers: every step copies
-    x (all layers) and y (all layers, projections) H2D from pinned memory,
-    prepares the batch from the host token map, runs the layers and reads
-    every y back D2H."""
+    the step's activations H2D from pinned memory (x of all layers and the y
+    outputs they update; under TP also z and the base partials), prepares the
+    batch from the host token map, runs the layers and reads every updated
+    output back D2H."""
     import torch
-    xh = W.x.cpu().pin_memory()
-    yh = W.y.cpu().pin_memory()
-    yo = torch.empty_like(yh).pin_memory()
-    bi = xh.numel() * xh.element_size() + yh.numel() * yh.element_size() + W.T * 8
-    bo = yo.numel() * yo.element_size()
+    ins = [W.x, W.y] + ([W.z, W.base] if W.tp_path else [])
+    outs = [W.y] + ([W.base] if W.tp_path else [])
+    hin = [t.cpu().pin_memory() for t in ins]
+    hout = [torch.empty_like(t, device="cpu").pin_memory() for t in outs]
+    bi = sum(t.numel() * t.element_size() for t in hin) + W.T * 8
+    bo = sum(t.numel() * t.element_size() for t in hout)
 
     def one():
-        W.x.copy_(xh, non_blocking=True)
-        W.y.copy_(yh, non_blocking=True)
+        for d, h in zip(ins, hin):
+            d.copy_(h, non_blocking=True)
         W.step(stream)
-        yo.copy_(W.y, non_blocking=True)
+        for h, d in zip(hout, outs):
+            h.copy_(d, non_blocking=True)
 
     for _ in range(2):
         one()
@@ -452,20 +537,46 @@ def oracle_layer(x, slot, proj, nthreads):
         oracle.lora_apply(x, y, As, Bs, slot, nthreads=nthreads)
 
 
-def cpu_baseline(cfg, batch, budget_s=10.0):
+def _time_loop(fn, budget_s):
+    fn()
+    n, t0 = 0, time.perf_counter()
+    while time.perf_counter() - t0 < budget_s:
+        fn()
+        n += 1
+    return (time.perf_counter() - t0) / max(n, 1), n
+
+
+def cpu_baseline(cfg, batch, budget_s=8.0):
+    """The oracle as it stands on the host cores: the LoRA delta
+    of one layer on all cores and on one thread, and the full layer
+    x.W + delta (base GEMM in the oracle's naive fp64 loops) on a bounded
+    token sample."""
+    import oracle
     cores = os.cpu_count() or 1
     x, slot, proj = oracle_sample(cfg, batch)
     Tad = int((slot >= 0).sum())
-    oracle_layer(x, slot, proj, cores)
-    n = 0
-    t0 = time.perf_counter()
-    while time.perf_counter() - t0 < budget_s:
-        oracle_layer(x, slot, proj, cores)
-        n += 1
-    dt = (time.perf_counter() - t0) / n
+    dt, n = _time_loop(lambda: oracle_layer(x, slot, proj, cores), budget_s)
+    dt1, n1 = _time_loop(lambda: oracle_layer(x, slot, proj, 1), budget_s / 2)
+    # full layer on the first 8 tokens: base x.W (h x d, W ~ N(0, 1/h)) + delta, 4 projections
+    Ts = min(8, batch.T)
+    rng = np.random.default_rng(7)
+    Ws = [rng.standard_normal((cfg.hidden, cfg.hidden)) / np.sqrt(cfg.hidden) for _ in range(4)]
+    xs, ss = x[:Ts], slot[:Ts]
+
+    def full():
+        for (As, Bs, y), Wp in zip(proj, Ws):
+            base = oracle.base_forward(xs, Wp, nthreads=cores)
+            oracle.lora_apply(xs, base, As, Bs, ss, nthreads=cores)
+
+    dtf, nf = _time_loop(full, budget_s / 2)
+    Tads = int((ss >= 0).sum())
     return {"value": round(Tad / dt, 2), "unit": UNIT, "cores": cores, "kind": "oracle",
             "sample": f"{n} repetitions of one layer's q,k,v,o deltas of the {cfg.name} batch "
-                      f"({Tad} tokens, {len(batch.ranks)} adapters), fp64 C oracle, {cores} threads"}
+                      f"({Tad} tokens, {len(batch.ranks)} adapters), fp64 C oracle, {cores} threads",
+            "one_thread_value": round(Tad / dt1, 2),
+            "full_layer_value": round(Tads / dtf, 2),
+            "full_layer_sample": f"{nf} repetitions of x.W + delta for q,k,v,o on the batch's first {Ts} tokens "
+                                 f"(W: {cfg.hidden}x{cfg.hidden} fp64, naive loops), {cores} threads"}
 
 
 def run_reference(args):

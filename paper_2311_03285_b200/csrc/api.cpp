@@ -1457,9 +1457,13 @@ extern "C" slora_status slora_batch_prepare(slora_batch_t b, const int64_t* tok_
             if (!st2) st2 = ensure_call(p, b, fused_kc(p, 1), 0x8, stream);
             if (!st2) st2 = ensure_group(p, b, 0x7, stream);
             if (!st2) st2 = ensure_group(p, b, 0x8, stream);
-        } else {
+        }
+        // split (TP) calls: eagerly whenever they can run, so that a CUDA graph
+        // of slora_tp_lora_* captures kernel launches and NCCL calls only
+        if (p->N() > 1 || p->tp_comm) {
+            const int kc_o = p->N() > 1 ? 2 : 1;  // the o shrink's configuration (slora_lora_shrink)
             if (!st2 && p->kcfg[1].ok) st2 = ensure_call(p, b, 1, 0x7, stream);
-            if (!st2 && p->kcfg[2].ok) st2 = ensure_call(p, b, 2, 0x8, stream);
+            if (!st2 && p->kcfg[kc_o].ok) st2 = ensure_call(p, b, kc_o, 0x8, stream);
             if (!st2 && p->kcfg[3].ok) st2 = ensure_call(p, b, 3, 0x7, stream);
             if (!st2 && p->kcfg[3].ok) st2 = ensure_call(p, b, 3, 0x8, stream);
         }
@@ -1505,6 +1509,12 @@ slora_status ensure_call(slora_pool* p, slora_batch* b, int kc, uint32_t mask, v
     slora_batch::Call& call = b->calls[kc][np];
     if (call.built && call.mask == mask) return SLORA_OK;
     if (!p->kcfg[kc].ok) return fail(SLORA_ERR_SHAPE, "no valid kernel configuration");
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    if (p->dev && cudaStreamIsCapturing(static_cast<cudaStream_t>(stream), &cap) == cudaSuccess &&
+        cap != cudaStreamCaptureStatusNone)
+        return fail(SLORA_ERR_INVALID_ARG, "call descriptor (kernel cfg %d, mask 0x%x) not built by the last prepare: "
+                    "a CUDA graph may only capture calls whose descriptors exist (run the call once eagerly "
+                    "after prepare, or use the calls prepare builds)", kc, mask);
     build_call(b, p->kcfg[kc], p->N(), np, mask, call);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     cudaError_t e = cudaSuccess;
