@@ -204,18 +204,6 @@ slora_status slora_lora_apply(slora_pool_t pool, slora_batch_t batch, int32_t la
                               uint32_t proj_mask, const void* x, int64_t ldx,
                               void* const y[4], const int64_t ldy[4], void* stream);
 
-/* Next-call L2 prefetch hint (single GPU).  The adapter pages of the call
- * (layer, proj_mask) -- the rows every later slora_lora_apply(batch, layer,
- * proj_mask, ...) streams -- are pulled into L2 by the NEXT slora_lora_apply
- * enqueued on this batch while it runs, so HBM keeps streaming across the
- * launch boundary (a serving loop knows the layer order; the paper's
- * kernels read the pages of one call at a time).  One-shot: the
- * hint is consumed by that next apply; proj_mask 0 clears it; a prepare
- * clears it.  Results never depend on it (prefetches only move data into
- * L2).  Errors: INVALID_ARG (layer/mask, tp_size > 1), STALE_HANDLE. */
-slora_status slora_lora_prefetch_next(slora_pool_t pool, slora_batch_t batch, int32_t layer,
-                                      uint32_t proj_mask);
-
 /* Split form (for tensor parallelism).
  * shrink: v = x A_shard in fp32.  For projection p, the stored A shard has
  *   r/div rank columns, div = tp_size for q,k,v and 1 for o (and 1 when

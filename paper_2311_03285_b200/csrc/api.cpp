@@ -20,6 +20,7 @@
 #include <string>
 #include <thread>
 #include <unordered_map>
+#include <unordered_set>
 #include <vector>
 
 #include "../../include/slora.h"
@@ -160,7 +161,7 @@ int esize_of(slora_dtype d) { return d == SLORA_F32 ? 4 : 2; }
 // columns (<= 256 16-byte vectors: one per consumer thread; measured: bulk
 // copies of >= 2 KB stream at full rate).  ns = ring slots filling smem.
 // SLORA_DCHUNK overrides the expand width.
-KernelCfg make_kernel_cfg(int mode, int64_t K, int64_t D, int64_t P, int es, int dtype, bool want_v8 = false) {
+KernelCfg make_kernel_cfg(int mode, int64_t K, int64_t D, int64_t P, int es, int dtype) {
     (void)P;
     KernelCfg k;
     k.mode = mode;
@@ -187,23 +188,6 @@ KernelCfg make_kernel_cfg(int mode, int64_t K, int64_t D, int64_t P, int es, int
         return e ? atoi(e) : 0;
     }();
     if (ns_cap >= 2) ns = std::min(ns, ns_cap);
-    // warp-task kernel (mbgmv8.cu) when asked for (see fused_kc)
-    static const int64_t ebytes = [] {
-        const char* e = getenv("SLORA_V8_EBYTES");
-        return e ? int64_t(atoll(e)) : int64_t(16384);
-    }();
-    if (want_v8) {
-        k.v8 = true;
-        k.ebytes = ebytes;
-        k.ns = 0;
-        k.smem = 0;
-        int dev = 0, sms = 0;
-        cudaGetDevice(&dev);
-        if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) sms = 148;
-        k.grid = sms;
-        k.ok = true;
-        return k;
-    }
     if (ns < 2) return k;
     k.ns = ns;
     k.smem = lora_smem_bytes(mode, K, k.dchunk, ns, es);
@@ -236,11 +220,13 @@ struct slora_pool {
     void* stage_dev[2] = {nullptr, nullptr};
     cudaEvent_t stage_ev[2] = {nullptr, nullptr};
     bool stage_used[2] = {false, false};
-    cudaEvent_t release_ev = nullptr;
-    bool release_pending = false;
+    // page releases (kv_free, adapter_evict) are stream-ordered: one event per
+    // release, and a load waits for every release still in flight (any stream)
+    std::vector<cudaEvent_t> release_evs, spare_evs;
+    std::unordered_set<slora_batch*> batches;  // live batches (detached by pool_destroy)
     // kernel configurations: 0 fused (K=D=H), 1 shrink q/k/v (K=H),
     // 2 shrink o (K=H/N), 3 expand (D=H/N)
-    KernelCfg kcfg[5];  // 0 fused (ring pipeline), 1 shrink q/k/v, 2 shrink o, 3 expand, 4 fused warp-task
+    KernelCfg kcfg[4];  // 0 fused (ring pipeline), 1 shrink q/k/v, 2 shrink o, 3 expand
     long long* trace_dev = nullptr;   // SLORA_TRACE=1: kernel event timestamps
     // rotating per-launch slots: item-done counters (zeroed once; each item's
     // last expand piece re-zeroes its counter) and the fused v workspace
@@ -296,11 +282,10 @@ struct slora_batch {
         uint32_t mask = 0;
         std::vector<DevItem> items;
         std::vector<DevPiece> pieces;   // grouped by CTA (schedule_pieces)
-        std::vector<DevTask8> tasks8;   // v8 kernel: pieces with their items folded in
         std::vector<int32_t> cta_off;   // grid + 1
         std::vector<MgUnit> mg_s, mg_e; // MBGMM shrink / expand units (fused calls with long runs)
         size_t off_items = 0, off_pieces = 0, off_cta = 0, off_mg_s = 0, off_mg_e = 0;
-    } calls[5][5];
+    } calls[4][5];
     // fused single-GPU MBGMV group-kernel plans (mbgmv.cu), per projection count
     struct GroupPlan {
         bool built = false, ok = false;
@@ -319,10 +304,6 @@ struct slora_batch {
     bool mg_gather = false;    // MBGMM runs are whole segments of scattered tokens (x gathered, y via tok_idx)
     int64_t mg_units_max = 0;  // units of one 4-projection fused call (arena sizing)
     size_t off_tok = 0;
-    size_t off_pf = 0;         // PfSeg per segment (next-call L2 prefetch)
-    int32_t pf_rows = 0;       // sum over segments of 2*rank
-    int32_t pf_layer = 0;      // pending slora_lora_prefetch_next hint (consumed by the next apply)
-    uint32_t pf_mask = 0;
     // device arena (bump allocated per prepare) + its pinned staging mirror
     size_t arena_cap = 0, arena_used = 0;
     void* arena_host = nullptr;
@@ -330,6 +311,8 @@ struct slora_batch {
     cudaEvent_t upload_ev = nullptr;
     bool upload_pending = false;
 };
+
+static void batch_free_device(slora_batch* b);
 
 static void tp_release(slora_pool* p) {
     if (p->tp_comm && nccl().ok) nccl().CommDestroy(p->tp_comm);
@@ -391,7 +374,6 @@ extern "C" slora_status slora_pool_create(const slora_pool_config* cfg, slora_po
         if ((e = cudaSetDevice(cfg->device))) return cleanup(e, "cudaSetDevice");
         if ((e = configure_lora_kernels(cfg->device))) return cleanup(e, "configure kernels");
         if ((e = configure_mbgmm_kernels())) return cleanup(e, "configure MBGMM kernels");
-        if ((e = configure_lora8_kernels())) return cleanup(e, "configure MBGMV kernels");
         if ((e = configure_mbgmv_group())) return cleanup(e, "configure MBGMV group kernels");
         if ((e = cudaDeviceGetAttribute(&p->sms, cudaDevAttrMultiProcessorCount, cfg->device))) return cleanup(e, "SM count");
         if ((e = cudaMalloc(&p->g_ctr, sizeof(int32_t) * 2 * kGCtrSlots))) return cleanup(e, "cudaMalloc counters");
@@ -407,17 +389,14 @@ extern "C" slora_status slora_pool_create(const slora_pool_config* cfg, slora_po
             if ((e = cudaEventCreateWithFlags(&p->stage_ev[b], cudaEventDisableTiming)))
                 return cleanup(e, "cudaEventCreate");
         }
-        if ((e = cudaEventCreateWithFlags(&p->release_ev, cudaEventDisableTiming)))
-            return cleanup(e, "cudaEventCreate");
         const int dt = cfg->dtype == SLORA_F32 ? kF32 : (cfg->dtype == SLORA_F16 ? kF16 : kBF16);
         const int64_t H = cfg->hidden;
         p->kcfg[0] = make_kernel_cfg(kFused, H, H, P, es, dt);
         p->kcfg[1] = make_kernel_cfg(kShrink, H, P, P, es, dt);
         p->kcfg[2] = make_kernel_cfg(kShrink, cfg->tp_size > 1 ? P : H, P, P, es, dt);
         p->kcfg[3] = make_kernel_cfg(kExpand, P, P, P, es, dt);
-        p->kcfg[4] = make_kernel_cfg(kFused, H, H, P, es, dt, true);
         if (const char* vb = getenv("SLORA_VERBOSE"); vb && atoi(vb) > 0)
-            for (int c = 0; c < 5; ++c)
+            for (int c = 0; c < 4; ++c)
                 fprintf(stderr, "slora: kcfg[%d] mode=%d K=%lld D=%lld dchunk=%lld ns=%d smem=%zu grid=%d ok=%d\n", c,
                         p->kcfg[c].mode, (long long)p->kcfg[c].K, (long long)p->kcfg[c].D,
                         (long long)p->kcfg[c].dchunk, p->kcfg[c].ns, p->kcfg[c].smem, p->kcfg[c].grid,
@@ -450,7 +429,8 @@ extern "C" slora_status slora_pool_destroy(slora_pool_t p) {
             cudaFree(p->stage_dev[b]);
             cudaEventDestroy(p->stage_ev[b]);
         }
-        cudaEventDestroy(p->release_ev);
+        for (cudaEvent_t ev : p->release_evs) cudaEventDestroy(ev);
+        for (cudaEvent_t ev : p->spare_evs) cudaEventDestroy(ev);
         if (p->sync_dev) cudaFree(p->sync_dev);
         if (p->ws_dev) cudaFree(p->ws_dev);
         if (p->xg_dev) cudaFree(p->xg_dev);
@@ -461,6 +441,10 @@ extern "C" slora_status slora_pool_destroy(slora_pool_t p) {
         if (p->trace_dev) cudaFree(p->trace_dev);
     }
     tp_release(p);
+    for (slora_batch* b : p->batches) {  // live batches become stale handles (their device side freed here)
+        if (p->dev) batch_free_device(b);
+        b->pool = nullptr;
+    }
     delete p;
     return ok();
 }
@@ -488,8 +472,32 @@ extern "C" slora_status slora_fragmentation_report(slora_pool_t p, slora_frag_re
 
 static void record_release(slora_pool* p, void* stream) {
     if (!p->dev) return;
-    cudaEventRecord(p->release_ev, static_cast<cudaStream_t>(stream));
-    p->release_pending = true;
+    cudaEvent_t ev = nullptr;
+    if (!p->spare_evs.empty()) {
+        ev = p->spare_evs.back();
+        p->spare_evs.pop_back();
+    } else if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess) {
+        cudaStreamSynchronize(static_cast<cudaStream_t>(stream));  // no event: make the release complete now
+        return;
+    }
+    cudaEventRecord(ev, static_cast<cudaStream_t>(stream));
+    p->release_evs.push_back(ev);
+}
+// make `s` wait for every page release still in flight; completed ones are recycled
+static cudaError_t wait_releases(slora_pool* p, cudaStream_t s) {
+    std::vector<cudaEvent_t> keep;
+    for (cudaEvent_t ev : p->release_evs) {
+        if (cudaEventQuery(ev) == cudaSuccess) {
+            p->spare_evs.push_back(ev);
+            continue;
+        }
+        cudaGetLastError();  // clear cudaErrorNotReady
+        cudaError_t e = cudaStreamWaitEvent(s, ev, 0);
+        if (e) return e;
+        keep.push_back(ev);
+    }
+    p->release_evs.swap(keep);
+    return cudaSuccess;
 }
 
 // ---------------------------------------------------------------------- KV
@@ -684,7 +692,7 @@ extern "C" slora_status slora_adapter_load(slora_pool_t p, int64_t id, int32_t r
     if (p->dev) {
         cudaStream_t s = static_cast<cudaStream_t>(stream);
         cudaError_t e = cudaSetDevice(p->cfg.device);
-        if (!e && p->release_pending) e = cudaStreamWaitEvent(s, p->release_ev, 0);
+        if (!e) e = wait_releases(p, s);
         if (!e) e = cudaMallocAsync(reinterpret_cast<void**>(&ad.dev_tab), sizeof(int32_t) * size_t(need), s);
         if (!e) e = cudaMemcpyAsync(ad.dev_tab, ad.pages.data(), sizeof(int32_t) * size_t(need),
                                     cudaMemcpyHostToDevice, s);
@@ -746,6 +754,13 @@ extern "C" slora_status slora_adapter_load(slora_pool_t p, int64_t id, int32_t r
             }
         if (!e) e = flush();
         if (e) {
+            // scatter kernels of earlier flushes may still write into the pages: let them finish
+            // before the pages return to the free stack; drop the slot's page table
+            cudaStreamSynchronize(s);
+            cudaGetLastError();
+            const int32_t* none = nullptr;
+            cudaMemcpy(p->slot_tab_dev + ad.slot, &none, sizeof(none), cudaMemcpyHostToDevice);
+            if (ad.dev_tab) cudaFree(ad.dev_tab);
             rollback();
             return fail(SLORA_ERR_CUDA, "adapter load: %s", cudaGetErrorString(e));
         }
@@ -833,6 +848,7 @@ extern "C" slora_status slora_batch_create(slora_pool_t p, slora_batch_t* out) {
     if (check_pool(p) || !out) return fail(SLORA_ERR_INVALID_ARG, "null argument");
     slora_batch* b = new slora_batch();
     b->pool = p;
+    p->batches.insert(b);
     if (p->dev) {
         cudaError_t e = cudaEventCreateWithFlags(&b->upload_ev, cudaEventDisableTiming);
         if (e) {
@@ -844,14 +860,23 @@ extern "C" slora_status slora_batch_create(slora_pool_t p, slora_batch_t* out) {
     return ok();
 }
 
+static void batch_free_device(slora_batch* b) {
+    if (b->upload_pending) cudaEventSynchronize(b->upload_ev);
+    if (b->arena_dev) cudaFree(b->arena_dev);
+    if (b->arena_host) cudaFreeHost(b->arena_host);
+    cudaEventDestroy(b->upload_ev);
+    b->arena_dev = b->arena_host = nullptr;
+    b->upload_pending = false;
+}
+
 extern "C" slora_status slora_batch_destroy(slora_batch_t b) {
     if (!b) return fail(SLORA_ERR_INVALID_ARG, "null batch");
-    if (b->pool->dev) {
-        if (b->upload_pending) cudaEventSynchronize(b->upload_ev);
-        if (b->arena_dev) cudaFree(b->arena_dev);
-        if (b->arena_host) cudaFreeHost(b->arena_host);
-        cudaEventDestroy(b->upload_ev);
+    if (!b->pool) {  // its pool was destroyed first: the device side is already freed
+        delete b;
+        return ok();
     }
+    b->pool->batches.erase(b);
+    if (b->pool->dev) batch_free_device(b);
     delete b;
     return ok();
 }
@@ -941,12 +966,6 @@ void build_call(slora_batch* b, const KernelCfg& k, int N, int nproj, uint32_t m
         return e ? atoi(e) : 32;
     }();
     auto item_dchunk = [&](int rank) -> int64_t {
-        if (k.v8) {  // ~ebytes of B per expand task, in whole warp passes (32 lanes x 16 B)
-            const int64_t pass = 32 * 16 / es;
-            int64_t c = (k.ebytes / (int64_t(rank) * es) + pass - 1) / pass * pass;
-            c = std::max<int64_t>(pass, std::min<int64_t>(c, (k.D + pass - 1) / pass * pass));
-            return c;
-        }
         const int64_t half = k.dchunk / 2;
         if (hirank > 0 && rank >= hirank && half > 0 && k.D % half == 0 && (half * es) % 16 == 0) return half;
         if (o_hirank > 0 && np == 1 && rank >= o_hirank && half > 0 && k.D % half == 0 && (half * es) % 16 == 0)
@@ -954,11 +973,11 @@ void build_call(slora_batch* b, const KernelCfg& k, int N, int nproj, uint32_t m
         return k.dchunk;
     };
     auto item_n_ep = [&](int rank) -> int64_t {
-        if (k.mode == kShrink || (k.dchunk <= 0 && !k.v8)) return 0;
+        if (k.mode == kShrink || k.dchunk <= 0) return 0;
         const int64_t dc = item_dchunk(rank);
         return (k.D + dc - 1) / dc;
     };
-    const int srows = k.v8 ? 1 : kShrinkRows;  // stored A rows per shrink piece
+    const int srows = kShrinkRows;  // stored A rows per shrink piece
     const bool use_runs = k.mode == kFused && b->n_runs > 0;
     call.mg_s.clear();
     call.mg_e.clear();
@@ -1045,26 +1064,6 @@ void build_call(slora_batch* b, const KernelCfg& k, int N, int nproj, uint32_t m
             }
     }
     schedule_pieces(pieces, cost, k.grid, call.pieces, call.cta_off);
-    call.tasks8.clear();
-    if (k.v8)
-        for (const DevPiece& pc : call.pieces) {
-            const DevItem& it = call.items[size_t(pc.item)];
-            DevTask8 t{};
-            t.tab = it.tab;
-            t.vrow = it.vrow;
-            t.kind = pc.kind;
-            t.a = pc.a;
-            t.b = pc.b;
-            t.item = pc.item;
-            t.rank = it.rank;
-            t.pi = it.pi;
-            t.nt = it.nt;
-            t.tok_off = it.tok_off;
-            t.n_sp = it.n_sp;
-            t.n_ep = it.n_ep;
-            t.scale = it.scale;
-            call.tasks8.push_back(t);
-        }
 }
 // --------------------------------------------- MBGMV group kernel plan
 // Streaming rate of the whole GPU (GB/s) for the group kernel's copy pattern:
@@ -1224,27 +1223,13 @@ namespace {
 slora_status ensure_call(slora_pool* p, slora_batch* b, int kc, uint32_t mask, void* stream);
 slora_status ensure_group(slora_pool* p, slora_batch* b, uint32_t mask, void* stream);
 
-// Which single-GPU fused kernel serves a call of np projections.  Measured on
-// C2 decode (tools/layer_micro.py, graphs of 32 layers): the ring pipeline
-// (kernels.cu) streams the large q/k/v call faster (24.4 vs 36 us per launch);
-// the warp-task kernel (mbgmv8.cu) wins an o-only sequence (17.3 vs 19.4 us)
-// but not the interleaved q/k/v + o layer (21.8 vs 21.7 us per launch), so the
-// ring pipeline serves every call by default.  SLORA_MBGMV=warp selects the
-// warp-task kernel for every call, SLORA_MBGMV=auto for the o call only.
-int fused_kc(const slora_pool* p, int np) {
-    static const int force = [] {
-        const char* e = getenv("SLORA_MBGMV");
-        if (!e) return 1;
-        return std::string(e) == "warp" ? 2 : (std::string(e) == "auto" ? 0 : 1);
-    }();
-    const bool v8 = force == 2 || (force == 0 && np == 1);
-    if (v8 && p->kcfg[4].ok) return 4;
-    return 0;
-}
-}
+// The single-GPU fused call's configuration: the ring-pipeline MBGMV kernel (kcfg[0]).
+int fused_kc(const slora_pool*, int) { return 0; }
+}  // namespace
 
 extern "C" slora_status slora_batch_prepare(slora_batch_t b, const int64_t* tok_adapter, int32_t T, void* stream) {
     if (!b) return fail(SLORA_ERR_INVALID_ARG, "null batch");
+    if (!b->pool) return fail(SLORA_ERR_STALE_HANDLE, "the batch's pool was destroyed");
     if (T < 0 || (T > 0 && !tok_adapter)) return fail(SLORA_ERR_INVALID_ARG, "token map");
     slora_pool* p = b->pool;
     for (int32_t i = 0; i < T; ++i)
@@ -1374,12 +1359,14 @@ extern "C" slora_status slora_batch_prepare(slora_batch_t b, const int64_t* tok_
     int64_t chunks = 0;
     for (const DevSeg& s : b->segs) chunks += (s.n_tok + kItemTokCap - 1) / kItemTokCap;
     const int64_t max_items = 4 * chunks;
-    const int64_t max_pieces_per_item = kMaxRank + 64;  // v8: one piece per stored A row
+    // ring kernel: <= ceil(r/8) shrink pieces + D/(dchunk/2) expand pieces per item
+    const int64_t dmin = std::max<int64_t>(1, p->kcfg[0].dchunk / 2);
+    const int64_t max_pieces_per_item = (kMaxRank + kShrinkRows - 1) / kShrinkRows + (p->cfg.hidden + dmin - 1) / dmin;
     const int64_t gitems_max = 4 * (int64_t(b->segs.size()) + (b->adapted + 3) / 4 + b->n_runs + 1);
     const size_t gneed = 5 * (size_t(gitems_max) * sizeof(GItem) + size_t(2 * p->sms + 2) * 4 + 1024);
-    const size_t need = gneed + 256 + size_t(T) * 4 + b->segs.size() * sizeof(PfSeg) + 16 * (1024 + 4 * 1024 + size_t(b->mg_units_max) * sizeof(MgUnit) +
+    const size_t need = gneed + 256 + size_t(T) * 4 + 6 * (1024 + 4 * 1024 + size_t(b->mg_units_max) * sizeof(MgUnit) +
                                                    size_t(max_items) * sizeof(DevItem) +
-                                                   size_t(max_items * max_pieces_per_item) * sizeof(DevTask8));
+                                                   size_t(max_items * max_pieces_per_item) * sizeof(DevPiece));
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     CUDA_TRY(cudaSetDevice(p->cfg.device));
     if (b->upload_pending) CUDA_TRY(cudaEventSynchronize(b->upload_ev));  // pinned arena free again
@@ -1389,7 +1376,7 @@ extern "C" slora_status slora_batch_prepare(slora_batch_t b, const int64_t* tok_
         if (b->arena_dev) CUDA_TRY(cudaFreeAsync(b->arena_dev, s));
         b->arena_host = nullptr;
         b->arena_dev = nullptr;
-        const size_t cap = need * 2;
+        const size_t cap = need + need / 4;  // sized from this batch's call shapes; grows at a later prepare
         CUDA_TRY(cudaHostAlloc(&b->arena_host, cap, cudaHostAllocDefault));
         CUDA_TRY(cudaMallocAsync(&b->arena_dev, cap, s));
         b->arena_cap = cap;
@@ -1397,17 +1384,6 @@ extern "C" slora_status slora_batch_prepare(slora_batch_t b, const int64_t* tok_
     b->arena_used = 0;
     cudaError_t e = cudaSuccess;
     b->off_tok = arena_put(b, b->tok_idx.data(), b->tok_idx.size() * sizeof(int32_t), s, e);
-    {
-        std::vector<PfSeg> pf(b->segs.size());
-        int32_t off = 0;
-        for (size_t si = 0; si < b->segs.size(); ++si) {
-            pf[si] = PfSeg{b->seg_tab[si], off, b->segs[si].rank};
-            off += 2 * b->segs[si].rank;
-        }
-        b->pf_rows = off;
-        b->pf_mask = 0;
-        if (!e && !pf.empty()) b->off_pf = arena_put(b, pf.data(), pf.size() * sizeof(PfSeg), s, e);
-    }
     if (e) return fail(SLORA_ERR_CUDA, "batch upload: %s", cudaGetErrorString(e));
     // per-launch sync slots and fused workspace, sized for this batch
     const int64_t sync_need = 2 + max_items + 32;
@@ -1434,7 +1410,6 @@ extern "C" slora_status slora_batch_prepare(slora_batch_t b, const int64_t* tok_
         if (p->ws_dev) CUDA_TRY(cudaFreeAsync(p->ws_dev, s));
         const int64_t st = ws_need * (2 + kMgKsplit);
         CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&p->ws_dev), sizeof(float) * st * kLaunchSlots, s));
-        // all entries "empty" (0xFFFFFFFF): the warp-task kernel's readiness flags (mbgmv8.cu stage_v)
         CUDA_TRY(cudaMemsetAsync(p->ws_dev, 0xFF, sizeof(float) * st * kLaunchSlots, s));
         p->ws_stride = st;
         p->ws_region = ws_need;
@@ -1487,6 +1462,7 @@ extern "C" slora_status slora_batch_get_info(slora_batch_t b, slora_batch_info* 
 namespace {
 slora_status common_checks(slora_pool* p, slora_batch* b, int32_t layer, uint32_t mask) {
     if (!p || !b) return fail(SLORA_ERR_INVALID_ARG, "null pool/batch");
+    if (!b->pool) return fail(SLORA_ERR_STALE_HANDLE, "the batch's pool was destroyed");
     if (b->pool != p) return fail(SLORA_ERR_INVALID_ARG, "batch belongs to another pool");
     if (!p->dev) return fail(SLORA_ERR_NO_DEVICE, "bookkeeping-only pool");
     if (!b->prepared) return fail(SLORA_ERR_INVALID_ARG, "batch not prepared");
@@ -1519,10 +1495,7 @@ slora_status ensure_call(slora_pool* p, slora_batch* b, int kc, uint32_t mask, v
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     cudaError_t e = cudaSuccess;
     call.off_items = arena_put(b, call.items.data(), call.items.size() * sizeof(DevItem), s, e);
-    if (!e && call.tasks8.empty())
-        call.off_pieces = arena_put(b, call.pieces.data(), call.pieces.size() * sizeof(DevPiece), s, e);
-    if (!e && !call.tasks8.empty())
-        call.off_pieces = arena_put(b, call.tasks8.data(), call.tasks8.size() * sizeof(DevTask8), s, e);
+    if (!e) call.off_pieces = arena_put(b, call.pieces.data(), call.pieces.size() * sizeof(DevPiece), s, e);
     if (!e) call.off_cta = arena_put(b, call.cta_off.data(), call.cta_off.size() * sizeof(int32_t), s, e);
     if (!e) call.off_mg_s = arena_put(b, call.mg_s.data(), call.mg_s.size() * sizeof(MgUnit), s, e);
     if (!e) call.off_mg_e = arena_put(b, call.mg_e.data(), call.mg_e.size() * sizeof(MgUnit), s, e);
@@ -1582,7 +1555,6 @@ slora_status prepare_call(slora_pool* p, slora_batch* b, int kc, int32_t layer, 
     q.tok_idx = reinterpret_cast<const int32_t*>(base + b->off_tok);
     q.items = reinterpret_cast<const DevItem*>(base + call.off_items);
     q.pieces = reinterpret_cast<const DevPiece*>(base + call.off_pieces);
-    q.tasks = reinterpret_cast<const DevTask8*>(base + call.off_pieces);
     q.cta_off = reinterpret_cast<const int32_t*>(base + call.off_cta);
     q.n_pieces = int32_t(call.pieces.size());
     q.n_items = int32_t(call.items.size());
@@ -1605,7 +1577,7 @@ slora_status prepare_call(slora_pool* p, slora_batch* b, int kc, int32_t layer, 
         q.a_row_pages[pj] = (pj < 3) ? N : 1;
     }
     p->ws_slot_base = p->ws_dev + int64_t(slot) * p->ws_stride;
-    if (k.mode == kFused) q.v = p->ws_slot_base + (k.v8 ? p->ws_region : 0);
+    if (k.mode == kFused) q.v = p->ws_slot_base;
     q.trace = p->trace_dev;
     return SLORA_OK;
 }
@@ -1614,10 +1586,7 @@ slora_status launch(slora_pool* p, int kc, LoraParams& q, void* stream) {
     const KernelCfg& k = p->kcfg[kc];
     CUDA_TRY(cudaSetDevice(p->cfg.device));
     const int dt = p->cfg.dtype == SLORA_F32 ? kF32 : (p->cfg.dtype == SLORA_F16 ? kF16 : kBF16);
-    if (k.v8)
-        CUDA_TRY(launch_lora8(q, k.mode, dt, k.grid, static_cast<cudaStream_t>(stream)));
-    else
-        CUDA_TRY(launch_lora(q, k.mode, dt, k.grid, static_cast<cudaStream_t>(stream), k.smem));
+    CUDA_TRY(launch_lora(q, k.mode, dt, k.grid, static_cast<cudaStream_t>(stream), k.smem));
     return ok();
 }
 }  // namespace
@@ -1711,16 +1680,6 @@ extern "C" slora_status slora_lora_apply(slora_pool_t p, slora_batch_t b, int32_
         q.ldy[pj] = ldy[pj];
     }
     q.v_blocks = 1;
-    if (b->pf_mask) {  // one-shot hint: the ring kernel prefetches the next call's pages into L2
-        if (!p->kcfg[kc].v8 && !b->segs.empty()) {
-            q.pf_segs = reinterpret_cast<const PfSeg*>(static_cast<uint8_t*>(b->arena_dev) + b->off_pf);
-            q.pf_nseg = int32_t(b->segs.size());
-            q.pf_rows = b->pf_rows;
-            q.pf_layer = b->pf_layer;
-            q.pf_mask = b->pf_mask;
-        }
-        b->pf_mask = 0;
-    }
     const slora_batch::Call& call = b->calls[kc][q.nproj];
     if (!call.mg_s.empty()) {
         st = launch_mbgmm_pair(p, b, call, q, x, ldx, stream);
@@ -1764,19 +1723,6 @@ extern "C" slora_status slora_lora_apply(slora_pool_t p, slora_batch_t b, int32_
         }
     }
     return launch(p, kc, q, stream);
-}
-
-extern "C" slora_status slora_lora_prefetch_next(slora_pool_t p, slora_batch_t b, int32_t layer, uint32_t mask) {
-    if (mask == 0) {
-        if (b) b->pf_mask = 0;
-        return b ? ok() : fail(SLORA_ERR_INVALID_ARG, "null batch");
-    }
-    slora_status st = common_checks(p, b, layer, mask);
-    if (st) return st;
-    if (p->N() != 1) return fail(SLORA_ERR_INVALID_ARG, "prefetch hints are single-GPU (slora_lora_apply)");
-    b->pf_layer = layer;
-    b->pf_mask = mask;
-    return ok();
 }
 
 extern "C" slora_status slora_lora_v_elems(slora_batch_t b, uint32_t mask, int32_t div, int64_t* out) {

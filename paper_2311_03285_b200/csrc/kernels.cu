@@ -45,6 +45,7 @@
 
 #include <atomic>
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 
 #include "slora_internal.h"
@@ -153,10 +154,6 @@ __device__ __forceinline__ void red_release_add(int* p, int v) {
     asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-// bulk prefetch of `bytes` (multiple of 16) at a 16-byte aligned address into L2
-__device__ __forceinline__ void prefetch_l2_bulk(const void* p, uint32_t bytes) {
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
-}
 __device__ __forceinline__ void prefetch_l1(const void* p) {
     asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
 }
@@ -1108,8 +1105,21 @@ __global__ void __launch_bounds__(kThreads, 1) mbgmv_kernel(const __grid_constan
                 float* vb = vbuf + eb * (kItemTokCap * kMaxRank);
                 if (es == 0) pdl_wait();
                 if (MODE == kFused) {
-                    if (lane == 0)
-                        while (ld_acquire(&p.sync[M.item]) < M.n_sp) __nanosleep(32);
+                    if (lane == 0) {
+                        // bounded: an expand piece waits for shrink pieces of other CTAs, which
+                        // must all be resident (grid <= co-resident CTAs, api.cpp).  If the device
+                        // cannot hold them (e.g. SMs taken by MPS / green contexts), fail the
+                        // launch after ~4 s instead of hanging (surfaces as SLORA_ERR_CUDA).
+                        const long long t_end = gtimer() + 4000000000LL;
+                        while (ld_acquire(&p.sync[M.item]) < M.n_sp) {
+                            __nanosleep(32);
+                            if (gtimer() > t_end) {
+                                printf("slora: expand piece of item %d waited > 4 s for its shrink pieces: "
+                                       "not all CTAs are resident\n", M.item);
+                                __trap();
+                            }
+                        }
+                    }
                     __syncwarp();
                     for (int e = lane; e < M.nt * M.r; e += 32) vb[e] = __ldcg(p.v + M.vbase + e);
                     __syncwarp();
@@ -1146,39 +1156,6 @@ __global__ void __launch_bounds__(kThreads, 1) mbgmv_kernel(const __grid_constan
             if (lane == 0) mbar_arrive(&pempty[b]);
             if (item < 0) break;
             if (lane == 0 && MODE == kFused) red_release_add(&p.sync[item], 1);
-        }
-    } else if (warp == kWarpL2) {
-        // ===================== next-call L2 prefetcher ====================
-        // The adapter pages of the call that follows this one on the stream
-        // (slora_lora_prefetch_next) are pulled into L2 while this launch
-        // runs, so that HBM keeps streaming across the launch boundary.  Row
-        // g of the next call's (projection, segment, A/B row) list goes to
-        // CTA g mod grid; pages are written only by the loader, so this needs
-        // no griddepcontrol.wait.
-        if (p.pf_mask) {
-            const int R2 = p.pf_rows;
-            int npf = 0;
-            for (int pj = 0; pj < 4; ++pj) npf += (p.pf_mask >> pj) & 1;
-            const int64_t total = int64_t(npf) * R2;
-            const uint32_t rowb = uint32_t(P * ES);
-            for (int64_t g = blockIdx.x + int64_t(lane) * gridDim.x; g < total; g += 32LL * gridDim.x) {
-                const int kq = int(g / R2), rem = int(g - int64_t(kq) * R2);
-                int proj = 0;
-                for (int pj = 0, c = 0; pj < 4; ++pj)
-                    if ((p.pf_mask >> pj) & 1) {
-                        if (c == kq) proj = pj;
-                        ++c;
-                    }
-                int lo = 0, hi = p.pf_nseg - 1;  // last segment with off <= rem
-                while (lo < hi) {
-                    const int mid = (lo + hi + 1) >> 1;
-                    if (p.pf_segs[mid].off <= rem) lo = mid;
-                    else hi = mid - 1;
-                }
-                const PfSeg sg = p.pf_segs[lo];
-                const int32_t page = sg.tab[int64_t((p.pf_layer * 4 + proj) * 2) * sg.rank + (rem - sg.off)];
-                prefetch_l2_bulk(pool + int64_t(page) * P, rowb);
-            }
         }
     } else {
         // ============================ consumers ===========================

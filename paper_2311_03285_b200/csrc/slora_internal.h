@@ -50,19 +50,6 @@ struct DevPiece {
 };
 static_assert(sizeof(DevPiece) == 16, "DevPiece layout");
 
-// The warp-task kernel's unit (mbgmv8.cu): a piece with its item's fields
-// folded in, so that a warp resolves it with one load + one page-table hop.
-struct DevTask8 {
-    const int32_t* tab;  // the adapter's device page table
-    int64_t vrow;        // v row offset of the item's token chunk
-    int32_t kind, a, b, item;
-    int32_t rank, pi, nt, tok_off;
-    int32_t n_sp, n_ep;
-    float scale;
-    int32_t pad;
-};
-static_assert(sizeof(DevTask8) == 64, "DevTask8 layout");
-
 #ifndef SLORA_ITEM_TOK
 #define SLORA_ITEM_TOK 2
 #endif
@@ -87,14 +74,13 @@ constexpr int kStreamers = SLORA_STREAMERS;
 constexpr int kWarpStreamer0 = kConsumerWarps, kWarpResolver = kConsumerWarps + 1,
               kWarpStreamer1 = kConsumerWarps + 2, kWarpPrefetch = kConsumerWarps + 3,
               kWarpPublish = kConsumerWarps + 4, kWarpStreamerX = kConsumerWarps + 5;
-// last warp: L2 prefetcher of the next call's adapter pages (LoraParams.pf_*)
-constexpr int kWarpL2 = kConsumerWarps + 3 + kStreamers;
-constexpr int kThreads = (kWarpL2 + 1) * 32;
+constexpr int kWarpsEnd = kConsumerWarps + 3 + kStreamers;  // one past the last streamer
+constexpr int kThreads = kWarpsEnd * 32;
 // streamer index of a warp (-1: not a streamer)
 inline __host__ __device__ int streamer_id(int warp) {
     return warp == kWarpStreamer0 ? 0
            : warp == kWarpStreamer1 ? 1
-           : (warp >= kWarpStreamerX && warp < kWarpL2 ? 2 + warp - kWarpStreamerX : -1);
+           : (warp >= kWarpStreamerX && warp < kWarpsEnd ? 2 + warp - kWarpStreamerX : -1);
 }
 constexpr int kMaxChunks = 8;    // pages one stored A row spans (TP q/k/v: N)
 constexpr int kSlotBytes = 32 * 1024;  // ring slot
@@ -107,22 +93,12 @@ enum Mode : int { kFused = 0, kShrink = 1, kExpand = 2 };
 enum DType : int { kF32 = 0, kF16 = 1, kBF16 = 2 };
 enum PieceKind : int { kPieceS = 0, kPieceE = 1, kPieceStop = 2 };
 
-// Next-call L2 prefetch (slora_lora_prefetch_next): one entry per segment of
-// the batch; off = prefix sum of 2*rank (A and B rows of one projection).
-struct PfSeg {
-    const int32_t* tab;  // the adapter's device page table
-    int32_t off;         // first row of this segment in the per-projection row list
-    int32_t rank;
-};
-static_assert(sizeof(PfSeg) == 16, "PfSeg layout");
-
 struct LoraParams {
     const void* pool;             // page buffer
     int64_t page_elems;           // P
     const int32_t* tok_idx;
     const DevItem* items;
     const DevPiece* pieces;       // grouped by CTA: CTA b runs pieces [cta_off[b], cta_off[b+1])
-    const DevTask8* tasks;        // v8: the same pieces with their items folded in
     const int32_t* cta_off;       // grid + 1 entries
     int32_t n_pieces;
     int32_t n_items;
@@ -144,11 +120,6 @@ struct LoraParams {
     const float* v_in;            // expand input
     int32_t v_blocks;
     int64_t NR;                   // sum over adapted tokens of rank
-    const PfSeg* pf_segs;         // L2 prefetch of call (pf_layer, pf_mask); pf_mask 0 = none
-    int32_t pf_nseg;
-    int32_t pf_rows;              // rows per projection = sum over segments of 2*rank
-    int32_t pf_layer;
-    uint32_t pf_mask;
 };
 
 // Per-launch kernel configuration (chosen on the host, see api.cpp).
@@ -160,8 +131,6 @@ struct KernelCfg {
     size_t smem = 0;
     int grid = 0;                 // persistent CTAs
     bool ok = false;
-    bool v8 = false;              // warp-task kernel (mbgmv8.cu) instead of the ring pipeline
-    int64_t ebytes = 0;           // v8: target B bytes per expand task (rank-dependent column chunk)
 };
 
 // smem bytes for a launch (host and device agree via smem_layout in kernels.cu)
@@ -170,16 +139,6 @@ size_t lora_slot_stride(int mode, int64_t K, int esize);  // ring slot stride (b
 int lora_max_ctas(int mode, int dtype, size_t smem);
 cudaError_t launch_lora(const LoraParams& p, int mode, int dtype, int grid, cudaStream_t s, size_t smem);
 cudaError_t configure_lora_kernels(int device);
-// warp-task MBGMV (mbgmv8.cu): kW8 warps per CTA, one CTA per SM, one stored A
-// row per shrink task
-#ifndef SLORA_W8
-#define SLORA_W8 8
-#endif
-constexpr int kW8 = SLORA_W8;
-size_t lora8_smem_bytes();
-cudaError_t configure_lora8_kernels();
-cudaError_t launch_lora8(const LoraParams& p, int mode, int dtype, int grid, cudaStream_t s);
-
 // ------------------------------------------------- MBGMV cluster kernel (mbgmv.cu)
 // The fused single-GPU MBGMV: a grid of thread-block clusters of C CTAs.
 // Every CTA of a cluster walks the same item list; CTA c owns the K-slice c

@@ -92,7 +92,6 @@ SIGNATURES = {
     "slora_batch_get_info": [_VP, ctypes.POINTER(BatchInfo)],
     "slora_lora_apply": [_VP, _VP, _I32, _U32, _VP, _I64, ctypes.POINTER(_VP), _PI64, _VP],
     "slora_lora_v_elems": [_VP, _U32, _I32, _PI64],
-    "slora_lora_prefetch_next": [_VP, _VP, _I32, _U32],
     "slora_lora_shrink": [_VP, _VP, _I32, _U32, _VP, _I64, _VP, _VP],
     "slora_lora_expand": [_VP, _VP, _I32, _U32, _VP, _I32, ctypes.POINTER(_VP), _PI64, _VP],
     "slora_tp_unique_id": [_VP],
@@ -350,10 +349,6 @@ class Batch:
         yp, ld = self._ys(ys, ldys)
         _check(lib().slora_lora_apply(self.pool.h, self.h, layer, mask_of(projs), _ptr(x), ldx, yp, ld,
                                       _stream(stream)))
-
-    def prefetch_next(self, layer: int, projs) -> None:
-        """One-shot hint: the next apply() prefetches call (layer, projs)'s pages into L2."""
-        _check(lib().slora_lora_prefetch_next(self.pool.h, self.h, layer, mask_of(projs) if projs else 0))
 
     def shrink(self, layer: int, projs, x, ldx: int, v, stream=None) -> None:
         _check(lib().slora_lora_shrink(self.pool.h, self.h, layer, mask_of(projs), _ptr(x), ldx, _ptr(v),

@@ -123,10 +123,6 @@ def test_device_calls_refused_on_bookkeeping_pool():
     with pytest.raises(sl.SloraError) as e:
         b.apply(0, "qkv", 0, 8, [0, 0, 0, 0], [8] * 4)
     assert e.value.name == "NO_DEVICE"
-    with pytest.raises(sl.SloraError) as e:  # L2 prefetch hints need a device pool too
-        b.prefetch_next(0, "o")
-    assert e.value.name == "NO_DEVICE"
-    b.prefetch_next(0, 0)  # clearing a hint is always allowed
     with pytest.raises(sl.SloraError) as e:
         b.prepare(np.array([1, 5], np.int64))
     assert e.value.name == "NONRESIDENT_ADAPTER"
@@ -184,3 +180,18 @@ def test_tp_entry_points_refuse_without_device_or_communicator():
         b.tp_o(0, 0, 64, 0, 64)
     assert e.value.name == "INVALID_ARG"
     assert c.tp_stats()["allgather_calls"] == 0
+
+
+def test_pool_destroy_detaches_live_batches():
+    """Destroying a pool while a batch is alive leaves the batch a
+    stale handle instead of a dangling pointer: prepare -> STALE_HANDLE, and
+    destroying it afterwards is safe."""
+    c, _ = mk(1000, hidden=64, L=1, max_ad=8)
+    c.adapter_load(1, 4)
+    b = sl.Batch(c)
+    b.prepare(np.array([1, -1], np.int64))
+    c.close()
+    with pytest.raises(sl.SloraError) as e:
+        b.prepare(np.array([1], np.int64))
+    assert e.value.name == "STALE_HANDLE"
+    b.close()

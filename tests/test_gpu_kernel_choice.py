@@ -1,10 +1,10 @@
-"""Both single-GPU MBGMV kernels pass the whole parity suite on their own.
+"""Both single-GPU fused MBGMV kernels pass the parity suite on their own.
 
-The library serves a fused call with the ring-pipelined kernel (kernels.cu)
-or the warp-task kernel (mbgmv8.cu) depending on the call's projection count
-(api.cpp fused_kc, ring by default); SLORA_MBGMV=warp forces the warp-task kernel for every call, =auto for the o call.
-The choice is read once per process, so each forced run is a subprocess that
-re-runs the parity and MBGMM suites.  Mark: gpu.
+The library serves a fused call with the ring-pipelined kernel (kernels.cu,
+the default) or, with SLORA_MBGMV=group, the cluster kernel (mbgmv.cu:
+K-split clusters exchanging partial v through distributed shared memory,
+dynamic item claiming).  The choice is read once per process, so each forced
+run is a subprocess that re-runs the parity and MBGMM suites.  Mark: gpu.
 """
 import os
 import subprocess
@@ -16,7 +16,7 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-@pytest.mark.parametrize("kernel", ["warp", "auto"])
+@pytest.mark.parametrize("kernel", ["group"])
 def test_parity_suite_with_forced_kernel(kernel):
     env = dict(os.environ, SLORA_MBGMV=kernel)
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", "-p", "no:cacheprovider",
