@@ -1205,9 +1205,17 @@ __global__ void __launch_bounds__(kThreads, 1) mbgmv_kernel(const __grid_constan
 #ifdef SLORA_FEW_VARIANTS
                     SLORA_SHRINK_CASE(1, 2)
 #else
-                    SLORA_SHRINK_CASE(1, 1) SLORA_SHRINK_CASE(2, 1) SLORA_SHRINK_CASE(3, 1) SLORA_SHRINK_CASE(4, 1)
-                    SLORA_SHRINK_CASE(1, 2) SLORA_SHRINK_CASE(2, 2) SLORA_SHRINK_CASE(3, 2) SLORA_SHRINK_CASE(4, 2)
-                    SLORA_SHRINK_CASE(1, 4) SLORA_SHRINK_CASE(2, 4) SLORA_SHRINK_CASE(3, 4) SLORA_SHRINK_CASE(4, 4)
+                    // only the token counts an item can have (NT <= kItemTokCap)
+                    SLORA_SHRINK_CASE(1, 1) SLORA_SHRINK_CASE(1, 2) SLORA_SHRINK_CASE(1, 4)
+#if SLORA_ITEM_TOK >= 2
+                    SLORA_SHRINK_CASE(2, 1) SLORA_SHRINK_CASE(2, 2) SLORA_SHRINK_CASE(2, 4)
+#endif
+#if SLORA_ITEM_TOK >= 3
+                    SLORA_SHRINK_CASE(3, 1) SLORA_SHRINK_CASE(3, 2) SLORA_SHRINK_CASE(3, 4)
+#endif
+#if SLORA_ITEM_TOK >= 4
+                    SLORA_SHRINK_CASE(4, 1) SLORA_SHRINK_CASE(4, 2) SLORA_SHRINK_CASE(4, 4)
+#endif
 #endif
 #undef SLORA_SHRINK_CASE
                     default: break;
@@ -1245,7 +1253,16 @@ __global__ void __launch_bounds__(kThreads, 1) mbgmv_kernel(const __grid_constan
 #ifdef SLORA_FEW_VARIANTS
                     SLORA_EXPAND_CASE(1)
 #else
-                    SLORA_EXPAND_CASE(1) SLORA_EXPAND_CASE(2) SLORA_EXPAND_CASE(3) SLORA_EXPAND_CASE(4)
+                    SLORA_EXPAND_CASE(1)
+#if SLORA_ITEM_TOK >= 2
+                    SLORA_EXPAND_CASE(2)
+#endif
+#if SLORA_ITEM_TOK >= 3
+                    SLORA_EXPAND_CASE(3)
+#endif
+#if SLORA_ITEM_TOK >= 4
+                    SLORA_EXPAND_CASE(4)
+#endif
 #endif
 #undef SLORA_EXPAND_CASE
                     default: break;
