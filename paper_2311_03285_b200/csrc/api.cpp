@@ -247,8 +247,6 @@ struct slora_pool {
     float* tp_u = nullptr;             // o partial / all-reduced intermediate: NR
     int64_t tp_cap = 0;                // NR the buffers hold
     slora_tp_stats tp_stats{};
-    int32_t* g_ctr = nullptr;          // MBGMV cluster kernel: claim counters, kGCtrSlots pairs (zeroed once)
-    uint64_t g_seq = 0;                // rotating counter slot of the next launch
 
     int64_t free_pages() const { return int64_t(free_stack.size()); }
     int N() const { return cfg.tp_size; }
@@ -286,17 +284,6 @@ struct slora_batch {
         std::vector<MgUnit> mg_s, mg_e; // MBGMM shrink / expand units (fused calls with long runs)
         size_t off_items = 0, off_pieces = 0, off_cta = 0, off_mg_s = 0, off_mg_e = 0;
     } calls[4][5];
-    // fused single-GPU MBGMV group-kernel plans (mbgmv.cu), per projection count
-    struct GroupPlan {
-        bool built = false, ok = false;
-        uint32_t mask = 0;
-        int C = 0, G = 0, grid = 0, ns = 0, Kc = 0, Dc = 0, SS = 0, cps = 0;
-        size_t smem = 0;
-        double pred_us = 0;
-        int64_t makespan = 0;           // predicted bytes of the busiest CTA
-        std::vector<GItem> items;       // largest first (claim order)
-        size_t off_items = 0;
-    } gplans[5];
     // per segment: token ranges [begin, end) of the segment's token list that
     // are MBGMM runs (>= theta consecutive x rows; fused 16-bit calls only)
     std::vector<std::vector<std::pair<int32_t, int32_t>>> runs;
@@ -374,10 +361,7 @@ extern "C" slora_status slora_pool_create(const slora_pool_config* cfg, slora_po
         if ((e = cudaSetDevice(cfg->device))) return cleanup(e, "cudaSetDevice");
         if ((e = configure_lora_kernels(cfg->device))) return cleanup(e, "configure kernels");
         if ((e = configure_mbgmm_kernels())) return cleanup(e, "configure MBGMM kernels");
-        if ((e = configure_mbgmv_group())) return cleanup(e, "configure MBGMV group kernels");
         if ((e = cudaDeviceGetAttribute(&p->sms, cudaDevAttrMultiProcessorCount, cfg->device))) return cleanup(e, "SM count");
-        if ((e = cudaMalloc(&p->g_ctr, sizeof(int32_t) * 2 * kGCtrSlots))) return cleanup(e, "cudaMalloc counters");
-        if ((e = cudaMemset(p->g_ctr, 0, sizeof(int32_t) * 2 * kGCtrSlots))) return cleanup(e, "cudaMemset counters");
         if ((e = cudaMalloc(&p->slot_tab_dev, sizeof(int32_t*) * size_t(cfg->max_adapters))))
             return cleanup(e, "cudaMalloc slot table");
         if ((e = cudaMemset(p->slot_tab_dev, 0, sizeof(int32_t*) * size_t(cfg->max_adapters))))
@@ -434,7 +418,6 @@ extern "C" slora_status slora_pool_destroy(slora_pool_t p) {
         if (p->sync_dev) cudaFree(p->sync_dev);
         if (p->ws_dev) cudaFree(p->ws_dev);
         if (p->xg_dev) cudaFree(p->xg_dev);
-        if (p->g_ctr) cudaFree(p->g_ctr);
         if (p->tp_vloc) cudaFree(p->tp_vloc);
         if (p->tp_vall) cudaFree(p->tp_vall);
         if (p->tp_u) cudaFree(p->tp_u);
@@ -1065,163 +1048,7 @@ void build_call(slora_batch* b, const KernelCfg& k, int N, int nproj, uint32_t m
     }
     schedule_pieces(pieces, cost, k.grid, call.pieces, call.cta_off);
 }
-// --------------------------------------------- MBGMV group kernel plan
-// Streaming rate of the whole GPU (GB/s) for the group kernel's copy pattern:
-// 8-row slots of `rowbytes` bulk copies, `cps` persistent CTAs per SM, one
-// producer warp each, in the C2 decode launch sequence under a CUDA graph
-// with programmatic dependent launch (tools/stream_micro2.cu, measured on
-// this pool's B200: profiles/stream_micro_r02.txt).
-int group_max_clusters(int dtype, int C, size_t smem) {
-    static std::unordered_map<uint64_t, int> cache;
-    const uint64_t key = (uint64_t(dtype) << 48) ^ (uint64_t(C) << 40) ^ uint64_t(smem);
-    auto it = cache.find(key);
-    if (it != cache.end()) return it->second;
-    int dev = 0;
-    const int n = cudaGetDevice(&dev) == cudaSuccess ? mbgmv_group_max_clusters(dtype, C, smem) : 0;
-    cache.emplace(key, n);
-    return n;
-}
-
-double group_stream_gbs(int cps, int64_t rowbytes) {  // two producer warps per CTA
-    if (cps >= 2) return rowbytes >= 4096 ? 6300 : rowbytes >= 2048 ? 6160 : rowbytes >= 1024 ? 5800 : 3810;
-    return rowbytes >= 4096 ? 6100 : rowbytes >= 2048 ? 5980 : rowbytes >= 1024 ? 4300 : 2320;
-}
-
-// Plan one fused call on the cluster kernel (mbgmv.cu): items = (segment,
-// projection, chunk of <= 8 tokens) outside the MBGMM runs, sorted largest
-// first (the order the clusters claim them in).  For each (CTAs per SM,
-// cluster size C) that the shapes allow, simulate the greedy claiming (= LPT)
-// over the G clusters the GPU holds at once and predict the launch time from
-// the measured streaming rate; keep the fastest.  SLORA_GROUP_C / _CPS (and
-// _C_O / _CPS_O for single-projection calls) pin the choice (experiments).
-void plan_group_call(slora_batch* b, uint32_t mask, slora_batch::GroupPlan& gp) {
-    const slora_pool* p = b->pool;
-    gp = slora_batch::GroupPlan{};
-    gp.built = true;
-    gp.mask = mask;
-    if (p->N() != 1) return;
-    int np = 0;
-    for (int pj = 0; pj < 4; ++pj) np += (mask >> pj) & 1;
-    const int64_t H = p->cfg.hidden;
-    const int es = p->es;
-    const int VE = 16 / es;
-    // items: token ranges of each segment outside its MBGMM runs, chunks of <= kGMaxTok tokens
-    std::vector<GItem> its;
-    for (int si = 0; si < int(b->segs.size()); ++si) {
-        const DevSeg& sg = b->segs[size_t(si)];
-        int32_t cur = 0;
-        std::vector<std::pair<int32_t, int32_t>> ranges;
-        if (b->n_runs > 0)
-            for (const auto& rn : b->runs[size_t(si)]) {
-                if (rn.first > cur) ranges.push_back({cur, rn.first});
-                cur = rn.second;
-            }
-        if (cur < sg.n_tok) ranges.push_back({cur, sg.n_tok});
-        for (int pi = 0; pi < np; ++pi)
-            for (const auto& rg : ranges)
-                for (int t0 = rg.first; t0 < rg.second; t0 += kGMaxTok) {
-                    GItem it{};
-                    it.tab = b->seg_tab.empty() ? nullptr : b->seg_tab[size_t(si)];
-                    it.rank = sg.rank;
-                    it.nt = std::min(kGMaxTok, rg.second - t0);
-                    it.pi = pi;
-                    it.scale = sg.scale;
-                    for (int t = 0; t < it.nt; ++t) it.tok[t] = b->tok_idx[size_t(sg.tok_off + t0 + t)];
-                    its.push_back(it);
-                }
-    }
-    // largest first (rank, then tokens); stable, so equal items keep batch order
-    std::stable_sort(its.begin(), its.end(), [](const GItem& a, const GItem& c2) {
-        return a.rank != c2.rank ? a.rank > c2.rank : a.nt > c2.nt;
-    });
-    auto knob = [](const char* a, const char* bk, bool single) {
-        const char* e = single ? getenv(bk) : nullptr;
-        if (!e) e = getenv(a);
-        return e ? atoi(e) : 0;
-    };
-    const int force_c = knob("SLORA_GROUP_C", "SLORA_GROUP_C_O", np == 1);
-    const int force_cps = knob("SLORA_GROUP_CPS", "SLORA_GROUP_CPS_O", np == 1);
-    static const int64_t item_ovh = [] {  // per-item fixed cost in streamed-byte units (x, y, exchange)
-        const char* e = getenv("SLORA_GROUP_ITEM_OVH");
-        return e ? int64_t(atoll(e)) : int64_t(8192);
-    }();
-    const int dtc = es == 4 ? kF32 : (p->cfg.dtype == SLORA_F16 ? kF16 : kBF16);
-    slora_batch::GroupPlan best;
-    for (int cps = 1; cps <= 2; ++cps) {
-        if (force_cps && cps != force_cps) continue;
-        for (int C : {1, 2, 4, 8, 16}) {
-            if (force_c && C != force_c) continue;
-            if (H % C) continue;
-            const int64_t Kc = H / C, Dc = H / C;
-            if ((Kc * es) % 16) continue;
-            if (es == 2 && Kc % 256) continue;  // 8 warps x whole pairs of 16-element k-steps
-            if (es == 2 && Kc > 2048) continue; // x fragments in registers (<= 16 k-steps per warp)
-            if (Dc % VE || (es == 4 && Dc / VE > kGConsumers * 32)) continue;  // fp32 expand: a vector per thread
-            const int64_t rowbytes = Kc * es;
-            if (rowbytes > 4096) continue;
-            const int SS = int(8 * (rowbytes + 16));
-            const int64_t budget = cps == 2 ? 113 * 1024 : 227 * 1024;  // two CTAs per SM: <= 113 KB each
-            const int ns = int(std::min<int64_t>(kGMaxSlots, (budget - kGFixedSmem) / SS));
-            if (ns < (es == 4 ? 10 : 4)) continue;  // fp32 shrink holds its X slot over <= 8 A slots
-            const size_t smem = size_t(kGFixedSmem) + size_t(ns) * size_t(SS);
-            // clusters the GPCs hold at once (C >= 4 does not tile every GPC: measured 33 clusters of 4
-            // at one CTA per SM, 71 at two)
-            const int G = std::min((cps * p->sms) / C, group_max_clusters(dtc, C, smem));
-            if (G < 1) continue;
-            // greedy claiming of the sorted items = LPT; bytes streamed per CTA
-            using HE = std::pair<int64_t, int32_t>;
-            std::priority_queue<HE, std::vector<HE>, std::greater<HE>> heap;
-            for (int g = 0; g < G; ++g) heap.push({0, g});
-            for (const GItem& it : its) {
-                HE h = heap.top();
-                heap.pop();
-                h.first += int64_t(2) * it.rank * rowbytes + item_ovh;
-                heap.push(h);
-            }
-            int64_t makespan = 0;
-            while (!heap.empty()) {
-                makespan = std::max(makespan, heap.top().first);
-                heap.pop();
-            }
-            const double rate = group_stream_gbs(cps, rowbytes) * 1e3 / (double(cps) * p->sms);  // bytes/us per CTA
-            const double us = double(makespan) / rate;
-            if (best.ok && us >= best.pred_us) continue;
-            slora_batch::GroupPlan cand;
-            cand.built = true;
-            cand.ok = true;
-            cand.mask = mask;
-            cand.C = C;
-            cand.G = G;
-            cand.grid = G * C;
-            cand.ns = ns;
-            cand.Kc = int(Kc);
-            cand.Dc = int(Dc);
-            cand.SS = SS;
-            cand.cps = cps;
-            cand.smem = smem;
-            cand.pred_us = us;
-            cand.makespan = makespan;
-            best = std::move(cand);
-        }
-    }
-    if (best.ok) {
-        gp = std::move(best);
-        gp.items = std::move(its);
-    }
-    if (const char* vb = getenv("SLORA_VERBOSE"); vb && atoi(vb) > 0 && gp.ok) {
-        int64_t tot = 0;
-        for (const GItem& it : gp.items) tot += 2 * int64_t(it.rank) * gp.Kc * es;
-        fprintf(stderr, "slora: group plan mask=0x%x C=%d G=%d cps=%d ns=%d smem=%zu items=%zu pred=%.2fus "
-                        "balance=%.3f\n", mask, gp.C, gp.G, gp.cps, gp.ns, gp.smem, gp.items.size(), gp.pred_us,
-                double(tot) / std::max<int64_t>(1, gp.makespan * gp.G));
-    }
-}
-
-}  // namespace
-
-namespace {
 slora_status ensure_call(slora_pool* p, slora_batch* b, int kc, uint32_t mask, void* stream);
-slora_status ensure_group(slora_pool* p, slora_batch* b, uint32_t mask, void* stream);
 
 // The single-GPU fused call's configuration: the ring-pipeline MBGMV kernel (kcfg[0]).
 int fused_kc(const slora_pool*, int) { return 0; }
@@ -1346,7 +1173,6 @@ extern "C" slora_status slora_batch_prepare(slora_batch_t b, const int64_t* tok_
     }
     for (auto& row : b->calls)
         for (auto& c : row) c.built = false;
-    for (auto& g : b->gplans) g.built = false;
     b->epoch = p->epoch;
     b->prepared = true;
     if (!p->dev) {
@@ -1362,9 +1188,7 @@ extern "C" slora_status slora_batch_prepare(slora_batch_t b, const int64_t* tok_
     // ring kernel: <= ceil(r/8) shrink pieces + D/(dchunk/2) expand pieces per item
     const int64_t dmin = std::max<int64_t>(1, p->kcfg[0].dchunk / 2);
     const int64_t max_pieces_per_item = (kMaxRank + kShrinkRows - 1) / kShrinkRows + (p->cfg.hidden + dmin - 1) / dmin;
-    const int64_t gitems_max = 4 * (int64_t(b->segs.size()) + (b->adapted + 3) / 4 + b->n_runs + 1);
-    const size_t gneed = 5 * (size_t(gitems_max) * sizeof(GItem) + size_t(2 * p->sms + 2) * 4 + 1024);
-    const size_t need = gneed + 256 + size_t(T) * 4 + 6 * (1024 + 4 * 1024 + size_t(b->mg_units_max) * sizeof(MgUnit) +
+    const size_t need = 256 + size_t(T) * 4 + 6 * (1024 + 4 * 1024 + size_t(b->mg_units_max) * sizeof(MgUnit) +
                                                    size_t(max_items) * sizeof(DevItem) +
                                                    size_t(max_items * max_pieces_per_item) * sizeof(DevPiece));
     cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -1430,8 +1254,6 @@ extern "C" slora_status slora_batch_prepare(slora_batch_t b, const int64_t* tok_
         if (p->N() == 1) {
             if (!st2) st2 = ensure_call(p, b, fused_kc(p, 3), 0x7, stream);
             if (!st2) st2 = ensure_call(p, b, fused_kc(p, 1), 0x8, stream);
-            if (!st2) st2 = ensure_group(p, b, 0x7, stream);
-            if (!st2) st2 = ensure_group(p, b, 0x8, stream);
         }
         // split (TP) calls: eagerly whenever they can run, so that a CUDA graph
         // of slora_tp_lora_* captures kernel launches and NCCL calls only
@@ -1503,32 +1325,6 @@ slora_status ensure_call(slora_pool* p, slora_batch* b, int kc, uint32_t mask, v
     call.built = true;
     call.mask = mask;
     return SLORA_OK;
-}
-
-// Build + upload the group-kernel plan of a fused call (first use after a
-// prepare) and grow the pool's partial-v workspace / counters to fit it.
-slora_status ensure_group(slora_pool* p, slora_batch* b, uint32_t mask, void* stream) {
-    int np = 0;
-    for (int pj = 0; pj < 4; ++pj) np += (mask >> pj) & 1;
-    slora_batch::GroupPlan& gp = b->gplans[np];
-    if (gp.built && gp.mask == mask) return SLORA_OK;
-    plan_group_call(b, mask, gp);
-    if (!gp.ok || !p->dev) return SLORA_OK;
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
-    cudaError_t e = cudaSuccess;
-    gp.off_items = arena_put(b, gp.items.data(), gp.items.size() * sizeof(GItem), s, e);
-    if (e) return fail(SLORA_ERR_CUDA, "group plan upload: %s", cudaGetErrorString(e));
-    return SLORA_OK;
-}
-
-// Which fused MBGMV kernel serves single-GPU calls: the group kernel
-// (mbgmv.cu) with SLORA_MBGMV=group, else the round-1 ring pipeline (kernels.cu)
-bool use_group_kernel() {
-    static const bool on = [] {
-        const char* e = getenv("SLORA_MBGMV");
-        return e && std::string(e) == "group";
-    }();
-    return on;
 }
 
 // Resolve (building + uploading on first use) the call descriptor and fill the
@@ -1684,43 +1480,6 @@ extern "C" slora_status slora_lora_apply(slora_pool_t p, slora_batch_t b, int32_
     if (!call.mg_s.empty()) {
         st = launch_mbgmm_pair(p, b, call, q, x, ldx, stream);
         if (st) return st;
-    }
-    if (use_group_kernel()) {
-        st = ensure_group(p, b, mask, stream);
-        if (st) return st;
-        const slora_batch::GroupPlan& gp = b->gplans[np];
-        if (gp.ok) {
-            if (gp.items.empty()) return ok();
-            GroupParams g;
-            memset(&g, 0, sizeof(g));
-            uint8_t* base = static_cast<uint8_t*>(b->arena_dev);
-            g.pool = p->cfg.device_buffer;
-            g.P = p->P;
-            g.items = reinterpret_cast<const GItem*>(base + gp.off_items);
-            g.n_items = int32_t(gp.items.size());
-            g.ctr = p->g_ctr + 2 * int64_t(p->g_seq++ % kGCtrSlots);
-            g.C = gp.C;
-            g.Kc = gp.Kc;
-            g.Dc = gp.Dc;
-            g.ns = gp.ns;
-            g.SS = gp.SS;
-            g.layer = layer;
-            for (int pj = 0; pj < 4; ++pj) {
-                g.proj_ids[pj] = q.proj_ids[pj];
-                g.y[pj] = y[pj];
-                g.ldy[pj] = ldy[pj];
-            }
-            g.x = x;
-            g.ldx = ldx;
-            static const int gdbg = [] { const char* e = getenv("SLORA_GDBG"); return e ? atoi(e) : 0; }();
-            g.dbg = gdbg;
-            static const int tr_layer = [] { const char* e = getenv("SLORA_TRACE_LAYER"); return e ? atoi(e) : 16; }();
-            if (p->trace_dev && layer == tr_layer) g.trace = p->trace_dev + (np == 1 ? 8192 : 0);
-            const int dt = p->cfg.dtype == SLORA_F32 ? kF32 : (p->cfg.dtype == SLORA_F16 ? kF16 : kBF16);
-            CUDA_TRY(cudaSetDevice(p->cfg.device));
-            CUDA_TRY(launch_mbgmv_group(g, dt, gp.grid, gp.smem, static_cast<cudaStream_t>(stream)));
-            return ok();
-        }
     }
     return launch(p, kc, q, stream);
 }

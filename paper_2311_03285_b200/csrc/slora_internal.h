@@ -139,61 +139,6 @@ size_t lora_slot_stride(int mode, int64_t K, int esize);  // ring slot stride (b
 int lora_max_ctas(int mode, int dtype, size_t smem);
 cudaError_t launch_lora(const LoraParams& p, int mode, int dtype, int grid, cudaStream_t s, size_t smem);
 cudaError_t configure_lora_kernels(int device);
-// ------------------------------------------------- MBGMV cluster kernel (mbgmv.cu)
-// The fused single-GPU MBGMV: a grid of thread-block clusters of C CTAs.
-// Every CTA of a cluster walks the same item list; CTA c owns the K-slice c
-// of every stored A row (shrink: partial dot products over that slice) and
-// the output column slice c (expand).  The C partial v of an item meet in
-// distributed shared memory; the items are software-pipelined so that the
-// exchange of item i overlaps the shrink of the next ones.
-struct GItem {
-    const int32_t* tab;  // the adapter's device page table ([layer][proj][A/B][row])
-    int32_t rank;        // r
-    int32_t nt;          // tokens of this item (<= kGMaxTok)
-    int32_t pi;          // index of the projection in the call's mask order
-    int32_t pad0;
-    float scale;         // per-adapter scale (reading R6)
-    int32_t pad1;
-    int32_t tok[8];      // x / y rows of the item's tokens
-};
-static_assert(sizeof(GItem) == 64, "GItem layout");
-constexpr int kGMaxTok = 8;       // tokens per item (larger segments are chunked)
-constexpr int kGQueue = 8;        // claimed-item descriptor ring per CTA
-constexpr int kGMaxSlots = 16;    // ring slots
-constexpr int kGConsumers = 8;    // consumer warps
-constexpr int kGDepth = 2;        // consumer pipeline: shrink of item i+kGDepth before the expand of item i
-constexpr int kGProducers = 2;    // bulk-copy issuing warps (alternate slots; one warp issues ~60 ns/copy)
-constexpr int kGThreads = (kGConsumers + kGProducers + 1) * 32;  // + exchange warp
-// barriers, zero row, deferred activation slots, claimed indices | descriptor ring | page-id ring
-// (4 items) | shrink partials (2 x 8 warps x 64) | v (2 x 8 x 64) | this CTA's partial v (3 x 8 x 64)
-constexpr int kGFixedSmem = 1152 + kGQueue * 64 + 4 * 128 * 4 + 2 * 8 * 64 * 4 + 2 * kGMaxTok * 64 * 4 +
-                            3 * kGMaxTok * 64 * 4;  // 18048
-constexpr int kGCtrSlots = 128;   // per-launch claim counters (rotating; adjacent launches never share one)
-
-struct GroupParams {
-    const void* pool;
-    int64_t P;                 // page elements
-    const GItem* items;        // the call's items, largest first; clusters claim them in order
-    int32_t n_items;
-    int32_t* ctr;              // this launch's claim counter pair (zero on entry, reset by the last cluster)
-    int32_t C;                 // CTAs per cluster
-    int32_t Kc, Dc;            // shrink K slice, expand column slice (elements)
-    int32_t ns;                // ring slots
-    int32_t SS;                // ring slot stride (bytes): 8 rows x (max(Kc, Dc) * es + 16)
-    int32_t layer;
-    int32_t proj_ids[4];
-    const void* x;
-    int64_t ldx;
-    void* y[4];
-    int64_t ldy[4];
-    int32_t dbg;               // diagnostics (SLORA_GDBG): 1 no exchange, 8 no shrink math,
-                               // 16 no expand math, 32 no weight copies
-    long long* trace;          // diagnostics: globaltimer events (nullptr = off)
-};
-cudaError_t configure_mbgmv_group();
-cudaError_t launch_mbgmv_group(const GroupParams& p, int dtype, int grid, size_t smem, cudaStream_t s);
-int mbgmv_group_max_clusters(int dtype, int C, size_t smem);  // co-resident clusters (occupancy query)
-
 // ------------------------------------------------------------------ MBGMM
 // Long prefill runs (>= theta consecutive x rows of one adapter) go to the
 // tensor-core MBGMM kernels (mbgmm.cu); units are built on the host.
