@@ -446,6 +446,11 @@ def run_ours(args):
         out["e2e"] = run_e2e(W, stream, max(3, args.steps // 2))
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(cfg, W.batch, budget_s=8.0)
+    if ws == 1 and not tp_path and not args.no_secondary and use_graph:
+        try:
+            out["adapter_io"] = run_adapter_io(W, stream)
+        except Exception as e:  # reported, never silently dropped
+            out["adapter_io"] = {"error": f"{type(e).__name__}: {e}"}
     W.close()
     if ws == 1 and not tp_path and not args.no_secondary and name == "c2":
         sec = {}
@@ -466,6 +471,105 @@ def run_ours(args):
     if ws > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def run_adapter_io(W, stream, n_adapters=16):
+    """NEXT-1: adapter loads on the library's loader thread + copy stream
+    (slora_adapter_prefetch), alone and overlapped with the decode step.
+
+    A second set of adapters (the ranks of the batch's first n_adapters, new ids, all layers)
+    is loaded into a pool of its own on the same GPU: from page-locked host buffers (the
+    loader's H2D reads them directly) and from pageable numpy buffers (packed by the loader's
+    host threads into pinned staging).  Then the pinned set is prefetched while the step's
+    graph is replayed: hidden = 1 - (T_both - T_steps) / T_load, with T_both the wall time
+    until the steps and the loads are both done."""
+    import torch
+    from paper_2311_03285_b200 import Pool
+    cfg, L = W.cfg, W.L
+    ranks = [W.batch.ranks[a] for a in W.batch.unique][:n_adapters]
+    ids = [1_000_000 + i for i in range(len(ranks))]
+    need = sum(L * 8 * r for r in ranks)
+    pool = Pool(W.H, L, need + 16, dtype=cfg.dtype, device=torch.cuda.current_device(), max_adapters=len(ids) + 8)
+    by_rank = {r: wl.adapter_host_buffer(cfg, 100_000 + r, L, rank=r) for r in set(ranks)}  # content is immaterial
+    hosts = [by_rank[r].copy() for r in ranks]
+    td = torch.int16 if cfg.dtype == "bf16" else None
+    pinned = [(torch.from_numpy(h.view(np.int16)) if td else torch.from_numpy(h)).pin_memory() for h in hosts]
+    nbytes = sum(h.nbytes for h in hosts)
+
+    def load_all(bufs):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for i, r, hb in zip(ids, ranks, bufs):
+            pool.adapter_prefetch(i, r, hb)
+        for i in ids:
+            pool.adapter_wait(i)
+        t = time.perf_counter() - t0
+        for i in ids:
+            pool.adapter_evict(i, stream=stream)
+        torch.cuda.synchronize()
+        return t
+
+    # the serving loop's compute stream at high priority, the library's copy stream at the lowest:
+    # the LoRA kernels' CTAs are scheduled ahead of the loader's scatter kernels
+    lo, hi = torch.cuda.Stream.priority_range() if hasattr(torch.cuda.Stream, "priority_range") else (0, -5)
+    stream = torch.cuda.Stream(priority=hi)
+    ctx = torch.cuda.stream(stream)
+    ctx.__enter__()
+    load_all(pinned)  # warm-up (first-touch of staging, thread start)
+    t_pinned = min(load_all(pinned) for _ in range(2))
+    t_pageable = load_all(hosts)
+    # steps alone: enough graph replays to outlast the load
+    step_ms = None
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(3):
+        W.step(stream)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    step_ms = e0.elapsed_time(e1) / 3
+    k = max(8, int(np.ceil(1.5 * t_pinned * 1e3 / step_ms)))
+
+    def steps(n):
+        e0.record(stream)
+        for _ in range(n):
+            W.step(stream)
+        e1.record(stream)
+
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    steps(k)
+    torch.cuda.synchronize()
+    t_steps = time.perf_counter() - t0
+    gpu_steps_alone = e0.elapsed_time(e1)
+    # overlapped: prefetch the set, replay the steps meanwhile
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for i, r, hb in zip(ids, ranks, pinned):
+        pool.adapter_prefetch(i, r, hb)
+    steps(k)
+    for i in ids:
+        pool.adapter_wait(i)
+    torch.cuda.synchronize()
+    t_both = time.perf_counter() - t0
+    gpu_steps_both = e0.elapsed_time(e1)
+    st = pool.loader_stats()
+    for i in ids:
+        pool.adapter_evict(i, stream=stream)
+    pool.close()
+    ctx.__exit__(None, None, None)
+    hidden = 1.0 - (t_both - t_steps) / t_pinned
+    return {"adapters": len(ids), "bytes": int(nbytes), "layers": L,
+            "pinned_GBps": round(nbytes / t_pinned / 1e9, 2), "pinned_ms": round(1e3 * t_pinned, 2),
+            "pageable_GBps": round(nbytes / t_pageable / 1e9, 2), "pageable_ms": round(1e3 * t_pageable, 2),
+            "overlap": {"steps": k, "steps_alone_ms": round(1e3 * t_steps, 2), "both_ms": round(1e3 * t_both, 2),
+                        "hidden_fraction": round(max(0.0, min(1.0, hidden)), 3),
+                        "step_ms_alone": round(gpu_steps_alone / k, 4), "step_ms_while_loading":
+                            round(gpu_steps_both / k, 4)},
+            "loader": {"loads": st["loads"], "direct_loads": st["direct_loads"]},
+            "note": "slora_adapter_prefetch on the library's loader thread and copy stream; pinned = page-locked "
+                    "host_w read by the H2D directly, pageable = numpy packed into pinned staging; a separate "
+                    "pool on the same GPU; steps on a high-priority stream; hidden = 1 - (T_both - T_steps) / T_load"}
 
 
 def run_ablations(stream):

@@ -120,7 +120,8 @@ slora_status slora_fragmentation_report(slora_pool_t pool, slora_frag_report* ou
  *     for layer l in 0..L-1, for proj p in (q,k,v,o): A (h x r, row-major)
  *     then B (r x d, row-major); h = d = hidden.  The library packs its TP
  *     shard into its own pinned staging, copies it H2D and scatters it into
- *     pages on `stream`; host_w may be reused as soon as the call returns.
+ *     pages (the loader pipeline of slora_adapter_prefetch below), and makes
+ *     `stream` wait for it; host_w may be reused as soon as the call returns.
  *     Must be NULL for a bookkeeping-only pool, non-NULL otherwise.
  *   scale: multiplies this adapter's delta (reading R6; 1.0 = the paper).
  *   Errors: INVALID_ARG (rank < 1, bad pointer), INDIVISIBLE (N does not
@@ -135,6 +136,40 @@ slora_status slora_adapter_load(slora_pool_t pool, int64_t adapter_id, int32_t r
  * prepared before the eviction become STALE_HANDLE. */
 slora_status slora_adapter_evict(slora_pool_t pool, int64_t adapter_id, void* stream,
                                  int64_t* released_out);
+/* NEXT-1: asynchronous adapter load ("prefetch": the adapters a
+ * coming batch needs are fetched while the current batch computes).
+ *   Pages and slot are claimed synchronously, with the same checks and errors
+ *   as slora_adapter_load (the pool is unchanged on error); the call then
+ *   returns and the pool's loader thread streams the data: every tensor shard
+ *   is packed into a ring of kLoadChunks pinned staging chunks (16 MB) --
+ *   skipped when host_w is page-locked (cudaHostAlloc / cudaHostRegister) and
+ *   tp_size == 1: the H2D then reads host_w itself -- and each chunk is copied
+ *   H2D and scattered into pages on the pool's own copy stream, so the pack of
+ *   chunk k+1, the H2D of chunk k and the caller's kernels overlap.
+ *   Page reuse is fenced: the copy stream first waits (cudaStreamWaitEvent,
+ *   taken at this call) for every page release still in flight.
+ *   Ownership: host_w must stay valid and unchanged until slora_adapter_wait
+ *   returns, or slora_adapter_query reports loading == 0.
+ *   The adapter may be named in a batch at once: slora_batch_prepare makes
+ *   its stream wait for the load (stream-ordered; the host blocks only until
+ *   the loader has enqueued the adapter's last chunk).  Evicting a loading
+ *   adapter fences its load the same way.  A failed copy surfaces as CUDA on
+ *   wait / query / prepare / evict.  slora_adapter_load is prefetch + that
+ *   fence on its stream (host_w free on return). */
+slora_status slora_adapter_prefetch(slora_pool_t pool, int64_t adapter_id, int32_t rank,
+                                    const void* host_w, float scale, int32_t* slot_out);
+/* Block until the adapter's load completed on the device (NOT_RESIDENT, CUDA). */
+slora_status slora_adapter_wait(slora_pool_t pool, int64_t adapter_id);
+/* loading_out = 1 while the adapter's load is in flight, else 0. */
+slora_status slora_adapter_query(slora_pool_t pool, int64_t adapter_id, int32_t* loading_out);
+typedef struct {
+    int64_t loads;          /* loads the loader thread finished                        */
+    int64_t direct_loads;   /* of which read a page-locked host_w directly (no pack)   */
+    int64_t bytes;          /* host bytes of this rank's shards streamed               */
+    double busy_s;          /* loader-thread wall time spent streaming (host side)     */
+    int64_t queued;         /* loads waiting or in progress now                        */
+} slora_loader_stats;
+slora_status slora_loader_get_stats(slora_pool_t pool, slora_loader_stats* out);
 slora_status slora_adapter_pin(slora_pool_t pool, int64_t adapter_id);   /* NOT_RESIDENT */
 slora_status slora_adapter_unpin(slora_pool_t pool, int64_t adapter_id); /* NOT_RESIDENT, NOT_PINNED */
 /* The adapter's page ids in claim order (n_out = count; copies min(cap, n)). */

@@ -2,8 +2,10 @@
 //
 //   * Unified Paging pool bookkeeping: LIFO free stack, owner
 //     table, KV handles, adapter handles, pin/evict, fragmentation report.
-//   * adapter loader: pack this rank's TP shard into pinned staging,
-//     H2D on the caller's stream, scatter kernel into pages.
+//   * adapter loader: a loader thread per pool packs this
+//     rank's TP shard into a ring of pinned staging chunks (or reads a pinned
+//     host_w directly) and streams it H2D || scatter kernel into pages on the
+//     pool's copy stream, overlapping the caller's kernels (slora_adapter_prefetch).
 //   * batch descriptor builder: group tokens by adapter, pack
 //     (segment x projection) work into balanced units, upload.
 //   * launchers of the sm_100a kernels (kernels.cu).
@@ -16,6 +18,11 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <chrono>
+#include <condition_variable>
+#include <deque>
+#include <memory>
+#include <mutex>
 #include <queue>
 #include <string>
 #include <thread>
@@ -127,8 +134,26 @@ NcclApi& nccl() {
 // -------------------------------------------------------------------- pool
 namespace {
 constexpr int kNumProj = 4;
-constexpr size_t kStageBytes = size_t(32) << 20;   // per staging buffer
-constexpr size_t kJobBytes = size_t(64) << 10;     // job table at the head
+constexpr size_t kStageBytes = size_t(16) << 20;   // per loader staging chunk (pinned host + device)
+constexpr size_t kJobBytes = size_t(64) << 10;     // job table at the head of a chunk
+constexpr int kLoadChunks = 4;                     // staging ring depth (pack || H2D || scatter)
+constexpr size_t kTabBytes = size_t(1) << 20;      // pinned page-table staging per ring entry
+
+// One adapter load in flight (slora_adapter_prefetch / slora_adapter_load).
+struct LoadJob {
+    int64_t id = 0;
+    int32_t rank = 0;
+    const uint8_t* host_w = nullptr;
+    bool direct = false;            // host_w is page-locked and N == 1: H2D straight from it, no pack
+    int32_t* dev_tab = nullptr;     // the adapter's device page table (claim order)
+    int32_t slot = -1;
+    std::vector<int32_t> pages;     // page ids in claim order (uploaded by the loader)
+    cudaEvent_t ready = nullptr;    // copy stream, after the adapter's last scatter kernel
+    // guarded by Loader::mu
+    int state = 0;                  // 0 queued / streaming, 1 host_w consumed and all device work enqueued, 2 failed
+    cudaError_t err = cudaSuccess;
+    int64_t bytes = 0;              // host bytes of the shard this rank copies
+};
 
 enum Owner : uint8_t { kFree = 0, kKv = 1, kAdapter = 2 };
 
@@ -139,6 +164,7 @@ struct Adapter {
     bool pinned = false;
     std::vector<int32_t> pages;  // claim order: layer, proj, tensor, row, chunk
     int32_t* dev_tab = nullptr;
+    std::shared_ptr<LoadJob> load;  // set while the load may still be in flight
 };
 
 struct Kv {
@@ -216,10 +242,25 @@ struct slora_pool {
     uint64_t epoch = 0;               // bumped by every eviction
     // device resources
     int32_t** slot_tab_dev = nullptr;
-    void* stage_host[2] = {nullptr, nullptr};
-    void* stage_dev[2] = {nullptr, nullptr};
-    cudaEvent_t stage_ev[2] = {nullptr, nullptr};
-    bool stage_used[2] = {false, false};
+    // adapter loader: one thread, one copy stream, a ring of staging chunks
+    struct Loader {
+        std::thread th;
+        std::mutex mu;
+        std::condition_variable cv;            // queue and job-state changes
+        std::deque<std::shared_ptr<LoadJob>> q;
+        bool stop = false;
+        cudaStream_t stream = nullptr;
+        void* host[kLoadChunks] = {};          // pinned
+        void* dev[kLoadChunks] = {};
+        cudaEvent_t ev[kLoadChunks] = {};      // chunk free again (its H2D and scatter done)
+        void* tab_host[kLoadChunks] = {};      // pinned page-table staging (slot pointer + page ids)
+        cudaEvent_t tab_ev[kLoadChunks] = {};
+        bool tab_used[kLoadChunks] = {};
+        int tab_next = 0;
+        bool used[kLoadChunks] = {};
+        int next = 0;                          // loader thread only
+        slora_loader_stats stats{};            // guarded by mu
+    } ld;
     // page releases (kv_free, adapter_evict) are stream-ordered: one event per
     // release, and a load waits for every release still in flight (any stream)
     std::vector<cudaEvent_t> release_evs, spare_evs;
@@ -248,6 +289,7 @@ struct slora_pool {
     int64_t tp_cap = 0;                // NR the buffers hold
     slora_tp_stats tp_stats{};
 
+    ~slora_pool();
     int64_t free_pages() const { return int64_t(free_stack.size()); }
     int N() const { return cfg.tp_size; }
     // (stored rows, chunks per row) of one tensor shard (reading R3/R4)
@@ -300,6 +342,8 @@ struct slora_batch {
 };
 
 static void batch_free_device(slora_batch* b);
+static cudaError_t loader_start(slora_pool* p);
+static void loader_stop(slora_pool* p);
 
 static void tp_release(slora_pool* p) {
     if (p->tp_comm && nccl().ok) nccl().CommDestroy(p->tp_comm);
@@ -366,13 +410,7 @@ extern "C" slora_status slora_pool_create(const slora_pool_config* cfg, slora_po
             return cleanup(e, "cudaMalloc slot table");
         if ((e = cudaMemset(p->slot_tab_dev, 0, sizeof(int32_t*) * size_t(cfg->max_adapters))))
             return cleanup(e, "cudaMemset");
-        for (int b = 0; b < 2; ++b) {
-            if ((e = cudaHostAlloc(&p->stage_host[b], kStageBytes, cudaHostAllocDefault)))
-                return cleanup(e, "cudaHostAlloc staging");
-            if ((e = cudaMalloc(&p->stage_dev[b], kStageBytes))) return cleanup(e, "cudaMalloc staging");
-            if ((e = cudaEventCreateWithFlags(&p->stage_ev[b], cudaEventDisableTiming)))
-                return cleanup(e, "cudaEventCreate");
-        }
+        if ((e = loader_start(p))) return cleanup(e, "adapter loader");
         const int dt = cfg->dtype == SLORA_F32 ? kF32 : (cfg->dtype == SLORA_F16 ? kF16 : kBF16);
         const int64_t H = cfg->hidden;
         p->kcfg[0] = make_kernel_cfg(kFused, H, H, P, es, dt);
@@ -404,15 +442,11 @@ extern "C" slora_status slora_pool_destroy(slora_pool_t p) {
     if (!p) return fail(SLORA_ERR_INVALID_ARG, "null pool");
     if (p->dev) {
         cudaSetDevice(p->cfg.device);
+        loader_stop(p);  // finishes the queued loads
         cudaDeviceSynchronize();
         for (auto& kvp : p->adapters)
             if (kvp.second.dev_tab) cudaFree(kvp.second.dev_tab);
         cudaFree(p->slot_tab_dev);
-        for (int b = 0; b < 2; ++b) {
-            cudaFreeHost(p->stage_host[b]);
-            cudaFree(p->stage_dev[b]);
-            cudaEventDestroy(p->stage_ev[b]);
-        }
         for (cudaEvent_t ev : p->release_evs) cudaEventDestroy(ev);
         for (cudaEvent_t ev : p->spare_evs) cudaEventDestroy(ev);
         if (p->sync_dev) cudaFree(p->sync_dev);
@@ -633,9 +667,218 @@ static void pack_shard(const slora_pool* p, const uint8_t* A, const uint8_t* B, 
     }
 }
 
-extern "C" slora_status slora_adapter_load(slora_pool_t p, int64_t id, int32_t rank, const void* host_w,
-                                           float scale, void* stream, int32_t* slot_out) {
-    if (check_pool(p)) return SLORA_ERR_INVALID_ARG;
+// ---------------------------------------------------------- adapter loader
+// ("prefetching ... overlapping the loading of adapters with
+// the computation").  One thread per pool streams queued loads in order:
+// every (layer, proj, A/B) shard of the adapter goes into the current staging
+// chunk of a kLoadChunks ring; a full chunk is flushed as
+//   pack (host threads, pageable host_w -> pinned chunk; skipped when host_w is
+//   page-locked and N == 1: the H2D reads host_w itself)
+//   -> cudaMemcpyAsync H2D -> scatter kernel (pages) -> chunk event
+// on the pool's copy stream, so the pack of chunk k+1 overlaps the H2D and
+// scatter of chunk k, and the caller's kernels run meanwhile.  A chunk is
+// re-packed only after its event completed.
+static double now_s() {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+static cudaError_t run_load(slora_pool* p, LoadJob& jb) {
+    auto& L = p->ld;
+    const int64_t H = p->cfg.hidden;
+    const int es = p->es;
+    const int64_t per_lp = (H * jb.rank + int64_t(jb.rank) * H);  // elements of A+B per (layer, proj)
+    size_t used = kJobBytes;
+    std::vector<ScatterJob> jobs;
+    std::vector<CopySeg> segs;
+    cudaError_t e = cudaSuccess;
+    int k = L.next;
+    auto acquire = [&]() -> cudaError_t {  // chunk k's previous flush is done (host buffer reusable)
+        if (!L.used[k]) return cudaSuccess;
+        L.used[k] = false;
+        return cudaEventSynchronize(L.ev[k]);
+    };
+    auto flush = [&]() -> cudaError_t {
+        if (jobs.empty()) return cudaSuccess;
+        uint8_t* hb = static_cast<uint8_t*>(L.host[k]);
+        uint8_t* db = static_cast<uint8_t*>(L.dev[k]);
+        cudaError_t e2 = cudaSuccess;
+        memcpy(hb, jobs.data(), jobs.size() * sizeof(ScatterJob));
+        if (jb.direct) {
+            e2 = cudaMemcpyAsync(db, hb, jobs.size() * sizeof(ScatterJob), cudaMemcpyHostToDevice, L.stream);
+            // consecutive shards are contiguous in host_w and in the chunk: one H2D per run
+            for (size_t a = 0; a < segs.size() && !e2;) {
+                size_t b2 = a + 1, n = segs[a].bytes;
+                while (b2 < segs.size() && segs[b2].src == segs[a].src + n && segs[b2].dst == segs[a].dst + n)
+                    n += segs[b2++].bytes;
+                e2 = cudaMemcpyAsync(db + (segs[a].dst - hb), segs[a].src, n, cudaMemcpyHostToDevice, L.stream);
+                a = b2;
+            }
+            segs.clear();
+        } else {
+            copy_segments(segs);
+            e2 = cudaMemcpyAsync(db, hb, used, cudaMemcpyHostToDevice, L.stream);
+        }
+        if (!e2) e2 = launch_scatter(db + kJobBytes, reinterpret_cast<const ScatterJob*>(db), int(jobs.size()),
+                                     p->cfg.device_buffer, p->P, es, L.stream);
+        if (!e2) e2 = cudaEventRecord(L.ev[k], L.stream);
+        L.used[k] = true;
+        k = (k + 1) % kLoadChunks;
+        used = kJobBytes;
+        jobs.clear();
+        return e2;
+    };
+    {  // page table, then the slot's table pointer, from pinned staging (never a pageable copy:
+       // that would drain the copy stream)
+        const int tk = L.tab_next;
+        L.tab_next = (tk + 1) % kLoadChunks;
+        if (L.tab_used[tk] && (e = cudaEventSynchronize(L.tab_ev[tk]))) return e;
+        uint8_t* th = static_cast<uint8_t*>(L.tab_host[tk]);
+        memcpy(th, &jb.dev_tab, sizeof(int32_t*));
+        memcpy(th + 16, jb.pages.data(), jb.pages.size() * sizeof(int32_t));
+        e = cudaMemcpyAsync(jb.dev_tab, th + 16, jb.pages.size() * sizeof(int32_t), cudaMemcpyHostToDevice, L.stream);
+        if (!e) e = cudaMemcpyAsync(p->slot_tab_dev + jb.slot, th, sizeof(int32_t*), cudaMemcpyHostToDevice, L.stream);
+        if (!e) e = cudaEventRecord(L.tab_ev[tk], L.stream);
+        L.tab_used[tk] = true;
+        if (e) return e;
+    }
+    int64_t page_cursor = 0;
+    for (int l = 0; l < p->cfg.num_layers && !e; ++l)
+        for (int pr = 0; pr < kNumProj && !e; ++pr) {
+            const uint8_t* A = jb.host_w + size_t((int64_t(l) * kNumProj + pr) * per_lp) * es;
+            const uint8_t* B = A + size_t(H * jb.rank) * es;
+            for (int t = 0; t < 2 && !e; ++t) {
+                int rows_s, chunks;
+                p->tensor_shape(pr, t, jb.rank, rows_s, chunks);
+                const size_t bytes = size_t(rows_s) * chunks * size_t(p->P) * es;
+                if (used + bytes > kStageBytes || (jobs.size() + 1) * sizeof(ScatterJob) > kJobBytes) {
+                    if ((e = flush())) break;
+                }
+                if (jobs.empty() && (e = acquire())) break;
+                int rows, cols;
+                pack_shard(p, A, B, pr, t, jb.rank, static_cast<uint8_t*>(L.host[k]) + used, rows, cols, segs);
+                ScatterJob sj;
+                sj.src_off = int64_t((used - kJobBytes) / size_t(es));
+                sj.pages = jb.dev_tab + page_cursor;
+                sj.kind = t;
+                sj.rows = rows;
+                sj.cols = cols;
+                sj.row_pages = (t == 0) ? chunks : 1;
+                jobs.push_back(sj);
+                used += bytes;
+                jb.bytes += int64_t(bytes);
+                page_cursor += int64_t(rows_s) * chunks;
+            }
+        }
+    if (!e) e = flush();
+    // host_w is consumed once its last chunk is packed (or, read directly, once its H2D completed)
+    if (!e && jb.direct) e = cudaEventSynchronize(L.ev[(k + kLoadChunks - 1) % kLoadChunks]);
+    if (!e) e = cudaEventRecord(jb.ready, L.stream);
+    L.next = k;
+    return e;
+}
+
+static void loader_main(slora_pool* p) {
+    auto& L = p->ld;
+    cudaSetDevice(p->cfg.device);
+    for (;;) {
+        std::shared_ptr<LoadJob> jb;
+        {
+            std::unique_lock<std::mutex> lk(L.mu);
+            L.cv.wait(lk, [&] { return L.stop || !L.q.empty(); });
+            if (L.q.empty()) return;  // stop requested, queue drained
+            jb = L.q.front();
+        }
+        const double t0 = now_s();
+        cudaError_t e = run_load(p, *jb);
+        const double t1 = now_s();
+        {
+            std::lock_guard<std::mutex> lk(L.mu);
+            jb->err = e;
+            jb->state = e ? 2 : 1;
+            L.q.pop_front();
+            L.stats.loads += 1;
+            L.stats.bytes += jb->bytes;
+            L.stats.direct_loads += jb->direct ? 1 : 0;
+            L.stats.busy_s += t1 - t0;
+        }
+        L.cv.notify_all();
+    }
+}
+
+static cudaError_t loader_start(slora_pool* p) {
+    auto& L = p->ld;
+    // the copy stream runs at the lowest priority: the LoRA kernels' CTAs go first
+    int least = 0, greatest = 0;
+    cudaDeviceGetStreamPriorityRange(&least, &greatest);
+    cudaError_t e = cudaStreamCreateWithPriority(&L.stream, cudaStreamNonBlocking, least);
+    for (int k = 0; k < kLoadChunks && !e; ++k) {
+        if (!e) e = cudaHostAlloc(&L.host[k], kStageBytes, cudaHostAllocDefault);
+        if (!e) e = cudaMalloc(&L.dev[k], kStageBytes);
+        if (!e) e = cudaEventCreateWithFlags(&L.ev[k], cudaEventDisableTiming);
+        if (!e) e = cudaHostAlloc(&L.tab_host[k], kTabBytes, cudaHostAllocDefault);
+        if (!e) e = cudaEventCreateWithFlags(&L.tab_ev[k], cudaEventDisableTiming);
+    }
+    if (e) return e;
+    L.th = std::thread(loader_main, p);
+    return cudaSuccess;
+}
+
+static void loader_stop(slora_pool* p) {
+    auto& L = p->ld;
+    if (L.th.joinable()) {
+        {
+            std::lock_guard<std::mutex> lk(L.mu);
+            L.stop = true;
+        }
+        L.cv.notify_all();
+        L.th.join();
+    }
+    if (L.stream) cudaStreamSynchronize(L.stream);
+    for (int k = 0; k < kLoadChunks; ++k) {
+        if (L.host[k]) cudaFreeHost(L.host[k]);
+        if (L.dev[k]) cudaFree(L.dev[k]);
+        if (L.ev[k]) cudaEventDestroy(L.ev[k]);
+        if (L.tab_host[k]) cudaFreeHost(L.tab_host[k]);
+        if (L.tab_ev[k]) cudaEventDestroy(L.tab_ev[k]);
+        L.host[k] = L.dev[k] = L.tab_host[k] = nullptr;
+        L.ev[k] = L.tab_ev[k] = nullptr;
+    }
+    if (L.stream) cudaStreamDestroy(L.stream);
+    L.stream = nullptr;
+}
+
+slora_pool::~slora_pool() { loader_stop(this); }
+
+// Block until the adapter's load reached `state` >= want (1: host_w consumed and
+// all its device work enqueued); surfaces a failed load.
+static slora_status load_wait_host(slora_pool* p, Adapter& ad) {
+    if (!ad.load) return SLORA_OK;
+    auto& L = p->ld;
+    std::unique_lock<std::mutex> lk(L.mu);
+    L.cv.wait(lk, [&] { return ad.load->state != 0; });
+    if (ad.load->state == 2)
+        return fail(SLORA_ERR_CUDA, "adapter %lld load: %s", (long long)ad.id, cudaGetErrorString(ad.load->err));
+    return SLORA_OK;
+}
+// Make `stream` wait for the adapter's load (stream-ordered); drop the job once complete.
+static slora_status load_fence(slora_pool* p, Adapter& ad, cudaStream_t stream) {
+    if (!ad.load) return SLORA_OK;
+    if (slora_status st = load_wait_host(p, ad)) return st;
+    if (cudaEventQuery(ad.load->ready) == cudaSuccess) {
+        cudaEventDestroy(ad.load->ready);
+        ad.load.reset();
+        return SLORA_OK;
+    }
+    cudaGetLastError();  // cudaErrorNotReady
+    if (cudaError_t e = cudaStreamWaitEvent(stream, ad.load->ready, 0))
+        return fail(SLORA_ERR_CUDA, "adapter load fence: %s", cudaGetErrorString(e));
+    return SLORA_OK;
+}
+
+// Claim pages and slot (synchronous, leaves the pool unchanged on error), upload
+// the page table on the copy stream and queue the data load.
+static slora_status adapter_begin(slora_pool* p, int64_t id, int32_t rank, const void* host_w, float scale,
+                                  int32_t* slot_out) {
     if (rank < 1) return fail(SLORA_ERR_INVALID_ARG, "rank < 1");
     if (rank > kMaxRank) return fail(SLORA_ERR_SHAPE, "rank %d > %d (max rank of the MBGMV path)", rank, kMaxRank);
     if (rank % p->N()) return fail(SLORA_ERR_INDIVISIBLE, "rank %d %% tp_size %d", rank, p->N());
@@ -652,6 +895,8 @@ extern "C" slora_status slora_adapter_load(slora_pool_t p, int64_t id, int32_t r
     const size_t tensor_max_bytes = size_t(std::max<int64_t>(H * rank, int64_t(rank) * p->P)) * es;
     if (p->dev && tensor_max_bytes + kJobBytes > kStageBytes)
         return fail(SLORA_ERR_SHAPE, "adapter tensor of %zu bytes exceeds staging", tensor_max_bytes);
+    if (p->dev && size_t(need) * sizeof(int32_t) + 16 > kTabBytes)
+        return fail(SLORA_ERR_SHAPE, "adapter page table of %lld pages exceeds staging", (long long)need);
 
     Adapter ad;
     ad.id = id;
@@ -665,93 +910,107 @@ extern "C" slora_status slora_adapter_load(slora_pool_t p, int64_t id, int32_t r
         p->owner[size_t(pg)] = kAdapter;
         ad.pages.push_back(pg);
     }
-    auto rollback = [&]() {
-        for (auto it = ad.pages.rbegin(); it != ad.pages.rend(); ++it) {
-            p->owner[size_t(*it)] = kFree;
-            p->free_stack.push_back(*it);
-        }
-    };
-
     if (p->dev) {
-        cudaStream_t s = static_cast<cudaStream_t>(stream);
+        auto& L = p->ld;
+        auto jb = std::make_shared<LoadJob>();
+        jb->id = id;
+        jb->rank = rank;
+        jb->host_w = static_cast<const uint8_t*>(host_w);
+        cudaPointerAttributes at{};
+        if (p->N() == 1 && cudaPointerGetAttributes(&at, host_w) == cudaSuccess && at.type == cudaMemoryTypeHost)
+            jb->direct = true;  // page-locked: no pack, the H2D reads host_w
+        cudaGetLastError();
         cudaError_t e = cudaSetDevice(p->cfg.device);
-        if (!e) e = wait_releases(p, s);
-        if (!e) e = cudaMallocAsync(reinterpret_cast<void**>(&ad.dev_tab), sizeof(int32_t) * size_t(need), s);
-        if (!e) e = cudaMemcpyAsync(ad.dev_tab, ad.pages.data(), sizeof(int32_t) * size_t(need),
-                                    cudaMemcpyHostToDevice, s);
-        if (!e) e = cudaMemcpyAsync(p->slot_tab_dev + ad.slot, &ad.dev_tab, sizeof(int32_t*),
-                                    cudaMemcpyHostToDevice, s);
-        // stream the tensors through the two staging buffers
-        const uint8_t* W = static_cast<const uint8_t*>(host_w);
-        const int64_t per_lp = (H * rank + int64_t(rank) * H);  // elements of A+B per (layer, proj)
-        int buf = 0;
-        size_t used = kJobBytes;
-        std::vector<ScatterJob> jobs;
-        std::vector<CopySeg> segs;
-        auto flush = [&]() -> cudaError_t {
-            if (jobs.empty()) return cudaSuccess;
-            copy_segments(segs);
-            memcpy(p->stage_host[buf], jobs.data(), jobs.size() * sizeof(ScatterJob));
-            cudaError_t e2 = cudaMemcpyAsync(p->stage_dev[buf], p->stage_host[buf], used, cudaMemcpyHostToDevice, s);
-            if (!e2) e2 = launch_scatter(static_cast<uint8_t*>(p->stage_dev[buf]) + kJobBytes,
-                                         static_cast<const ScatterJob*>(p->stage_dev[buf]), int(jobs.size()),
-                                         p->cfg.device_buffer, p->P, es, s);
-            if (!e2) e2 = cudaEventRecord(p->stage_ev[buf], s);
-            p->stage_used[buf] = true;
-            buf ^= 1;
-            used = kJobBytes;
-            jobs.clear();
-            return e2;
-        };
-        int64_t page_cursor = 0;
-        for (int l = 0; l < p->cfg.num_layers && !e; ++l)
-            for (int pr = 0; pr < kNumProj && !e; ++pr) {
-                const uint8_t* A = W + size_t((int64_t(l) * kNumProj + pr) * per_lp) * es;
-                const uint8_t* B = A + size_t(H * rank) * es;
-                for (int t = 0; t < 2 && !e; ++t) {
-                    int rows_s, chunks;
-                    p->tensor_shape(pr, t, rank, rows_s, chunks);
-                    const size_t bytes = size_t(rows_s) * chunks * size_t(p->P) * es;
-                    if (used + bytes > kStageBytes || (jobs.size() + 1) * sizeof(ScatterJob) > kJobBytes) {
-                        e = flush();
-                        if (e) break;
-                    }
-                    if (jobs.empty() && p->stage_used[buf]) {
-                        e = cudaEventSynchronize(p->stage_ev[buf]);  // staging buffer free again
-                        if (e) break;
-                    }
-                    int rows, cols;
-                    pack_shard(p, A, B, pr, t, rank, static_cast<uint8_t*>(p->stage_host[buf]) + used, rows, cols,
-                               segs);
-                    ScatterJob jb;
-                    jb.src_off = int64_t((used - kJobBytes) / size_t(es));
-                    jb.pages = ad.dev_tab + page_cursor;
-                    jb.kind = t;
-                    jb.rows = rows;
-                    jb.cols = cols;
-                    jb.row_pages = (t == 0) ? chunks : 1;
-                    jobs.push_back(jb);
-                    used += bytes;
-                    page_cursor += int64_t(rows_s) * chunks;
-                }
-            }
-        if (!e) e = flush();
+        // page reuse fence, taken now: released pages may still be read by queued kernels
+        if (!e) e = wait_releases(p, L.stream);
+        if (!e) e = cudaEventCreateWithFlags(&jb->ready, cudaEventDisableTiming);
+        if (!e) e = cudaMallocAsync(reinterpret_cast<void**>(&ad.dev_tab), sizeof(int32_t) * size_t(need), L.stream);
         if (e) {
-            // scatter kernels of earlier flushes may still write into the pages: let them finish
-            // before the pages return to the free stack; drop the slot's page table
-            cudaStreamSynchronize(s);
-            cudaGetLastError();
-            const int32_t* none = nullptr;
-            cudaMemcpy(p->slot_tab_dev + ad.slot, &none, sizeof(none), cudaMemcpyHostToDevice);
+            if (jb->ready) cudaEventDestroy(jb->ready);
             if (ad.dev_tab) cudaFree(ad.dev_tab);
-            rollback();
+            for (auto it = ad.pages.rbegin(); it != ad.pages.rend(); ++it) {
+                p->owner[size_t(*it)] = kFree;
+                p->free_stack.push_back(*it);
+            }
             return fail(SLORA_ERR_CUDA, "adapter load: %s", cudaGetErrorString(e));
         }
+        jb->dev_tab = ad.dev_tab;
+        jb->slot = ad.slot;
+        jb->pages = ad.pages;  // the loader uploads the page table (pinned copy) ahead of the data
+        ad.load = jb;
+        {
+            std::lock_guard<std::mutex> lk(L.mu);
+            L.q.push_back(jb);
+        }
+        L.cv.notify_all();
     }
     p->adapter_pages += need;
     p->slots[size_t(ad.slot)] = id;
     if (slot_out) *slot_out = ad.slot;
     p->adapters.emplace(id, std::move(ad));
+    return SLORA_OK;
+}
+
+extern "C" slora_status slora_adapter_prefetch(slora_pool_t p, int64_t id, int32_t rank, const void* host_w,
+                                               float scale, int32_t* slot_out) {
+    if (check_pool(p)) return SLORA_ERR_INVALID_ARG;
+    if (slora_status st = adapter_begin(p, id, rank, host_w, scale, slot_out)) return st;
+    return ok();
+}
+
+extern "C" slora_status slora_adapter_load(slora_pool_t p, int64_t id, int32_t rank, const void* host_w,
+                                           float scale, void* stream, int32_t* slot_out) {
+    if (check_pool(p)) return SLORA_ERR_INVALID_ARG;
+    if (slora_status st = adapter_begin(p, id, rank, host_w, scale, slot_out)) return st;
+    if (!p->dev) return ok();
+    // host_w is free on return; completion is stream-ordered on `stream`
+    Adapter& ad = p->adapters.at(id);
+    if (slora_status st = load_fence(p, ad, static_cast<cudaStream_t>(stream))) return st;
+    return ok();
+}
+
+extern "C" slora_status slora_adapter_wait(slora_pool_t p, int64_t id) {
+    if (check_pool(p)) return SLORA_ERR_INVALID_ARG;
+    auto it = p->adapters.find(id);
+    if (it == p->adapters.end()) return fail(SLORA_ERR_NOT_RESIDENT, "adapter %lld", (long long)id);
+    Adapter& ad = it->second;
+    if (!ad.load) return ok();
+    if (slora_status st = load_wait_host(p, ad)) return st;
+    if (cudaError_t e = cudaEventSynchronize(ad.load->ready))
+        return fail(SLORA_ERR_CUDA, "adapter %lld load: %s", (long long)id, cudaGetErrorString(e));
+    cudaEventDestroy(ad.load->ready);
+    ad.load.reset();
+    return ok();
+}
+
+extern "C" slora_status slora_adapter_query(slora_pool_t p, int64_t id, int32_t* loading) {
+    if (check_pool(p) || !loading) return fail(SLORA_ERR_INVALID_ARG, "null argument");
+    auto it = p->adapters.find(id);
+    if (it == p->adapters.end()) return fail(SLORA_ERR_NOT_RESIDENT, "adapter %lld", (long long)id);
+    Adapter& ad = it->second;
+    *loading = 0;
+    if (!ad.load) return ok();
+    int st;
+    {
+        std::lock_guard<std::mutex> lk(p->ld.mu);
+        st = ad.load->state;
+    }
+    if (st == 2) return fail(SLORA_ERR_CUDA, "adapter %lld load: %s", (long long)id, cudaGetErrorString(ad.load->err));
+    if (st == 1 && cudaEventQuery(ad.load->ready) == cudaSuccess) {
+        cudaEventDestroy(ad.load->ready);
+        ad.load.reset();
+        return ok();
+    }
+    cudaGetLastError();
+    *loading = 1;
+    return ok();
+}
+
+extern "C" slora_status slora_loader_get_stats(slora_pool_t p, slora_loader_stats* out) {
+    if (check_pool(p) || !out) return fail(SLORA_ERR_INVALID_ARG, "null argument");
+    std::lock_guard<std::mutex> lk(p->ld.mu);
+    *out = p->ld.stats;
+    out->queued = int64_t(p->ld.q.size());
     return ok();
 }
 
@@ -761,6 +1020,9 @@ extern "C" slora_status slora_adapter_evict(slora_pool_t p, int64_t id, void* st
     if (it == p->adapters.end()) return fail(SLORA_ERR_NOT_RESIDENT, "adapter %lld", (long long)id);
     if (it->second.pinned) return fail(SLORA_ERR_PINNED, "adapter %lld", (long long)id);
     Adapter& ad = it->second;
+    // a load still in flight: its scatters must land before the pages can be reused
+    if (slora_status st = load_fence(p, ad, static_cast<cudaStream_t>(stream))) return st;
+    if (ad.load) cudaEventDestroy(ad.load->ready);  // still pending: destruction is deferred by CUDA
     for (int32_t pg : ad.pages) {
         p->owner[size_t(pg)] = kFree;
         p->free_stack.push_back(pg);
@@ -1082,6 +1344,9 @@ extern "C" slora_status slora_batch_prepare(slora_batch_t b, const int64_t* tok_
         }
         toks[size_t(s)].push_back(i);
     }
+    // adapters still loading (slora_adapter_prefetch): the batch's stream waits for them
+    for (int64_t a : seg_ad)
+        if (slora_status st = load_fence(p, p->adapters.at(a), static_cast<cudaStream_t>(stream))) return st;
     b->segs.clear();
     b->seg_tab.clear();
     b->tok_idx.clear();

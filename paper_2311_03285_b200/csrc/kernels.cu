@@ -1370,25 +1370,57 @@ cudaError_t configure_lora_kernels(int /*device*/) {
 // dense shard (its stored rank columns) into position k of each column page
 // -> reads and writes are both coalesced across threads.  B jobs: plain row
 // copies.
+// It runs beside the LoRA kernels while adapters load (slora_adapter_prefetch), so its CTAs are
+// small and short-lived: <= 32 registers x 256 threads (they fit on an SM next to a persistent
+// LoRA CTA) and one (job, part) each.
 template <typename T>
-__global__ void scatter_kernel(const T* __restrict__ staging, const ScatterJob* __restrict__ jobs, T* pool,
-                               int64_t P) {
-    const ScatterJob jb = jobs[blockIdx.y];
-    const T* src = staging + jb.src_off;
-    if (jb.kind == 0) {
-        for (int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < jb.rows;
-             k += int64_t(gridDim.x) * blockDim.x) {
-            const int64_t chunk = k / P, off = k % P;
-            for (int j = 0; j < jb.cols; ++j) {
-                const int32_t page = jb.pages[j * jb.row_pages + chunk];
-                pool[page * P + off] = src[k * jb.cols + j];
+__global__ void __launch_bounds__(256, 8) scatter_kernel(const T* __restrict__ staging,
+                                                         const ScatterJob* __restrict__ jobs, int n_jobs, T* pool,
+                                                         int64_t P) {
+    constexpr int VE = 16 / int(sizeof(T));
+    {
+        const int q = blockIdx.y;
+        const ScatterJob jb = jobs[q];
+        const T* src = staging + jb.src_off;
+        if (jb.kind == 0) {
+            // A: input row k (cols stored rank columns, contiguous) -> position k%P of column page j
+            const bool vec = (jb.cols % VE) == 0 && (jb.src_off % VE) == 0;
+            for (int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < jb.rows;
+                 k += int64_t(gridDim.x) * blockDim.x) {
+                const int64_t chunk = k / P, off = k % P;
+                const T* row = src + k * jb.cols;
+                if (vec) {
+                    for (int j0 = 0; j0 < jb.cols; j0 += VE) {
+                        const uint4 u = *reinterpret_cast<const uint4*>(row + j0);
+                        const T* e = reinterpret_cast<const T*>(&u);
+#pragma unroll
+                        for (int t = 0; t < VE; ++t)
+                            pool[int64_t(jb.pages[(j0 + t) * jb.row_pages + chunk]) * P + off] = e[t];
+                    }
+                } else {
+                    for (int j = 0; j < jb.cols; ++j)
+                        pool[int64_t(jb.pages[j * jb.row_pages + chunk]) * P + off] = row[j];
+                }
             }
-        }
-    } else {
-        const int64_t n = int64_t(jb.rows) * jb.cols;
-        for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
-            const int64_t j = i / jb.cols, e = i % jb.cols;
-            pool[int64_t(jb.pages[j]) * P + e] = src[i];
+        } else {
+            // B: row j (cols = P elements) -> page j, 16-byte vectors
+            const int64_t nv = jb.cols / VE;
+            const bool vec = (jb.cols % VE) == 0 && (jb.src_off % VE) == 0 && (P % VE) == 0;
+            if (vec) {
+                for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < int64_t(jb.rows) * nv;
+                     i += int64_t(gridDim.x) * blockDim.x) {
+                    const int64_t j = i / nv, e = i % nv;
+                    reinterpret_cast<uint4*>(pool + int64_t(jb.pages[j]) * P)[e] =
+                        reinterpret_cast<const uint4*>(src + j * jb.cols)[e];
+                }
+            } else {
+                const int64_t n = int64_t(jb.rows) * jb.cols;
+                for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+                     i += int64_t(gridDim.x) * blockDim.x) {
+                    const int64_t j = i / jb.cols, e = i % jb.cols;
+                    pool[int64_t(jb.pages[j]) * P + e] = src[i];
+                }
+            }
         }
     }
 }
@@ -1396,13 +1428,13 @@ __global__ void scatter_kernel(const T* __restrict__ staging, const ScatterJob* 
 cudaError_t launch_scatter(const void* staging, const ScatterJob* jobs_dev, int n_jobs, void* pool,
                            int64_t page_elems, int esize, cudaStream_t s) {
     if (n_jobs == 0) return cudaSuccess;
-    dim3 grid(8, unsigned(n_jobs));
+    const dim3 grid(4, unsigned(n_jobs));
     count_launch();
     if (esize == 4)
-        scatter_kernel<uint32_t><<<grid, 256, 0, s>>>(static_cast<const uint32_t*>(staging), jobs_dev,
+        scatter_kernel<uint32_t><<<grid, 256, 0, s>>>(static_cast<const uint32_t*>(staging), jobs_dev, n_jobs,
                                                       static_cast<uint32_t*>(pool), page_elems);
     else
-        scatter_kernel<uint16_t><<<grid, 256, 0, s>>>(static_cast<const uint16_t*>(staging), jobs_dev,
+        scatter_kernel<uint16_t><<<grid, 256, 0, s>>>(static_cast<const uint16_t*>(staging), jobs_dev, n_jobs,
                                                       static_cast<uint16_t*>(pool), page_elems);
     return cudaGetLastError();
 }

@@ -58,6 +58,11 @@ class BatchInfo(ctypes.Structure):
                 ("mbgmm_segments", ctypes.c_int32)]
 
 
+class LoaderStats(ctypes.Structure):
+    _fields_ = [("loads", ctypes.c_int64), ("direct_loads", ctypes.c_int64), ("bytes", ctypes.c_int64),
+                ("busy_s", ctypes.c_double), ("queued", ctypes.c_int64)]
+
+
 class TPStats(ctypes.Structure):
     _fields_ = [("allgather_calls", ctypes.c_int64), ("allgather_send_elems", ctypes.c_int64),
                 ("allgather_recv_elems", ctypes.c_int64), ("allreduce_calls", ctypes.c_int64),
@@ -99,6 +104,10 @@ SIGNATURES = {
     "slora_tp_lora_qkv": [_VP, _VP, _I32, _VP, _I64, ctypes.POINTER(_VP), _PI64, _VP],
     "slora_tp_lora_o": [_VP, _VP, _I32, _VP, _I64, _VP, _I64, _VP],
     "slora_tp_get_stats": [_VP, ctypes.POINTER(TPStats)],
+    "slora_adapter_prefetch": [_VP, _I64, _I32, _VP, ctypes.c_float, ctypes.POINTER(_I32)],
+    "slora_adapter_wait": [_VP, _I64],
+    "slora_adapter_query": [_VP, _I64, ctypes.POINTER(_I32)],
+    "slora_loader_get_stats": [_VP, ctypes.POINTER(LoaderStats)],
     "slora_sync": [_VP, _VP],
     "slora_debug_trace": [_VP, _PI64, _I32],
 }
@@ -192,6 +201,7 @@ class Pool:
                          _ptr(self.buffer) or None, nbytes, max_adapters,
                          {"ascending": 0, "shuffle": 1}[order], seed)
         h = _VP()
+        self._inflight, self._retired = {}, []
         _check(lib().slora_pool_create(ctypes.byref(cfg), ctypes.byref(h)))
         self.h = h
 
@@ -207,32 +217,78 @@ class Pool:
             pass
 
     # ----------------------------------------------------------------- a2
-    def adapter_load(self, adapter_id: int, rank: int, host_w: np.ndarray | None = None,
+    def _host_ptr(self, host_w, rank: int):
+        """(pointer, kept object) of a host adapter buffer: a numpy array, or a CPU torch tensor
+        (pinned tensors are read directly by the loader).  Checks dtype and size."""
+        if host_w is None:
+            return None, None
+        want_item = ESIZE[self.dtype]
+        need = self.num_layers * 4 * 2 * self.hidden * rank * want_item
+        if hasattr(host_w, "data_ptr"):  # torch CPU tensor
+            import torch
+            ok = {"f32": (torch.float32,), "f16": (torch.float16,),
+                  "bf16": (torch.bfloat16, torch.int16, torch.uint16)}[self.dtype]
+            if host_w.device.type != "cpu" or not host_w.is_contiguous():
+                raise ValueError("host_w must be a contiguous CPU tensor")
+            if host_w.dtype not in ok:
+                raise ValueError(f"host_w dtype {host_w.dtype} does not match the pool dtype {self.dtype}")
+            if host_w.numel() * host_w.element_size() != need:
+                raise ValueError(f"host_w holds {host_w.numel() * host_w.element_size()} bytes, "
+                                 f"the canonical layout needs {need}")
+            return int(host_w.data_ptr()), host_w
+        host_w = np.ascontiguousarray(host_w)
+        # the library reads exactly this many bytes of the pool's element type from the pointer
+        kind_ok = (host_w.dtype == np.float32 if self.dtype == "f32" else
+                   host_w.dtype == np.float16 if self.dtype == "f16" else
+                   host_w.dtype in (np.uint16, np.int16))
+        if self.device < 0:
+            pass  # bookkeeping-only pool: the library refuses host weights (NO_DEVICE)
+        elif not kind_ok or host_w.itemsize != want_item:
+            raise ValueError(f"host_w dtype {host_w.dtype} does not match the pool dtype {self.dtype}")
+        elif host_w.nbytes != need:
+            raise ValueError(f"host_w holds {host_w.nbytes} bytes, the canonical layout needs {need}")
+        return host_w.ctypes.data, host_w
+
+    def adapter_load(self, adapter_id: int, rank: int, host_w=None,
                      scale: float = 1.0, stream=None) -> int:
         slot = ctypes.c_int32(-1)
-        ptr = None
-        if host_w is not None:
-            host_w = np.ascontiguousarray(host_w)
-            # the library reads exactly this many bytes of the pool's element type from the pointer
-            want_item = ESIZE[self.dtype]
-            kind_ok = (host_w.dtype == np.float32 if self.dtype == "f32" else
-                       host_w.dtype == np.float16 if self.dtype == "f16" else
-                       host_w.dtype in (np.uint16, np.int16))
-            need = self.num_layers * 4 * 2 * self.hidden * rank * want_item
-            if self.device < 0:
-                pass  # bookkeeping-only pool: the library refuses host weights (NO_DEVICE)
-            elif not kind_ok or host_w.itemsize != want_item:
-                raise ValueError(f"host_w dtype {host_w.dtype} does not match the pool dtype {self.dtype}")
-            elif host_w.nbytes != need:
-                raise ValueError(f"host_w holds {host_w.nbytes} bytes, the canonical layout needs {need}")
-            ptr = host_w.ctypes.data
+        ptr, _keep = self._host_ptr(host_w, rank)
         _check(lib().slora_adapter_load(self.h, adapter_id, rank, ptr, scale, _stream(stream),
                                         ctypes.byref(slot)))
         return slot.value
 
+    # ------------------------------------------------------------- NEXT-1
+    def adapter_prefetch(self, adapter_id: int, rank: int, host_w, scale: float = 1.0) -> int:
+        """Asynchronous load on the pool's loader thread and copy stream; host_w is kept
+        alive here until adapter_wait / adapter_loading reports the load complete."""
+        slot = ctypes.c_int32(-1)
+        ptr, keep = self._host_ptr(host_w, rank)
+        _check(lib().slora_adapter_prefetch(self.h, adapter_id, rank, ptr, scale, ctypes.byref(slot)))
+        self._inflight[adapter_id] = keep
+        return slot.value
+
+    def adapter_wait(self, adapter_id: int) -> None:
+        _check(lib().slora_adapter_wait(self.h, adapter_id))
+        self._inflight.pop(adapter_id, None)
+
+    def adapter_loading(self, adapter_id: int) -> bool:
+        v = ctypes.c_int32(0)
+        _check(lib().slora_adapter_query(self.h, adapter_id, ctypes.byref(v)))
+        if not v.value:
+            self._inflight.pop(adapter_id, None)
+        return bool(v.value)
+
+    def loader_stats(self) -> dict:
+        st = LoaderStats()
+        _check(lib().slora_loader_get_stats(self.h, ctypes.byref(st)))
+        return {f: getattr(st, f) for f, _ in LoaderStats._fields_}
+
     def adapter_evict(self, adapter_id: int, stream=None) -> int:
         n = ctypes.c_int64(0)
         _check(lib().slora_adapter_evict(self.h, adapter_id, _stream(stream), ctypes.byref(n)))
+        keep = self._inflight.pop(adapter_id, None)
+        if keep is not None:  # a load still in flight reads host_w until the fenced stream gets there
+            self._retired.append((keep, stream))
         return n.value
 
     def pin(self, adapter_id: int) -> None:

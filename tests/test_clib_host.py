@@ -195,3 +195,24 @@ def test_pool_destroy_detaches_live_batches():
         b.prepare(np.array([1], np.int64))
     assert e.value.name == "STALE_HANDLE"
     b.close()
+
+
+def test_prefetch_on_bookkeeping_pool():
+    """slora_adapter_prefetch claims pages exactly like slora_adapter_load (same errors, same
+    pop order); with no device there is nothing in flight: wait / query return at once."""
+    a, b = mk(64)[0], mk(64)[0]
+    a.adapter_load(1, 2)
+    b.adapter_prefetch(1, 2, None)
+    assert np.array_equal(a.adapter_pages(1), b.adapter_pages(1))
+    b.adapter_wait(1)
+    assert not b.adapter_loading(1)
+    with pytest.raises(sl.SloraError) as e:
+        b.adapter_prefetch(1, 2, None)
+    assert e.value.name == "ALREADY_RESIDENT"
+    with pytest.raises(sl.SloraError) as e:
+        b.adapter_prefetch(2, 64, None)
+    assert e.value.name == "OUT_OF_PAGES"
+    with pytest.raises(sl.SloraError) as e:
+        b.adapter_wait(9)
+    assert e.value.name == "NOT_RESIDENT"
+    assert b.loader_stats()["loads"] == 0
