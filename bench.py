@@ -232,11 +232,29 @@ class Workload:
         torch.cuda.synchronize()
         self.graph = g
 
-    def step(self, stream, events=None):
+    def rotating_maps(self, n, seed=99):
+        """n decode token maps over the resident adapters, each a different batch with the SAME
+        work: adapters permuted within each rank class (so segment sizes per rank are kept) and
+        token order shuffled -- a serving loop's batch changes every iteration."""
+        rng = np.random.default_rng(seed)
+        tok = self.batch.token_adapter
+        ads = sorted(set(int(a) for a in tok if a >= 0))
+        maps = []
+        for _ in range(n):
+            perm = {}
+            for r in sorted(set(self.batch.ranks[a] for a in ads)):
+                cls = [a for a in ads if self.batch.ranks[a] == r]
+                for a, b2 in zip(cls, rng.permutation(cls)):
+                    perm[a] = int(b2)
+            m = np.array([perm[int(a)] if a >= 0 else -1 for a in tok], np.int64)
+            maps.append(m[rng.permutation(len(m))])
+        return maps
+
+    def step(self, stream, events=None, token_map=None):
         """One step: prepare + all layers.  events: list to append
         (start, end, kind) CUDA event pairs around each launch."""
         b = self.dbatch
-        b.prepare(self.batch.token_adapter, stream=stream)
+        b.prepare(self.batch.token_adapter if token_map is None else token_map, stream=stream)
         if self.graph is not None and events is None:
             self.graph.replay()
             return
@@ -292,6 +310,32 @@ def timed_steps(W, stream, steps, ws):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = float(tt.item())
     return ms, per
+
+
+def rotating_steps(W, stream, steps):
+    """Like timed_steps, but every step prepares a different batch (re-drawn token maps over
+    the resident adapters) and replays the SAME graph: the launches read the descriptors
+    prepare just rewrote (fixed-address call headers).  Also the host time per step."""
+    import torch
+    maps = W.rotating_maps(8)
+    for m in maps[:3]:
+        W.step(stream, token_map=m)
+    torch.cuda.synchronize()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    ev[0].record(stream)
+    t0 = time.perf_counter()
+    for i in range(steps):
+        W.step(stream, token_map=maps[i % len(maps)])
+    host_ms = (time.perf_counter() - t0) * 1e3 / steps
+    ev[1].record(stream)
+    torch.cuda.synchronize()
+    ms = ev[0].elapsed_time(ev[1]) / steps
+    W.dbatch.prepare(W.batch.token_adapter, stream=stream)
+    torch.cuda.synchronize()
+    return {"ms_per_step": round(ms, 4), "host_ms_per_step": round(host_ms, 4), "batches": len(maps),
+            "note": "every step: slora_batch_prepare of a different decode batch (adapters permuted within each "
+                    "rank class, token order shuffled: same work, new descriptors) + replay of the one captured "
+                    "graph; host time includes prepare waiting for the previous step's upload"}
 
 
 def roofline_of(W, ms, stream, serialized=True):
@@ -442,6 +486,10 @@ def run_ours(args):
                                            P337_allreduce_elems=2 * (ws - 1) * NR // ws * layers,
                                            source="counts from the arguments passed to ncclAllGather/"
                                                   "ncclAllReduce (slora_tp_get_stats)")
+    if use_graph and not tp_path and W.dbatch.info()["mbgmm_segments"] == 0:
+        rot = rotating_steps(W, stream, args.steps)
+        rot["vs_fixed_batch"] = round(rot["ms_per_step"] / ms, 3)
+        out["rotating_batch"] = rot
     if not args.no_e2e:
         out["e2e"] = run_e2e(W, stream, max(3, args.steps // 2))
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:

@@ -209,6 +209,19 @@ slora_status slora_batch_create(slora_pool_t pool, slora_batch_t* out);
 slora_status slora_batch_destroy(slora_batch_t batch);
 slora_status slora_batch_prepare(slora_batch_t batch, const int64_t* token_adapter_host, int32_t T,
                                  void* stream);
+/* CUDA-graph replay across batches (the batch changes every
+ * iteration).  The MBGMV launches read their descriptors through a header at
+ * a fixed device address per (batch, call shape); prepare rewrites every
+ * header (one H2D with the descriptors, on its stream) and rebuilds every
+ * call shape launched on this batch since it was created.  So a graph that
+ * captured fused / split calls of this batch handle replays, after each
+ * prepare, the NEW batch -- provided each prepared batch has
+ * mbgmm_segments == 0 (MBGMM launch counts are batch-dependent and baked
+ * into a graph); SLORA_BATCH_MBGMV_ONLY guarantees it (every segment on the
+ * MBGMV path).  Under TP the NCCL element counts are baked as well: replay
+ * only batches of the same sum of ranks. */
+enum { SLORA_BATCH_MBGMV_ONLY = 1 };
+slora_status slora_batch_set_options(slora_batch_t batch, uint32_t flags);
 
 typedef struct {
     int32_t T;                 /* tokens in the batch                         */

@@ -337,8 +337,15 @@ struct slora_batch {
     size_t arena_cap = 0, arena_used = 0;
     void* arena_host = nullptr;
     void* arena_dev = nullptr;
+    size_t dirty_lo = 0, dirty_hi = 0;  // host arena bytes not yet uploaded (arena_flush)
     cudaEvent_t upload_ev = nullptr;
     bool upload_pending = false;
+    // call headers at fixed device addresses ([kernel cfg][nproj]); prepare rewrites them
+    CallHdr* hdr_dev = nullptr;
+    CallHdr* hdr_host = nullptr;          // pinned mirror
+    uint32_t used_masks[4][5] = {};       // call shapes launched since create: rebuilt by every prepare
+    bool in_prepare = false;
+    uint32_t options = 0;                 // slora_batch_set_options
 };
 
 static void batch_free_device(slora_batch* b);
@@ -1096,10 +1103,16 @@ extern "C" slora_status slora_batch_create(slora_pool_t p, slora_batch_t* out) {
     p->batches.insert(b);
     if (p->dev) {
         cudaError_t e = cudaEventCreateWithFlags(&b->upload_ev, cudaEventDisableTiming);
+        if (!e) e = cudaMalloc(&b->hdr_dev, sizeof(CallHdr) * 20);
+        if (!e) e = cudaMemset(b->hdr_dev, 0, sizeof(CallHdr) * 20);
+        if (!e) e = cudaHostAlloc(&b->hdr_host, sizeof(CallHdr) * 20, cudaHostAllocDefault);
         if (e) {
+            if (b->hdr_dev) cudaFree(b->hdr_dev);
+            p->batches.erase(b);
             delete b;
-            return fail(SLORA_ERR_CUDA, "cudaEventCreate: %s", cudaGetErrorString(e));
+            return fail(SLORA_ERR_CUDA, "batch create: %s", cudaGetErrorString(e));
         }
+        memset(b->hdr_host, 0, sizeof(CallHdr) * 20);
     }
     *out = b;
     return ok();
@@ -1109,6 +1122,10 @@ static void batch_free_device(slora_batch* b) {
     if (b->upload_pending) cudaEventSynchronize(b->upload_ev);
     if (b->arena_dev) cudaFree(b->arena_dev);
     if (b->arena_host) cudaFreeHost(b->arena_host);
+    if (b->hdr_dev) cudaFree(b->hdr_dev);
+    if (b->hdr_host) cudaFreeHost(b->hdr_host);
+    b->hdr_dev = nullptr;
+    b->hdr_host = nullptr;
     cudaEventDestroy(b->upload_ev);
     b->arena_dev = b->arena_host = nullptr;
     b->upload_pending = false;
@@ -1130,7 +1147,9 @@ namespace {
 // Copy `n` bytes into the batch's pinned arena and enqueue their H2D copy into
 // the device arena; returns the device offset.  The arena is bump-allocated
 // per prepare and sized by prepare (grown there, never mid-batch).
-size_t arena_put(slora_batch* b, const void* src, size_t n, cudaStream_t s, cudaError_t& err) {
+// Bump-allocate n bytes of the batch arena and fill its pinned mirror; the
+// device copy happens in arena_flush (one H2D per prepare).
+size_t arena_put(slora_batch* b, const void* src, size_t n, cudaStream_t, cudaError_t& err) {
     const size_t off = b->arena_used;
     const size_t n_al = (n + 255) & ~size_t(255);
     if (off + n_al > b->arena_cap) {
@@ -1139,13 +1158,44 @@ size_t arena_put(slora_batch* b, const void* src, size_t n, cudaStream_t s, cuda
     }
     if (n) {
         memcpy(static_cast<uint8_t*>(b->arena_host) + off, src, n);
-        err = cudaMemcpyAsync(static_cast<uint8_t*>(b->arena_dev) + off, static_cast<uint8_t*>(b->arena_host) + off,
-                              n, cudaMemcpyHostToDevice, s);
-        if (!err) err = cudaEventRecord(b->upload_ev, s);
-        b->upload_pending = true;
+        if (b->dirty_hi == b->dirty_lo) b->dirty_lo = off;
+        b->dirty_hi = off + n;
     }
     b->arena_used = off + n_al;
     return off;
+}
+
+// Point the header of call (kc, np) at its descriptors in the arena.
+void set_hdr(slora_pool* p, slora_batch* b, int kc, int np) {
+    const slora_batch::Call& call = b->calls[kc][np];
+    uint8_t* base = static_cast<uint8_t*>(b->arena_dev);
+    CallHdr& h = b->hdr_host[kc * 5 + np];
+    h.tok_idx = reinterpret_cast<const int32_t*>(base + b->off_tok);
+    h.items = reinterpret_cast<const DevItem*>(base + call.off_items);
+    h.pieces = reinterpret_cast<const DevPiece*>(base + call.off_pieces);
+    h.cta_off = reinterpret_cast<const int32_t*>(base + call.off_cta);
+    h.sync = p->sync_dev;
+    h.sync_stride = p->sync_stride;
+    h.ws = p->ws_dev;
+    h.ws_stride = p->ws_stride;
+    h.NR = b->NR;
+    h.n_items = int32_t(call.items.size());
+    h.n_pieces = int32_t(call.pieces.size());
+}
+
+// Upload the arena bytes written since the last flush and the call headers:
+// two H2D copies on the prepare's stream.
+cudaError_t arena_flush(slora_batch* b, cudaStream_t s) {
+    cudaError_t e = cudaSuccess;
+    if (b->dirty_hi > b->dirty_lo)
+        e = cudaMemcpyAsync(static_cast<uint8_t*>(b->arena_dev) + b->dirty_lo,
+                            static_cast<uint8_t*>(b->arena_host) + b->dirty_lo, b->dirty_hi - b->dirty_lo,
+                            cudaMemcpyHostToDevice, s);
+    b->dirty_lo = b->dirty_hi = 0;
+    if (!e) e = cudaMemcpyAsync(b->hdr_dev, b->hdr_host, sizeof(CallHdr) * 20, cudaMemcpyHostToDevice, s);
+    if (!e) e = cudaEventRecord(b->upload_ev, s);
+    b->upload_pending = true;
+    return e;
 }
 
 // Static schedule: LPT (largest first onto the least-loaded CTA) over the
@@ -1380,7 +1430,8 @@ extern "C" slora_status slora_batch_prepare(slora_batch_t b, const int64_t* tok_
             return e ? atoi(e) : kMgDefaultTheta;
         }();
         const int mg_rows = mbgmm_rows(p->cfg.hidden);
-        const bool ok_shape = p->cfg.dtype != SLORA_F32 && p->N() == 1 && theta > 0 && p->cfg.hidden % 64 == 0 &&
+        const bool ok_shape = !(b->options & SLORA_BATCH_MBGMV_ONLY) && p->cfg.dtype != SLORA_F32 && p->N() == 1 &&
+                              theta > 0 && p->cfg.hidden % 64 == 0 &&
                               p->cfg.hidden % kMgCols % 64 == 0 && mbgmm_smem(false, p->cfg.hidden, 0) <= 227 * 1024 &&
                               (!mbgmm_shrink_whole_rank() || (p->cfg.hidden / 64) % kMgKsplit == 0);
         for (size_t si = 0; ok_shape && si < b->segs.size(); ++si) {
@@ -1453,7 +1504,10 @@ extern "C" slora_status slora_batch_prepare(slora_batch_t b, const int64_t* tok_
     // ring kernel: <= ceil(r/8) shrink pieces + D/(dchunk/2) expand pieces per item
     const int64_t dmin = std::max<int64_t>(1, p->kcfg[0].dchunk / 2);
     const int64_t max_pieces_per_item = (kMaxRank + kShrinkRows - 1) / kShrinkRows + (p->cfg.hidden + dmin - 1) / dmin;
-    const size_t need = 256 + size_t(T) * 4 + 6 * (1024 + 4 * 1024 + size_t(b->mg_units_max) * sizeof(MgUnit) +
+    int n_shapes = 6;  // eager shapes + those launched since create (rebuilt below)
+    for (auto& row : b->used_masks)
+        for (uint32_t m : row) n_shapes += m ? 1 : 0;
+    const size_t need = 256 + size_t(T) * 4 + size_t(n_shapes) * (1024 + 4 * 1024 + size_t(b->mg_units_max) * sizeof(MgUnit) +
                                                    size_t(max_items) * sizeof(DevItem) +
                                                    size_t(max_items * max_pieces_per_item) * sizeof(DevPiece));
     cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -1471,6 +1525,12 @@ extern "C" slora_status slora_batch_prepare(slora_batch_t b, const int64_t* tok_
         b->arena_cap = cap;
     }
     b->arena_used = 0;
+    b->dirty_lo = b->dirty_hi = 0;
+    b->in_prepare = true;
+    struct PrepGuard {
+        slora_batch* b;
+        ~PrepGuard() { b->in_prepare = false; }
+    } prep_guard{b};
     cudaError_t e = cudaSuccess;
     b->off_tok = arena_put(b, b->tok_idx.data(), b->tok_idx.size() * sizeof(int32_t), s, e);
     if (e) return fail(SLORA_ERR_CUDA, "batch upload: %s", cudaGetErrorString(e));
@@ -1530,7 +1590,22 @@ extern "C" slora_status slora_batch_prepare(slora_batch_t b, const int64_t* tok_
             if (!st2 && p->kcfg[3].ok) st2 = ensure_call(p, b, 3, 0x8, stream);
         }
     }
+    // every call shape launched since the batch was created is rebuilt too, and all headers
+    // are uploaded with the descriptors in one flush: a CUDA graph that captured those
+    // launches replays the new batch (MBGMV path; see slora_batch_get_info().graph_ok)
+    for (int kc = 0; kc < 4 && !st2; ++kc)
+        for (int np = 1; np <= 4 && !st2; ++np)
+            if (b->used_masks[kc][np] && p->kcfg[kc].ok) st2 = ensure_call(p, b, kc, b->used_masks[kc][np], stream);
+    b->in_prepare = false;
     if (st2) return st2;
+    if (cudaError_t e = arena_flush(b, s)) return fail(SLORA_ERR_CUDA, "batch upload: %s", cudaGetErrorString(e));
+    return ok();
+}
+
+extern "C" slora_status slora_batch_set_options(slora_batch_t b, uint32_t flags) {
+    if (!b) return fail(SLORA_ERR_INVALID_ARG, "null batch");
+    if (flags & ~uint32_t(SLORA_BATCH_MBGMV_ONLY)) return fail(SLORA_ERR_INVALID_ARG, "unknown flags 0x%x", flags);
+    b->options = flags;
     return ok();
 }
 
@@ -1589,6 +1664,13 @@ slora_status ensure_call(slora_pool* p, slora_batch* b, int kc, uint32_t mask, v
     if (e) return fail(SLORA_ERR_CUDA, "call descriptor upload: %s", cudaGetErrorString(e));
     call.built = true;
     call.mask = mask;
+    if (p->dev) {
+        if (!b->in_prepare && b->upload_pending) cudaEventSynchronize(b->upload_ev);  // pinned header mirror free
+        set_hdr(p, b, kc, np);
+        if (!b->in_prepare) {  // built lazily by a call: upload now (prepare flushes once at its end)
+            if ((e = arena_flush(b, s))) return fail(SLORA_ERR_CUDA, "call descriptor upload: %s", cudaGetErrorString(e));
+        }
+    }
     return SLORA_OK;
 }
 
@@ -1610,18 +1692,13 @@ slora_status prepare_call(slora_pool* p, slora_batch* b, int kc, int32_t layer, 
     slora_batch::Call& call = b->calls[kc][np];
     slora_status cs = ensure_call(p, b, kc, mask, stream);
     if (cs) return cs;
-    uint8_t* base = static_cast<uint8_t*>(b->arena_dev);
+    (void)call;
+    b->used_masks[kc][np] = mask;
     q.pool = p->cfg.device_buffer;
     q.page_elems = p->P;
-    q.tok_idx = reinterpret_cast<const int32_t*>(base + b->off_tok);
-    q.items = reinterpret_cast<const DevItem*>(base + call.off_items);
-    q.pieces = reinterpret_cast<const DevPiece*>(base + call.off_pieces);
-    q.cta_off = reinterpret_cast<const int32_t*>(base + call.off_cta);
-    q.n_pieces = int32_t(call.pieces.size());
-    q.n_items = int32_t(call.items.size());
-    if (q.n_items > p->sync_stride) return fail(SLORA_ERR_SHAPE, "sync area too small");
+    q.hdr = b->hdr_dev + (kc * 5 + np);
     const uint64_t slot = p->launch_seq++ % kLaunchSlots;
-    q.sync = p->sync_dev + int64_t(slot) * p->sync_stride;
+    q.slot = int32_t(slot);
     q.layer = layer;
     q.K = int32_t(k.K);
     q.D = int32_t(k.D);
@@ -1631,14 +1708,12 @@ slora_status prepare_call(slora_pool* p, slora_batch* b, int kc, int32_t layer, 
         return e ? atoi(e) : 0;
     }();
     q.dbg = dbg;
-    q.NR = b->NR;
     const int N = p->N();
     for (int pj = 0; pj < 4; ++pj) {
         q.a_div[pj] = (pj < 3) ? N : 1;
         q.a_row_pages[pj] = (pj < 3) ? N : 1;
     }
-    p->ws_slot_base = p->ws_dev + int64_t(slot) * p->ws_stride;
-    if (k.mode == kFused) q.v = p->ws_slot_base;
+    p->ws_slot_base = p->ws_dev + int64_t(slot) * p->ws_stride;  // MBGMM's regions of the slot (host-baked)
     q.trace = p->trace_dev;
     return SLORA_OK;
 }

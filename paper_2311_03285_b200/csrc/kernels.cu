@@ -357,7 +357,7 @@ template <typename T, int NT, int XV>
 __device__ __forceinline__ void shrink_piece(const LoraParams& p, const PieceMeta& M, const unsigned char* ring,
                                              size_t SS, const uint4* xs, int nvec, uint32_t srow, int rps_s,
                                              uint64_t* full, uint64_t* empty, Ring& rg, int ns, uint64_t* xempty,
-                                             float* red, int warp, int lane, int i) {
+                                             float* red, float* vout, int warp, int lane, int i) {
     constexpr int NTP = NT == 3 ? 4 : NT;
     constexpr int VV = 2 * NTP;
     constexpr int LOG2VV = VV == 2 ? 1 : (VV == 4 ? 2 : 3);
@@ -433,7 +433,7 @@ __device__ __forceinline__ void shrink_piece(const LoraParams& p, const PieceMet
         float s = 0.f;
 #pragma unroll
         for (int w = 0; w < kConsumerWarps; ++w) s += red[(w * kShrinkRows + q) * kItemTokCap + t];
-        p.v[M.vbase + int64_t(t) * M.ra + M.row0 + q] = s;
+        vout[M.vbase + int64_t(t) * M.ra + M.row0 + q] = s;
     }
 }
 
@@ -480,7 +480,8 @@ template <typename T>
 __device__ __forceinline__ void shrink_piece_mma(const LoraParams& p, const PieceMeta& M, const unsigned char* ring,
                                                  size_t SS, const unsigned char* xs, uint32_t zero16, int K,
                                                  uint32_t srow, int lg_rps, uint64_t* full, uint64_t* empty, Ring& rg,
-                                                 int ns, uint64_t* xempty, float* red, int warp, int lane, int i) {
+                                                 int ns, uint64_t* xempty, float* red, float* vout, int warp,
+                                                 int lane, int i) {
     constexpr int ES = sizeof(T);
     const int kslice = K / kConsumerWarps;  // elements of K per warp (multiple of 16)
     const int k0w = warp * kslice;
@@ -595,7 +596,7 @@ __device__ __forceinline__ void shrink_piece_mma(const LoraParams& p, const Piec
         float sum = 0.f;
 #pragma unroll
         for (int w = 0; w < kConsumerWarps; ++w) sum += red[(w * kShrinkRows + q) * kItemTokCap + t];
-        p.v[M.vbase + int64_t(t) * M.ra + M.row0 + q] = sum;
+        vout[M.vbase + int64_t(t) * M.ra + M.row0 + q] = sum;
     }
 }
 
@@ -927,21 +928,26 @@ __global__ void __launch_bounds__(kThreads, 1) mbgmv_kernel(const __grid_constan
     pdl_trigger();  // the next launch may start its prologue
     const T* pool = reinterpret_cast<const T*>(p.pool);
     const int64_t P = p.page_elems;
+    // the call's descriptors (prepare rewrites the header; written before this grid by a memcpy)
+    const CallHdr& H = *p.hdr;
+    int32_t* const sync = H.sync + int64_t(p.slot) * H.sync_stride;
+    float* const vout = MODE == kFused ? H.ws + int64_t(p.slot) * H.ws_stride : p.v;
+    const int64_t NR = H.NR;
 
     if (warp == kWarpResolver) {
         // ============================ resolver ============================
         // This CTA's pieces (host schedule) are loaded 32 at a time, one per
         // lane, with their items; each piece then needs one dependent load
         // (its page ids), kMeta-1 pieces ahead of the consumers.
-        const int pb = p.cta_off[blockIdx.x], pe = p.cta_off[blockIdx.x + 1];
+        const int pb = H.cta_off[blockIdx.x], pe = H.cta_off[blockIdx.x + 1];
         int i = 0;
         for (int base = pb; base < pe; base += 32) {
             const int cnt = min(32, pe - base);
             DevPiece pcl{};
             DevItem itl{};
             if (lane < cnt) {
-                pcl = p.pieces[base + lane];
-                itl = p.items[pcl.item];
+                pcl = H.pieces[base + lane];
+                itl = H.items[pcl.item];
             }
             for (int q = 0; q < cnt; ++q, ++i) {
                 const int m = i & (kMeta - 1);
@@ -960,7 +966,7 @@ __global__ void __launch_bounds__(kThreads, 1) mbgmv_kernel(const __grid_constan
                 const int div = (MODE == kExpand) ? 1 : p.a_div[proj];
                 const int arp = (MODE == kExpand) ? 1 : p.a_row_pages[proj];
                 const int32_t* tab = itab + int64_t((p.layer * 4 + proj) * 2) * rank;
-                if (lane < nt) M.tok[lane] = p.tok_idx[tok_off + lane];
+                if (lane < nt) M.tok[lane] = H.tok_idx[tok_off + lane];
                 if (kind == kPieceS) {
                     for (int w = lane; w < pbn * arp; w += 32) M.pages[w] = tab[(pa + w / arp) * arp + w % arp];
                 } else {
@@ -977,7 +983,7 @@ __global__ void __launch_bounds__(kThreads, 1) mbgmv_kernel(const __grid_constan
                     M.n_sp = itl.n_sp;
                     M.n_ep = itl.n_ep;
                     M.scale = itl.scale;
-                    M.vbase = int64_t(pi) * (p.NR / div) + itl.vrow / div;
+                    M.vbase = int64_t(pi) * (NR / div) + itl.vrow / div;
                     M.pi = pi;
                     M.vrow = itl.vrow;
                     M.row0 = M.dcol0 = pa;
@@ -1111,7 +1117,7 @@ __global__ void __launch_bounds__(kThreads, 1) mbgmv_kernel(const __grid_constan
                         // cannot hold them (e.g. SMs taken by MPS / green contexts), fail the
                         // launch after ~4 s instead of hanging (surfaces as SLORA_ERR_CUDA).
                         const long long t_end = gtimer() + 4000000000LL;
-                        while (ld_acquire(&p.sync[M.item]) < M.n_sp) {
+                        while (ld_acquire(&sync[M.item]) < M.n_sp) {
                             __nanosleep(32);
                             if (gtimer() > t_end) {
                                 printf("slora: expand piece of item %d waited > 4 s for its shrink pieces: "
@@ -1121,16 +1127,16 @@ __global__ void __launch_bounds__(kThreads, 1) mbgmv_kernel(const __grid_constan
                         }
                     }
                     __syncwarp();
-                    for (int e = lane; e < M.nt * M.r; e += 32) vb[e] = __ldcg(p.v + M.vbase + e);
+                    for (int e = lane; e < M.nt * M.r; e += 32) vb[e] = __ldcg(vout + M.vbase + e);
                     __syncwarp();
                     // the item's last expand piece to read v resets its counter for
                     // the launch slot's next use (which starts after this grid ends)
-                    if (lane == 0 && atomicAdd(&p.sync[M.item], 1) == M.n_sp + M.n_ep - 1)
-                        atomicExch(&p.sync[M.item], 0);
+                    if (lane == 0 && atomicAdd(&sync[M.item], 1) == M.n_sp + M.n_ep - 1)
+                        atomicExch(&sync[M.item], 0);
                 } else {  // v from v_in: block layout of slora_lora_expand
                     const int vbk = p.v_blocks, rb = M.r / vbk;
-                    const int64_t stride = int64_t(p.nproj) * (p.NR / vbk);
-                    const int64_t base = int64_t(M.pi) * (p.NR / vbk) + M.vrow / vbk;
+                    const int64_t stride = int64_t(p.nproj) * (NR / vbk);
+                    const int64_t base = int64_t(M.pi) * (NR / vbk) + M.vrow / vbk;
                     for (int e = lane; e < M.nt * M.r; e += 32) {
                         const int t = e / M.r, j = e % M.r;
                         vb[e] = p.v_in[int64_t(j / rb) * stride + base + int64_t(t) * rb + j % rb];
@@ -1155,7 +1161,7 @@ __global__ void __launch_bounds__(kThreads, 1) mbgmv_kernel(const __grid_constan
             __syncwarp();
             if (lane == 0) mbar_arrive(&pempty[b]);
             if (item < 0) break;
-            if (lane == 0 && MODE == kFused) red_release_add(&p.sync[item], 1);
+            if (lane == 0 && MODE == kFused) red_release_add(&sync[item], 1);
         }
     } else {
         // ============================ consumers ===========================
@@ -1194,13 +1200,13 @@ __global__ void __launch_bounds__(kThreads, 1) mbgmv_kernel(const __grid_constan
                 const int xvn = ((nvec + kConsumerWarps - 1) / kConsumerWarps + 31) / 32;
                 if (use_mma) {
                     shrink_piece_mma<T>(p, M, ring, SS, reinterpret_cast<const unsigned char*>(xsm), zero16, int(K),
-                                        srow, lg_rps, full, empty, rg, ns, &xempty[xb], rd, warp, lane, i);
+                                        srow, lg_rps, full, empty, rg, ns, &xempty[xb], rd, vout, warp, lane, i);
                 } else
                 switch (M.nt * 8 + (xvn <= 1 ? 1 : (xvn == 2 ? 2 : 4))) {
 #define SLORA_SHRINK_CASE(N, X)                                                                                  \
     case N * 8 + X:                                                                                            \
         shrink_piece<T, N, X>(p, M, ring, SS, xsm, nvec, srow, rps_s, full, empty, rg, ns, &xempty[xb], rd,      \
-                              warp, lane, i);                                                                   \
+                              vout, warp, lane, i);                                                             \
         break;
 #ifdef SLORA_FEW_VARIANTS
                     SLORA_SHRINK_CASE(1, 2)
@@ -1336,7 +1342,7 @@ static cudaError_t launch_mode(const LoraParams& p, int mode, int grid, cudaStre
 }
 
 cudaError_t launch_lora(const LoraParams& p, int mode, int dtype, int grid, cudaStream_t s, size_t smem) {
-    if (p.n_pieces == 0 || grid == 0) return cudaSuccess;
+    if (grid == 0) return cudaSuccess;  // empty calls still launch: a captured graph may replay a later batch
     switch (dtype) {
         case kF32: return launch_mode<float>(p, mode, grid, s, smem);
         case kF16: return launch_mode<__half>(p, mode, grid, s, smem);

@@ -93,16 +93,28 @@ enum Mode : int { kFused = 0, kShrink = 1, kExpand = 2 };
 enum DType : int { kF32 = 0, kF16 = 1, kBF16 = 2 };
 enum PieceKind : int { kPieceS = 0, kPieceE = 1, kPieceStop = 2 };
 
-struct LoraParams {
-    const void* pool;             // page buffer
-    int64_t page_elems;           // P
+// The batch-dependent part of a call, at a FIXED device address per (batch,
+// call shape): slora_batch_prepare rewrites it (one H2D with the descriptor
+// upload), so a CUDA graph of the MBGMV launches stays valid while the batch
+// changes every iteration (iteration-level batching).
+struct CallHdr {
     const int32_t* tok_idx;
     const DevItem* items;
     const DevPiece* pieces;       // grouped by CTA: CTA b runs pieces [cta_off[b], cta_off[b+1])
     const int32_t* cta_off;       // grid + 1 entries
-    int32_t n_pieces;
-    int32_t n_items;
-    int32_t* sync;                // this launch's slot: per-item done counters (self-resetting)
+    int32_t* sync;                // kLaunchSlots slots of sync_stride per-item done counters (self-resetting)
+    float* ws;                    // kLaunchSlots slots of ws_stride floats: the fused call's v workspace
+    int64_t sync_stride, ws_stride;
+    int64_t NR;                   // sum over adapted tokens of rank
+    int32_t n_items, n_pieces;
+};
+static_assert(sizeof(CallHdr) == 80, "CallHdr layout");
+
+struct LoraParams {
+    const void* pool;             // page buffer
+    int64_t page_elems;           // P
+    const CallHdr* hdr;           // the call's descriptor header (batch_prepare rewrites it)
+    int32_t slot;                 // rotating launch slot: sync counters / workspace of this launch
     int32_t nproj;
     int32_t proj_ids[4];
     int32_t layer;
@@ -116,10 +128,9 @@ struct LoraParams {
     void* y[4];
     int64_t ldy[4];
     long long* trace;             // debug: per-CTA event timestamps (nullptr = off)
-    float* v;                     // shrink output / fused workspace (C-ABI v layout, div as stored)
+    float* v;                     // shrink output (split mode; C-ABI v layout, div as stored); fused: nullptr
     const float* v_in;            // expand input
     int32_t v_blocks;
-    int64_t NR;                   // sum over adapted tokens of rank
 };
 
 // Per-launch kernel configuration (chosen on the host, see api.cpp).

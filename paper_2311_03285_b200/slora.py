@@ -104,6 +104,7 @@ SIGNATURES = {
     "slora_tp_lora_qkv": [_VP, _VP, _I32, _VP, _I64, ctypes.POINTER(_VP), _PI64, _VP],
     "slora_tp_lora_o": [_VP, _VP, _I32, _VP, _I64, _VP, _I64, _VP],
     "slora_tp_get_stats": [_VP, ctypes.POINTER(TPStats)],
+    "slora_batch_set_options": [_VP, ctypes.c_uint32],
     "slora_adapter_prefetch": [_VP, _I64, _I32, _VP, ctypes.c_float, ctypes.POINTER(_I32)],
     "slora_adapter_wait": [_VP, _I64],
     "slora_adapter_query": [_VP, _I64, ctypes.POINTER(_I32)],
@@ -383,6 +384,10 @@ class Batch:
     def prepare(self, token_adapter, stream=None) -> None:
         ta = np.ascontiguousarray(token_adapter, np.int64)
         _check(lib().slora_batch_prepare(self.h, ta.ctypes.data_as(_PI64), int(ta.size), _stream(stream)))
+
+    def set_options(self, mbgmv_only: bool = False) -> None:
+        """mbgmv_only: every segment on the MBGMV path (graph replay across batches)."""
+        _check(lib().slora_batch_set_options(self.h, 1 if mbgmv_only else 0))
 
     def info(self) -> dict:
         r = BatchInfo()
