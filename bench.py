@@ -388,6 +388,87 @@ def measure(name, layers, steps, warmup, stream, graph=True):
     return out
 
 
+def measure_mlp(stream, layers=8, steps=10):
+    """NEXT-4 secondary: C2's decode batch with LoRA on all seven Llama-7B projections
+    (q,k,v,o 4096 -> 4096; MLP gate/up 4096 -> 11008, down 11008 -> 4096: stored rows over 3
+    pages), 4 fused calls per layer grouped by input width, graph replay like the headline.
+    Weight CONTENT is immaterial to the timing: one host buffer per rank serves every adapter
+    of that rank (the parity of these shapes is tests/test_gpu_proj_shapes.py)."""
+    import torch
+    from paper_2311_03285_b200 import Batch, Pool
+    cfg = wl.CONFIGS["c2-mlp"]
+    dims = wl.proj_dims(cfg)
+    b0 = wl.make_batch(cfg)
+    H, es = cfg.hidden, wl.elem_bytes(cfg.dtype)
+    units = sum(-(-i // H) + -(-o // H) for i, o in dims)
+    need = sum(layers * r * units for r in b0.ranks.values())
+    pool = Pool(H, layers, need + 64, dtype=cfg.dtype, device=torch.cuda.current_device(), order="shuffle",
+                seed=1234, max_adapters=len(b0.ranks) + 8, proj_dims=dims)
+    bufs = {r: wl.adapter_host_buffer(cfg, 100_000 + r, layers, rank=r) for r in set(b0.ranks.values())}
+    for a in b0.unique:
+        pool.adapter_load(a, b0.ranks[a], bufs[b0.ranks[a]], stream=stream)
+    torch.cuda.synchronize()
+    b = Batch(pool)
+    b.prepare(b0.token_adapter, stream=stream)
+    T = b0.T
+    td = {"f16": torch.float16, "bf16": torch.bfloat16, "f32": torch.float32}[cfg.dtype]
+    g = torch.Generator(device="cuda").manual_seed(9)
+    calls = [(0, 1, 2), (3,), (4, 5), (6,)]
+    xs = {c: torch.randn((layers, T, dims[c[0]][0]), generator=g, device="cuda").to(td) for c in calls}
+    ys = [torch.randn((layers, T, o), generator=g, device="cuda").to(td) for _, o in dims]
+    ld = [o for _, o in dims]
+
+    def run_layers():
+        for l in range(layers):
+            for c in calls:
+                b.apply(l, list(c), xs[c][l], dims[c[0]][0], [y[l] for y in ys], ld,
+                        stream=torch.cuda.current_stream())
+
+    def step():
+        b.prepare(b0.token_adapter, stream=stream)
+        gr.replay()
+
+    run_layers()
+    torch.cuda.synchronize()
+    gr = torch.cuda.CUDAGraph()
+    cs = torch.cuda.Stream()
+    with torch.cuda.graph(gr, stream=cs):
+        run_layers()
+    for _ in range(3):
+        step()
+    torch.cuda.synchronize()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
+    ev[0].record(stream)
+    for i in range(steps):
+        step()
+        ev[i + 1].record(stream)
+    torch.cuda.synchronize()
+    ms = ev[0].elapsed_time(ev[steps]) / steps
+    per = [ev[i].elapsed_time(ev[i + 1]) for i in range(steps)]
+    Tad = int((b0.token_adapter >= 0).sum())
+    wb = sum(sum(r * (i + o) * es for i, o in dims) for r in b0.ranks.values())
+    act = sum(Tad * dims[c[0]][0] * es for c in calls) + sum(2 * Tad * o * es for _, o in dims)
+    bytes_step = layers * (wb + act)
+    peaks, kind = measured_peaks()
+    achieved = bytes_step / (ms / 1e3) / 1e9
+    out = {"workload": cfg.name, "dtype": cfg.dtype, "hidden": H, "proj_dims": [list(d) for d in dims],
+           "layers": layers, "tokens": T, "adapted_tokens": Tad, "unique_adapters": len(b0.ranks),
+           "calls_per_layer": ["q,k,v", "o", "gate,up", "down"],
+           "ms_per_step": round(ms, 4), "value": round(Tad * layers / (ms / 1e3), 1), "unit": UNIT,
+           "p10_p50_p90_ms": [round(float(v), 4) for v in np.percentile(per, [10, 50, 90])],
+           "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                        "frac": round(achieved / peaks["hbm_gbs"], 4), "alg_bytes_per_layer": int(wb + act),
+                        "peak_source": f"{kind} copy bandwidth (MEASURED_PEAKS.json hbm_gbs)"},
+           "note": "value counts adapted tokens x layers (each layer = 7 LoRA'd projections); 8 layers of "
+                   "adapter pages (%.1f GB) rotate, >> L2" % (layers * wb / 1e9)}
+    b.close()
+    pool.close()
+    del xs, ys
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    return out
+
+
 def traffic_record(cfg_name):
     """Measured DRAM bytes per launch of the hot kernel: a STATIC record from
     the committed ncu capture (profiles/ncu_summary.json), not this run."""
@@ -509,6 +590,10 @@ def run_ours(args):
                 sec[sname] = {"error": f"{type(e).__name__}: {e}"}
         sec["c4"]["note"] = "70B shapes unsharded on one GPU (the TP8 config's N=1 point); 8 layers (670 MB of " \
                             "adapter pages rotate, >> L2)"
+        try:
+            sec["c2-mlp"] = measure_mlp(stream)
+        except Exception as e:
+            sec["c2-mlp"] = {"error": f"{type(e).__name__}: {e}"}
         out["secondary"] = sec
         try:
             out["ablations"] = run_ablations(stream)

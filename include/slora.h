@@ -96,7 +96,23 @@ typedef struct {
     int32_t max_adapters;       /* adapter slots (resident adapters), >= 1    */
     slora_alloc_order alloc_order;
     uint64_t seed;              /* for SLORA_ORDER_SHUFFLE                    */
+    /* NEXT-4 (P:321-327 uses the MLP as its example): the LoRA'd
+     * projections of a layer and their shapes.  num_proj = 0 means the four
+     * square attention projections q,k,v,o.  Projection p maps
+     * proj_in[p] inputs to proj_out[p] outputs (0 = hidden), e.g. Llama-7B
+     * MLP gate/up 4096 -> 11008, down 11008 -> 4096, or GQA k/v 4096 -> 1024.
+     * A stored row of n elements spans ceil(n / page_elems) pages, the last
+     * one partly used (reading R2): per adapter and layer, projection p takes
+     * r * (ceil(proj_in[p]/P) + ceil(proj_out[p]/P)) pages.  Non-square
+     * projections need tp_size == 1; every dim is a multiple of 16 bytes of
+     * the dtype and spans <= 8 pages; the host buffer of slora_adapter_load
+     * holds, per layer and projection p in order, A (proj_in x r) then B
+     * (r x proj_out), row-major. */
+    int32_t num_proj;           /* 1..8, or 0 = 4 (q,k,v,o)                    */
+    int64_t proj_in[8];
+    int64_t proj_out[8];
 } slora_pool_config;
+#define SLORA_MAX_PROJ 8
 
 slora_status slora_pool_create(const slora_pool_config* cfg, slora_pool_t* out);
 slora_status slora_pool_destroy(slora_pool_t pool); /* synchronizes the device */
@@ -236,10 +252,13 @@ slora_status slora_batch_get_info(slora_batch_t batch, slora_batch_info* out);
 /* ---------------------------------------------------------------- a5+a7 --
  * Fused shrink -> expand on one GPU (Eq. lora_factored P:121 per token; the
  * rank-r intermediate stays on chip):
- *   for every projection p in proj_mask (bit p: 0=q 1=k 2=v 3=o) and every
+ *   for every projection p in proj_mask (bit p: 0=q 1=k 2=v 3=o by default;
+ *   projection p of the pool's proj_in/proj_out list otherwise) and every
  *   adapted token i with adapter a:
  *     y_p[i, :] = round( y_p[i, :] + scale_a * (x[i, :] A_{a,layer,p}) B_{a,layer,p} )
- *   x: T x hidden, row stride ldx elements; y[p]: T x hidden, stride ldy[p];
+ *   x: T x proj_in (the projections of one call share their input width),
+ *   row stride ldx elements; y[p]: T x proj_out[p], stride ldy[p] (y and ldy
+ *   are indexed by projection id; only the mask's entries are read);
  *   pool dtype; 16-byte aligned rows.  fp32 accumulation; one rounding.
  *   Only for tp_size == 1 (else INVALID_ARG).
  *   Segments are served by MBGMV, or -- consecutive runs of >= 32 tokens of
@@ -250,7 +269,7 @@ slora_status slora_batch_get_info(slora_batch_t batch, slora_batch_info* out);
  *   are used in stream order. */
 slora_status slora_lora_apply(slora_pool_t pool, slora_batch_t batch, int32_t layer,
                               uint32_t proj_mask, const void* x, int64_t ldx,
-                              void* const y[4], const int64_t ldy[4], void* stream);
+                              void* const y[SLORA_MAX_PROJ], const int64_t ldy[SLORA_MAX_PROJ], void* stream);
 
 /* Split form (for tensor parallelism).
  * shrink: v = x A_shard in fp32.  For projection p, the stored A shard has
@@ -271,7 +290,7 @@ slora_status slora_lora_shrink(slora_pool_t pool, slora_batch_t batch, int32_t l
                                void* stream);
 slora_status slora_lora_expand(slora_pool_t pool, slora_batch_t batch, int32_t layer,
                                uint32_t proj_mask, const float* v, int32_t v_blocks,
-                               void* const y[4], const int64_t ldy[4], void* stream);
+                               void* const y[SLORA_MAX_PROJ], const int64_t ldy[SLORA_MAX_PROJ], void* stream);
 
 /* ---------------------------------------------------------------- a6/a8 --
  * Tensor-parallel LoRA (Fig. lora_tp; readings R3/R4/R13/R14):

@@ -21,6 +21,11 @@ What the paper leaves open, with the readings used here:
     LoRA tensor still takes r pages per GPU (q/k/v A shard: r/N rank columns
     of length H, i.e. N pages each; all other shards: r rows of H/N).
   * Adapter slots: the lowest free slot index is assigned on load.
+  * R2 (NEXT-4, P:321-327 uses the MLP as its worked example): projections
+    need not be square.  A stored row of n elements (A row j = column j of the
+    h_in x r matrix A; B row j of r x d_out) spans ceil(n/H) pages, the last
+    one partly used; for n = H this is P:262's one page per rank row.  Pools
+    with non-square projections are single-GPU (tp_size 1).
 Error names follow SPEC S:114-163 (see include/slora.h).
 """
 from __future__ import annotations
@@ -98,9 +103,14 @@ class PoolModel:
 
     def __init__(self, capacity_pages: int, hidden: int, num_layers: int,
                  tp_size: int = 1, tp_rank: int = 0, order: str = "ascending",
-                 seed: int = 0, max_adapters: int = 1024):
+                 seed: int = 0, max_adapters: int = 1024, proj_dims=None):
         if capacity_pages < 1 or hidden < 1 or num_layers < 1 or tp_size < 1:
             raise PoolError(ERR_INVALID_ARG, "sizes must be >= 1")
+        # (h_in, d_out) per LoRA'd projection; default q, k, v, o square
+        self.dims = [(hidden, hidden)] * 4 if proj_dims is None else [tuple(d) for d in proj_dims]
+        self.NUM_PROJ = len(self.dims)
+        if tp_size > 1 and self.dims != [(hidden, hidden)] * 4:
+            raise PoolError(ERR_SHAPE, "tensor parallelism needs the four square projections")
         if not (0 <= tp_rank < tp_size):
             raise PoolError(ERR_INVALID_ARG, "tp_rank")
         if hidden % tp_size:
@@ -136,9 +146,12 @@ class PoolModel:
         """(rows, chunks per row) of one LoRA tensor shard on this GPU (R3).
         A is stored transposed: one row per rank column (R1)."""
         N = self.N
-        if proj < 3 and tensor == 0:  # q/k/v A: column partition along r
-            return rank // N, N
-        return rank, 1
+        if N > 1:
+            if proj < 3 and tensor == 0:  # q/k/v A: column partition along r
+                return rank // N, N
+            return rank, 1
+        n = self.dims[proj][0 if tensor == 0 else 1]  # stored row length (R2)
+        return rank, -(-n // self.page_elems)
 
     def adapter_page_count(self, rank: int) -> int:
         n = 0

@@ -133,7 +133,9 @@ NcclApi& nccl() {
 
 // -------------------------------------------------------------------- pool
 namespace {
-constexpr int kNumProj = 4;
+constexpr int kNumProj = 4;       // the default projections q, k, v, o
+constexpr int kMaxKc = 8;         // kernel configurations: 0-3 below, 4+ fused for other input widths
+constexpr int kNpSlots = kMaxProj + 1;  // calls / headers per configuration, by projection count
 constexpr size_t kStageBytes = size_t(16) << 20;   // per loader staging chunk (pinned host + device)
 constexpr size_t kJobBytes = size_t(64) << 10;     // job table at the head of a chunk
 constexpr int kLoadChunks = 4;                     // staging ring depth (pack || H2D || scatter)
@@ -267,7 +269,22 @@ struct slora_pool {
     std::unordered_set<slora_batch*> batches;  // live batches (detached by pool_destroy)
     // kernel configurations: 0 fused (K=D=H), 1 shrink q/k/v (K=H),
     // 2 shrink o (K=H/N), 3 expand (D=H/N)
-    KernelCfg kcfg[4];  // 0 fused (ring pipeline), 1 shrink q/k/v, 2 shrink o, 3 expand
+    KernelCfg kcfg[kMaxKc];  // 0 fused K=hidden (ring pipeline), 1 shrink q/k/v, 2 shrink o, 3 expand,
+                             // 4.. fused for the other projection input widths (NEXT-4)
+    int n_kcfg = 4;
+    // LoRA'd projections (NEXT-4): count, dims, page-table layout in units of the rank
+    int np = kNumProj;
+    int64_t pin[kMaxProj] = {}, pout[kMaxProj] = {};
+    int32_t a_units[kMaxProj] = {}, b_units[kMaxProj] = {};  // page-table entries per rank unit (A, B)
+    int32_t b_row_pages[kMaxProj] = {};                      // pages per stored B row
+    int32_t proj_off[kMaxProj] = {};                         // projection p's tables in a layer (units of r)
+    int32_t layer_units = 0;
+    bool square = true;                                      // every projection hidden -> hidden
+    int fused_kc(int64_t K) const {  // the fused configuration of a call whose projections read K inputs
+        for (int c = 0; c < n_kcfg; ++c)
+            if ((c == 0 || c >= 4) && kcfg[c].K == K) return c;
+        return -1;
+    }
     long long* trace_dev = nullptr;   // SLORA_TRACE=1: kernel event timestamps
     // rotating per-launch slots: item-done counters (zeroed once; each item's
     // last expand piece re-zeroes its counter) and the fused v workspace
@@ -293,16 +310,23 @@ struct slora_pool {
     int64_t free_pages() const { return int64_t(free_stack.size()); }
     int N() const { return cfg.tp_size; }
     // (stored rows, chunks per row) of one tensor shard (reading R3/R4)
+    // (stored rows, pages per row) of one tensor shard.  One GPU: A has r stored rows of
+    // proj_in elements, B r rows of proj_out, each ceil(n/P) pages (reading R2, NEXT-4).
+    // TP (square projections only): readings R3/R4.
     void tensor_shape(int proj, int tensor, int rank, int& rows, int& chunks) const {
-        if (proj < 3 && tensor == 0) {
-            rows = rank / N();
-            chunks = N();
-        } else {
-            rows = rank;
-            chunks = 1;
+        if (N() > 1) {
+            rows = (proj < 3 && tensor == 0) ? rank / N() : rank;
+            chunks = (proj < 3 && tensor == 0) ? N() : 1;
+            return;
         }
+        rows = rank;
+        chunks = int(((tensor == 0 ? pin[proj] : pout[proj]) + P - 1) / P);
     }
-    int64_t adapter_page_count(int rank) const { return int64_t(cfg.num_layers) * kNumProj * 2 * rank; }
+    int64_t adapter_page_count(int rank) const { return int64_t(cfg.num_layers) * layer_units * rank; }
+    // dense elements of the host tensor (A: in x r, B: r x out) of projection p
+    int64_t host_elems(int proj, int tensor, int rank) const {
+        return int64_t(rank) * (tensor == 0 ? pin[proj] : pout[proj]);
+    }
 };
 
 struct slora_batch {
@@ -325,7 +349,7 @@ struct slora_batch {
         std::vector<int32_t> cta_off;   // grid + 1
         std::vector<MgUnit> mg_s, mg_e; // MBGMM shrink / expand units (fused calls with long runs)
         size_t off_items = 0, off_pieces = 0, off_cta = 0, off_mg_s = 0, off_mg_e = 0;
-    } calls[4][5];
+    } calls[kMaxKc][kNpSlots];
     // per segment: token ranges [begin, end) of the segment's token list that
     // are MBGMM runs (>= theta consecutive x rows; fused 16-bit calls only)
     std::vector<std::vector<std::pair<int32_t, int32_t>>> runs;
@@ -343,7 +367,7 @@ struct slora_batch {
     // call headers at fixed device addresses ([kernel cfg][nproj]); prepare rewrites them
     CallHdr* hdr_dev = nullptr;
     CallHdr* hdr_host = nullptr;          // pinned mirror
-    uint32_t used_masks[4][5] = {};       // call shapes launched since create: rebuilt by every prepare
+    uint32_t used_masks[kMaxKc][kNpSlots] = {};  // call shapes launched since create: rebuilt by every prepare
     bool in_prepare = false;
     uint32_t options = 0;                 // slora_batch_set_options
 };
@@ -385,11 +409,44 @@ extern "C" slora_status slora_pool_create(const slora_pool_config* cfg, slora_po
     } else if (cfg->device_buffer) {
         return fail(SLORA_ERR_INVALID_ARG, "bookkeeping-only pool takes no device_buffer");
     }
+    // LoRA'd projections (NEXT-4): default q,k,v,o square
+    const int np = cfg->num_proj == 0 ? kNumProj : cfg->num_proj;
+    if (np < 1 || np > kMaxProj) return fail(SLORA_ERR_INVALID_ARG, "num_proj %d not in 1..%d", np, kMaxProj);
+    int64_t pin[kMaxProj] = {}, pout[kMaxProj] = {};
+    bool square = np == kNumProj;
+    for (int q = 0; q < np; ++q) {
+        pin[q] = (cfg->num_proj == 0 || cfg->proj_in[q] == 0) ? cfg->hidden : cfg->proj_in[q];
+        pout[q] = (cfg->num_proj == 0 || cfg->proj_out[q] == 0) ? cfg->hidden : cfg->proj_out[q];
+        if (pin[q] < 1 || pout[q] < 1) return fail(SLORA_ERR_INVALID_ARG, "projection %d dims < 1", q);
+        if ((pin[q] * es) % 16 || (pout[q] * es) % 16)
+            return fail(SLORA_ERR_SHAPE, "projection %d dims must be multiples of 16 bytes", q);
+        if ((pin[q] + P - 1) / P > kMaxChunks || (pout[q] + P - 1) / P > kMaxChunks)
+            return fail(SLORA_ERR_SHAPE, "projection %d rows span more than %d pages", q, kMaxChunks);
+        square = square && pin[q] == cfg->hidden && pout[q] == cfg->hidden;
+    }
+    if (cfg->tp_size > 1 && !square)
+        return fail(SLORA_ERR_SHAPE, "tensor parallelism needs the four square projections (q,k,v,o)");
     slora_pool* p = new slora_pool();
     p->cfg = *cfg;
     p->P = P;
     p->es = es;
     p->dev = cfg->device >= 0;
+    p->np = np;
+    p->square = square;
+    for (int q = 0; q < np; ++q) {
+        p->pin[q] = pin[q];
+        p->pout[q] = pout[q];
+    }
+    for (int q = 0; q < np; ++q) {
+        int rows, ch;
+        p->tensor_shape(q, 0, cfg->tp_size, rows, ch);  // rank = N: units per rank unit = rows*ch/N
+        p->a_units[q] = rows * ch / cfg->tp_size;
+        p->tensor_shape(q, 1, cfg->tp_size, rows, ch);
+        p->b_units[q] = rows * ch / cfg->tp_size;
+        p->b_row_pages[q] = ch;
+        p->proj_off[q] = p->layer_units;
+        p->layer_units += p->a_units[q] + p->b_units[q];
+    }
     const int64_t cap = cfg->capacity_pages;
     p->free_stack.resize(size_t(cap));
     for (int64_t i = 0; i < cap; ++i) p->free_stack[size_t(i)] = int32_t(cap - 1 - i);
@@ -424,8 +481,10 @@ extern "C" slora_status slora_pool_create(const slora_pool_config* cfg, slora_po
         p->kcfg[1] = make_kernel_cfg(kShrink, H, P, P, es, dt);
         p->kcfg[2] = make_kernel_cfg(kShrink, cfg->tp_size > 1 ? P : H, P, P, es, dt);
         p->kcfg[3] = make_kernel_cfg(kExpand, P, P, P, es, dt);
+        for (int q = 0; q < np && cfg->tp_size == 1; ++q)  // fused configurations of the other input widths
+            if (p->fused_kc(pin[q]) < 0 && p->n_kcfg < kMaxKc) p->kcfg[p->n_kcfg++] = make_kernel_cfg(kFused, pin[q], P, P, es, dt);
         if (const char* vb = getenv("SLORA_VERBOSE"); vb && atoi(vb) > 0)
-            for (int c = 0; c < 4; ++c)
+            for (int c = 0; c < p->n_kcfg; ++c)
                 fprintf(stderr, "slora: kcfg[%d] mode=%d K=%lld D=%lld dchunk=%lld ns=%d smem=%zu grid=%d ok=%d\n", c,
                         p->kcfg[c].mode, (long long)p->kcfg[c].K, (long long)p->kcfg[c].D,
                         (long long)p->kcfg[c].dchunk, p->kcfg[c].ns, p->kcfg[c].smem, p->kcfg[c].grid,
@@ -647,6 +706,12 @@ static void pack_shard(const slora_pool* p, const uint8_t* A, const uint8_t* B, 
                        uint8_t* dst, int& rows_out, int& cols_out, std::vector<CopySeg>& segs) {
     const int64_t H = p->cfg.hidden, P = p->P;
     const int N = p->N(), k = p->cfg.tp_rank, es = p->es;
+    if (N == 1) {  // the dense tensor is the shard: A (proj_in x r), B (r x proj_out)
+        segs.push_back({dst, tensor == 0 ? A : B, size_t(p->host_elems(proj, tensor, r)) * es});
+        rows_out = int(tensor == 0 ? p->pin[proj] : r);
+        cols_out = int(tensor == 0 ? r : p->pout[proj]);
+        return;
+    }
     if (tensor == 0) {
         if (proj < 3) {
             const int rc = r / N;
@@ -693,7 +758,9 @@ static cudaError_t run_load(slora_pool* p, LoadJob& jb) {
     auto& L = p->ld;
     const int64_t H = p->cfg.hidden;
     const int es = p->es;
-    const int64_t per_lp = (H * jb.rank + int64_t(jb.rank) * H);  // elements of A+B per (layer, proj)
+    (void)H;
+    int64_t per_layer = 0;  // host elements of one layer: A and B of every projection
+    for (int pr = 0; pr < p->np; ++pr) per_layer += p->host_elems(pr, 0, jb.rank) + p->host_elems(pr, 1, jb.rank);
     size_t used = kJobBytes;
     std::vector<ScatterJob> jobs;
     std::vector<CopySeg> segs;
@@ -749,14 +816,16 @@ static cudaError_t run_load(slora_pool* p, LoadJob& jb) {
         if (e) return e;
     }
     int64_t page_cursor = 0;
-    for (int l = 0; l < p->cfg.num_layers && !e; ++l)
-        for (int pr = 0; pr < kNumProj && !e; ++pr) {
-            const uint8_t* A = jb.host_w + size_t((int64_t(l) * kNumProj + pr) * per_lp) * es;
-            const uint8_t* B = A + size_t(H * jb.rank) * es;
+    for (int l = 0; l < p->cfg.num_layers && !e; ++l) {
+        const uint8_t* A = jb.host_w + size_t(int64_t(l) * per_layer) * es;
+        for (int pr = 0; pr < p->np && !e; ++pr) {
+            const uint8_t* B = A + size_t(p->host_elems(pr, 0, jb.rank)) * es;
+            const uint8_t* An = B + size_t(p->host_elems(pr, 1, jb.rank)) * es;  // the next projection's A
             for (int t = 0; t < 2 && !e; ++t) {
                 int rows_s, chunks;
                 p->tensor_shape(pr, t, jb.rank, rows_s, chunks);
-                const size_t bytes = size_t(rows_s) * chunks * size_t(p->P) * es;
+                // staging bytes of this rank's shard (dense; = host bytes / N)
+                const size_t bytes = size_t(p->host_elems(pr, t, jb.rank) / p->N()) * es;
                 if (used + bytes > kStageBytes || (jobs.size() + 1) * sizeof(ScatterJob) > kJobBytes) {
                     if ((e = flush())) break;
                 }
@@ -769,13 +838,15 @@ static cudaError_t run_load(slora_pool* p, LoadJob& jb) {
                 sj.kind = t;
                 sj.rows = rows;
                 sj.cols = cols;
-                sj.row_pages = (t == 0) ? chunks : 1;
+                sj.row_pages = chunks;
                 jobs.push_back(sj);
-                used += bytes;
+                used += (bytes + 15) & ~size_t(15);
                 jb.bytes += int64_t(bytes);
                 page_cursor += int64_t(rows_s) * chunks;
             }
+            A = An;
         }
+    }
     if (!e) e = flush();
     // host_w is consumed once its last chunk is packed (or, read directly, once its H2D completed)
     if (!e && jb.direct) e = cudaEventSynchronize(L.ev[(k + kLoadChunks - 1) % kLoadChunks]);
@@ -899,7 +970,10 @@ static slora_status adapter_begin(slora_pool* p, int64_t id, int32_t rank, const
         return fail(SLORA_ERR_OUT_OF_PAGES, "needed=%lld free=%lld", (long long)need, (long long)p->free_pages());
     const int64_t H = p->cfg.hidden;
     const int es = p->es;
-    const size_t tensor_max_bytes = size_t(std::max<int64_t>(H * rank, int64_t(rank) * p->P)) * es;
+    size_t tensor_max_bytes = 0;
+    for (int pr = 0; pr < p->np; ++pr)
+        for (int t = 0; t < 2; ++t) tensor_max_bytes = std::max(tensor_max_bytes, size_t(p->host_elems(pr, t, rank)) * es);
+    (void)H;
     if (p->dev && tensor_max_bytes + kJobBytes > kStageBytes)
         return fail(SLORA_ERR_SHAPE, "adapter tensor of %zu bytes exceeds staging", tensor_max_bytes);
     if (p->dev && size_t(need) * sizeof(int32_t) + 16 > kTabBytes)
@@ -1103,16 +1177,16 @@ extern "C" slora_status slora_batch_create(slora_pool_t p, slora_batch_t* out) {
     p->batches.insert(b);
     if (p->dev) {
         cudaError_t e = cudaEventCreateWithFlags(&b->upload_ev, cudaEventDisableTiming);
-        if (!e) e = cudaMalloc(&b->hdr_dev, sizeof(CallHdr) * 20);
-        if (!e) e = cudaMemset(b->hdr_dev, 0, sizeof(CallHdr) * 20);
-        if (!e) e = cudaHostAlloc(&b->hdr_host, sizeof(CallHdr) * 20, cudaHostAllocDefault);
+        if (!e) e = cudaMalloc(&b->hdr_dev, sizeof(CallHdr) * kMaxKc * kNpSlots);
+        if (!e) e = cudaMemset(b->hdr_dev, 0, sizeof(CallHdr) * kMaxKc * kNpSlots);
+        if (!e) e = cudaHostAlloc(&b->hdr_host, sizeof(CallHdr) * kMaxKc * kNpSlots, cudaHostAllocDefault);
         if (e) {
             if (b->hdr_dev) cudaFree(b->hdr_dev);
             p->batches.erase(b);
             delete b;
             return fail(SLORA_ERR_CUDA, "batch create: %s", cudaGetErrorString(e));
         }
-        memset(b->hdr_host, 0, sizeof(CallHdr) * 20);
+        memset(b->hdr_host, 0, sizeof(CallHdr) * kMaxKc * kNpSlots);
     }
     *out = b;
     return ok();
@@ -1169,7 +1243,7 @@ size_t arena_put(slora_batch* b, const void* src, size_t n, cudaStream_t, cudaEr
 void set_hdr(slora_pool* p, slora_batch* b, int kc, int np) {
     const slora_batch::Call& call = b->calls[kc][np];
     uint8_t* base = static_cast<uint8_t*>(b->arena_dev);
-    CallHdr& h = b->hdr_host[kc * 5 + np];
+    CallHdr& h = b->hdr_host[kc * kNpSlots + np];
     h.tok_idx = reinterpret_cast<const int32_t*>(base + b->off_tok);
     h.items = reinterpret_cast<const DevItem*>(base + call.off_items);
     h.pieces = reinterpret_cast<const DevPiece*>(base + call.off_pieces);
@@ -1192,7 +1266,7 @@ cudaError_t arena_flush(slora_batch* b, cudaStream_t s) {
                             static_cast<uint8_t*>(b->arena_host) + b->dirty_lo, b->dirty_hi - b->dirty_lo,
                             cudaMemcpyHostToDevice, s);
     b->dirty_lo = b->dirty_hi = 0;
-    if (!e) e = cudaMemcpyAsync(b->hdr_dev, b->hdr_host, sizeof(CallHdr) * 20, cudaMemcpyHostToDevice, s);
+    if (!e) e = cudaMemcpyAsync(b->hdr_dev, b->hdr_host, sizeof(CallHdr) * kMaxKc * kNpSlots, cudaMemcpyHostToDevice, s);
     if (!e) e = cudaEventRecord(b->upload_ev, s);
     b->upload_pending = true;
     return e;
@@ -1241,11 +1315,18 @@ void schedule_pieces(const std::vector<DevPiece>& in, const std::vector<int64_t>
 void build_call(slora_batch* b, const KernelCfg& k, int N, int nproj, uint32_t mask, slora_batch::Call& call) {
     call.items.clear();
     call.pieces.clear();
-    int proj_ids[4], np = 0;
-    for (int pj = 0; pj < 4; ++pj)
+    const slora_pool* pl = b->pool;
+    int proj_ids[kMaxProj], np = 0;
+    for (int pj = 0; pj < pl->np; ++pj)
         if (mask & (1u << pj)) proj_ids[np++] = pj;
     (void)nproj;
-    const int es = b->pool->es;
+    const int es = pl->es;
+    const int64_t P = pl->P;
+    // B-row width of projection pj in this call: its output width (TP: this rank's H/N slice)
+    auto proj_D = [&](int pj) -> int64_t { return N > 1 ? P : (k.mode == kShrink ? 0 : pl->pout[pj]); };
+    bool all_square = true;  // MBGMM serves square projections only
+    for (int i = 0; i < np; ++i)
+        all_square = all_square && pl->pin[proj_ids[i]] == pl->cfg.hidden && pl->pout[proj_ids[i]] == pl->cfg.hidden;
     // expand column chunk per item (SLORA_HIRANK_SPLIT=r: items of rank >= r get
     // half-width chunks; off by default: measured slower on C2, 1.45-1.52 vs 1.42 ms)
     static const int hirank = [] {
@@ -1260,20 +1341,27 @@ void build_call(slora_batch* b, const KernelCfg& k, int N, int nproj, uint32_t m
         const char* e = getenv("SLORA_O_HIRANK");
         return e ? atoi(e) : 32;
     }();
-    auto item_dchunk = [&](int rank) -> int64_t {
+    auto item_dchunk = [&](int rank) -> int64_t {  // divides the page (k.dchunk | P): pieces never straddle a page
         const int64_t half = k.dchunk / 2;
-        if (hirank > 0 && rank >= hirank && half > 0 && k.D % half == 0 && (half * es) % 16 == 0) return half;
-        if (o_hirank > 0 && np == 1 && rank >= o_hirank && half > 0 && k.D % half == 0 && (half * es) % 16 == 0)
+        if (hirank > 0 && rank >= hirank && half > 0 && P % half == 0 && (half * es) % 16 == 0) return half;
+        if (o_hirank > 0 && np == 1 && rank >= o_hirank && half > 0 && P % half == 0 && (half * es) % 16 == 0)
             return half;
         return k.dchunk;
     };
-    auto item_n_ep = [&](int rank) -> int64_t {
+    // expand pieces of one item: page by page over [0, D), chunks of dch within each page
+    auto for_expand_chunks = [&](int64_t D, int64_t dch, auto&& fn) {
+        if (dch <= 0) return;  // no expand configuration (bookkeeping pools)
+        for (int64_t p0 = 0; p0 < D; p0 += P)
+            for (int64_t c0 = p0; c0 < std::min(D, p0 + P); c0 += dch) fn(c0, std::min(dch, std::min(D, p0 + P) - c0));
+    };
+    auto item_n_ep = [&](int rank, int pj) -> int64_t {
         if (k.mode == kShrink || k.dchunk <= 0) return 0;
-        const int64_t dc = item_dchunk(rank);
-        return (k.D + dc - 1) / dc;
+        int64_t n = 0;
+        for_expand_chunks(proj_D(pj), item_dchunk(rank), [&](int64_t, int64_t) { ++n; });
+        return n;
     };
     const int srows = kShrinkRows;  // stored A rows per shrink piece
-    const bool use_runs = k.mode == kFused && b->n_runs > 0;
+    const bool use_runs = k.mode == kFused && b->n_runs > 0 && all_square;
     call.mg_s.clear();
     call.mg_e.clear();
     for (int si = 0; si < int(b->segs.size()); ++si) {
@@ -1304,7 +1392,7 @@ void build_call(slora_batch* b, const KernelCfg& k, int N, int nproj, uint32_t m
                     it.tok_off = s.tok_off + t0;
                     it.scale = s.scale;
                     it.n_sp = (k.mode == kExpand) ? 0 : (ra + srows - 1) / srows;
-                    it.n_ep = int32_t(item_n_ep(s.rank));
+                    it.n_ep = int32_t(item_n_ep(s.rank, proj));
                     call.items.push_back(it);
                 }
             if (!use_runs) continue;
@@ -1352,18 +1440,17 @@ void build_call(slora_batch* b, const KernelCfg& k, int N, int nproj, uint32_t m
                 cost.push_back(int64_t(nr) * k.K * es + kPieceOverhead);
             }
         if (k.mode != kShrink)
-            for (int64_t c0 = 0, dch = item_dchunk(it.rank); c0 < k.D; c0 += dch) {
-                const int64_t dc = std::min<int64_t>(dch, k.D - c0);
+            for_expand_chunks(proj_D(proj), item_dchunk(it.rank), [&](int64_t c0, int64_t dc) {
                 pieces.push_back({kPieceE, ii, int32_t(c0), int32_t(dc)});
                 cost.push_back(int64_t(it.rank) * dc * es + kPieceOverhead);
-            }
+            });
     }
     schedule_pieces(pieces, cost, k.grid, call.pieces, call.cta_off);
 }
 slora_status ensure_call(slora_pool* p, slora_batch* b, int kc, uint32_t mask, void* stream);
 
 // The single-GPU fused call's configuration: the ring-pipeline MBGMV kernel (kcfg[0]).
-int fused_kc(const slora_pool*, int) { return 0; }
+int fused_kc(const slora_pool* p, int) { return p->fused_kc(p->cfg.hidden); }
 }  // namespace
 
 extern "C" slora_status slora_batch_prepare(slora_batch_t b, const int64_t* tok_adapter, int32_t T, void* stream) {
@@ -1500,10 +1587,17 @@ extern "C" slora_status slora_batch_prepare(slora_batch_t b, const int64_t* tok_
     // for every call this prepare can see (items <= segs*4*chunks).
     int64_t chunks = 0;
     for (const DevSeg& s : b->segs) chunks += (s.n_tok + kItemTokCap - 1) / kItemTokCap;
-    const int64_t max_items = 4 * chunks;
+    const int64_t max_items = std::max(kNumProj, p->np) * chunks;
     // ring kernel: <= ceil(r/8) shrink pieces + D/(dchunk/2) expand pieces per item
     const int64_t dmin = std::max<int64_t>(1, p->kcfg[0].dchunk / 2);
-    const int64_t max_pieces_per_item = (kMaxRank + kShrinkRows - 1) / kShrinkRows + (p->cfg.hidden + dmin - 1) / dmin;
+    int64_t max_out = p->cfg.hidden, max_in = p->cfg.hidden;
+    for (int q = 0; q < p->np; ++q) {
+        max_out = std::max(max_out, p->pout[q]);
+        max_in = std::max(max_in, p->pin[q]);
+    }
+    (void)max_in;
+    const int64_t max_pieces_per_item =
+        (kMaxRank + kShrinkRows - 1) / kShrinkRows + (max_out + dmin - 1) / dmin + (max_out + p->P - 1) / p->P;
     int n_shapes = 6;  // eager shapes + those launched since create (rebuilt below)
     for (auto& row : b->used_masks)
         for (uint32_t m : row) n_shapes += m ? 1 : 0;
@@ -1539,7 +1633,7 @@ extern "C" slora_status slora_batch_prepare(slora_batch_t b, const int64_t* tok_
     // workspace slot = three regions of ws_need floats: the ring kernel's v,
     // the warp-task kernel's v (readiness flags, kept "empty" between
     // launches) and MBGMM's v
-    const int64_t ws_need = 4 * b->NR + 64;
+    const int64_t ws_need = std::max(kNumProj, p->np) * b->NR + 64;
     if (sync_need > p->sync_stride) {
         if (p->sync_dev) CUDA_TRY(cudaFreeAsync(p->sync_dev, s));
         const int64_t st = sync_need * 2;
@@ -1593,8 +1687,8 @@ extern "C" slora_status slora_batch_prepare(slora_batch_t b, const int64_t* tok_
     // every call shape launched since the batch was created is rebuilt too, and all headers
     // are uploaded with the descriptors in one flush: a CUDA graph that captured those
     // launches replays the new batch (MBGMV path; see slora_batch_get_info().graph_ok)
-    for (int kc = 0; kc < 4 && !st2; ++kc)
-        for (int np = 1; np <= 4 && !st2; ++np)
+    for (int kc = 0; kc < p->n_kcfg && !st2; ++kc)
+        for (int np = 1; np <= kMaxProj && !st2; ++np)
             if (b->used_masks[kc][np] && p->kcfg[kc].ok) st2 = ensure_call(p, b, kc, b->used_masks[kc][np], stream);
     b->in_prepare = false;
     if (st2) return st2;
@@ -1630,8 +1724,28 @@ slora_status common_checks(slora_pool* p, slora_batch* b, int32_t layer, uint32_
     if (!b->prepared) return fail(SLORA_ERR_INVALID_ARG, "batch not prepared");
     if (b->epoch != p->epoch) return fail(SLORA_ERR_STALE_HANDLE, "batch prepared before an eviction");
     if (layer < 0 || layer >= p->cfg.num_layers) return fail(SLORA_ERR_INVALID_ARG, "layer %d", layer);
-    if (mask == 0 || mask > 0xF) return fail(SLORA_ERR_INVALID_ARG, "proj_mask 0x%x", mask);
+    if (mask == 0 || (mask >> p->np)) return fail(SLORA_ERR_INVALID_ARG, "proj_mask 0x%x (%d projections)", mask, p->np);
+    int64_t K = -1;  // the projections of one call read the same x
+    for (int pj = 0; pj < p->np; ++pj)
+        if (mask & (1u << pj)) {
+            if (K >= 0 && p->pin[pj] != K)
+                return fail(SLORA_ERR_SHAPE, "proj_mask 0x%x mixes input widths (%lld, %lld)", mask, (long long)K,
+                            (long long)p->pin[pj]);
+            K = p->pin[pj];
+        }
     return SLORA_OK;
+}
+
+int popcount_mask(uint32_t mask) {
+    int n = 0;
+    for (int pj = 0; pj < kMaxProj; ++pj) n += (mask >> pj) & 1;
+    return n;
+}
+// input width of a call's projections (common_checks makes them agree)
+int64_t mask_in(const slora_pool* p, uint32_t mask) {
+    for (int pj = 0; pj < p->np; ++pj)
+        if (mask & (1u << pj)) return p->pin[pj];
+    return p->cfg.hidden;
 }
 
 bool aligned16(const void* ptr, int64_t ld, int es) {
@@ -1642,8 +1756,7 @@ bool aligned16(const void* ptr, int64_t ld, int es) {
 // yet (prepare builds the usual q/k/v and o calls eagerly so that a captured
 // CUDA graph of the layer sequence contains kernel launches only).
 slora_status ensure_call(slora_pool* p, slora_batch* b, int kc, uint32_t mask, void* stream) {
-    int np = 0;
-    for (int pj = 0; pj < 4; ++pj) np += (mask >> pj) & 1;
+    const int np = popcount_mask(mask);
     slora_batch::Call& call = b->calls[kc][np];
     if (call.built && call.mask == mask) return SLORA_OK;
     if (!p->kcfg[kc].ok) return fail(SLORA_ERR_SHAPE, "no valid kernel configuration");
@@ -1683,7 +1796,7 @@ slora_status prepare_call(slora_pool* p, slora_batch* b, int kc, int32_t layer, 
                            (long long)k.D);
     memset(&q, 0, sizeof(q));
     int np = 0;
-    for (int pj = 0; pj < 4; ++pj)
+    for (int pj = 0; pj < p->np; ++pj)
         if (mask & (1u << pj)) q.proj_ids[np++] = pj;
     q.nproj = np;
     // descriptors depend on the mask only through np and which projections
@@ -1696,7 +1809,7 @@ slora_status prepare_call(slora_pool* p, slora_batch* b, int kc, int32_t layer, 
     b->used_masks[kc][np] = mask;
     q.pool = p->cfg.device_buffer;
     q.page_elems = p->P;
-    q.hdr = b->hdr_dev + (kc * 5 + np);
+    q.hdr = b->hdr_dev + (kc * kNpSlots + np);
     const uint64_t slot = p->launch_seq++ % kLaunchSlots;
     q.slot = int32_t(slot);
     q.layer = layer;
@@ -1709,9 +1822,15 @@ slora_status prepare_call(slora_pool* p, slora_batch* b, int kc, int32_t layer, 
     }();
     q.dbg = dbg;
     const int N = p->N();
-    for (int pj = 0; pj < 4; ++pj) {
-        q.a_div[pj] = (pj < 3) ? N : 1;
-        q.a_row_pages[pj] = (pj < 3) ? N : 1;
+    q.layer_units = p->layer_units;
+    for (int pj = 0; pj < p->np; ++pj) {
+        int rows, ch;
+        p->tensor_shape(pj, 0, N, rows, ch);
+        q.a_div[pj] = (N > 1 && pj < 3) ? N : 1;
+        q.a_row_pages[pj] = ch;
+        q.a_units[pj] = p->a_units[pj];
+        q.b_row_pages[pj] = p->b_row_pages[pj];
+        q.proj_off[pj] = p->proj_off[pj];
     }
     p->ws_slot_base = p->ws_dev + int64_t(slot) * p->ws_stride;  // MBGMM's regions of the slot (host-baked)
     q.trace = p->trace_dev;
@@ -1791,27 +1910,27 @@ slora_status launch_mbgmm_pair(slora_pool* p, slora_batch* b, const slora_batch:
 }  // namespace
 
 extern "C" slora_status slora_lora_apply(slora_pool_t p, slora_batch_t b, int32_t layer, uint32_t mask,
-                                         const void* x, int64_t ldx, void* const y[4], const int64_t ldy[4],
+                                         const void* x, int64_t ldx, void* const y[SLORA_MAX_PROJ], const int64_t ldy[SLORA_MAX_PROJ],
                                          void* stream) {
     slora_status st = common_checks(p, b, layer, mask);
     if (st) return st;
     if (p->N() != 1) return fail(SLORA_ERR_INVALID_ARG, "slora_lora_apply is single-GPU; use shrink/expand under TP");
     if (b->adapted == 0) return ok();
     if (!x || !y || !ldy) return fail(SLORA_ERR_INVALID_ARG, "null x/y");
-    if (!aligned16(x, ldx, p->es) || ldx < p->cfg.hidden) return fail(SLORA_ERR_SHAPE, "x alignment/stride");
-    for (int pj = 0; pj < 4; ++pj)
+    const int64_t K = mask_in(p, mask);
+    if (!aligned16(x, ldx, p->es) || ldx < K) return fail(SLORA_ERR_SHAPE, "x alignment/stride");
+    for (int pj = 0; pj < p->np; ++pj)
         if (mask & (1u << pj))
-            if (!y[pj] || !aligned16(y[pj], ldy[pj], p->es) || ldy[pj] < p->cfg.hidden)
+            if (!y[pj] || !aligned16(y[pj], ldy[pj], p->es) || ldy[pj] < p->pout[pj])
                 return fail(SLORA_ERR_SHAPE, "y[%d] alignment/stride", pj);
-    int np = 0;
-    for (int pj = 0; pj < 4; ++pj) np += (mask >> pj) & 1;
-    const int kc = fused_kc(p, np);
+    const int kc = p->fused_kc(K);
+    if (kc < 0) return fail(SLORA_ERR_SHAPE, "no fused kernel configuration for input width %lld", (long long)K);
     LoraParams q;
     st = prepare_call(p, b, kc, layer, mask, stream, q);
     if (st) return st;
     q.x = x;
     q.ldx = ldx;
-    for (int pj = 0; pj < 4; ++pj) {
+    for (int pj = 0; pj < p->np; ++pj) {
         q.y[pj] = y[pj];
         q.ldy[pj] = ldy[pj];
     }
@@ -1826,9 +1945,8 @@ extern "C" slora_status slora_lora_apply(slora_pool_t p, slora_batch_t b, int32_
 
 extern "C" slora_status slora_lora_v_elems(slora_batch_t b, uint32_t mask, int32_t div, int64_t* out) {
     if (!b || !out) return fail(SLORA_ERR_INVALID_ARG, "null argument");
-    if (mask == 0 || mask > 0xF || div < 1) return fail(SLORA_ERR_INVALID_ARG, "mask/div");
-    int np = 0;
-    for (int pj = 0; pj < 4; ++pj) np += (mask >> pj) & 1;
+    if (mask == 0 || (mask >> kMaxProj) || div < 1) return fail(SLORA_ERR_INVALID_ARG, "mask/div");
+    const int np = popcount_mask(mask);
     if (b->NR % div) return fail(SLORA_ERR_INDIVISIBLE, "NR %% div");
     *out = int64_t(np) * (b->NR / div);
     return ok();
@@ -1844,6 +1962,8 @@ extern "C" slora_status slora_lora_shrink(slora_pool_t p, slora_batch_t b, int32
     if (b->adapted == 0) return ok();
     const int kc = (N > 1 && (mask & 0x8)) ? 2 : 1;
     const int64_t K = p->kcfg[kc].K;
+    if (N == 1 && mask_in(p, mask) != K)
+        return fail(SLORA_ERR_SHAPE, "split shrink serves input width %lld only", (long long)K);
     if (!x || !v) return fail(SLORA_ERR_INVALID_ARG, "null x/v");
     if (!aligned16(x, ldx, p->es) || ldx < K) return fail(SLORA_ERR_SHAPE, "x alignment/stride");
     LoraParams q;
@@ -1856,7 +1976,7 @@ extern "C" slora_status slora_lora_shrink(slora_pool_t p, slora_batch_t b, int32
 }
 
 extern "C" slora_status slora_lora_expand(slora_pool_t p, slora_batch_t b, int32_t layer, uint32_t mask,
-                                          const float* v, int32_t v_blocks, void* const y[4], const int64_t ldy[4],
+                                          const float* v, int32_t v_blocks, void* const y[SLORA_MAX_PROJ], const int64_t ldy[SLORA_MAX_PROJ],
                                           void* stream) {
     slora_status st = common_checks(p, b, layer, mask);
     if (st) return st;
@@ -1865,16 +1985,16 @@ extern "C" slora_status slora_lora_expand(slora_pool_t p, slora_batch_t b, int32
     for (const DevSeg& s : b->segs)
         if (s.rank % v_blocks) return fail(SLORA_ERR_INDIVISIBLE, "rank %d %% v_blocks %d", s.rank, v_blocks);
     if (!v || !y || !ldy) return fail(SLORA_ERR_INVALID_ARG, "null v/y");
-    for (int pj = 0; pj < 4; ++pj)
+    for (int pj = 0; pj < p->np; ++pj)
         if (mask & (1u << pj))
-            if (!y[pj] || !aligned16(y[pj], ldy[pj], p->es) || ldy[pj] < p->P)
+            if (!y[pj] || !aligned16(y[pj], ldy[pj], p->es) || ldy[pj] < (p->N() > 1 ? p->P : p->pout[pj]))
                 return fail(SLORA_ERR_SHAPE, "y[%d] alignment/stride", pj);
     LoraParams q;
     st = prepare_call(p, b, 3, layer, mask, stream, q);
     if (st) return st;
     q.v_in = v;
     q.v_blocks = v_blocks;
-    for (int pj = 0; pj < 4; ++pj) {
+    for (int pj = 0; pj < p->np; ++pj) {
         q.y[pj] = y[pj];
         q.ldy[pj] = ldy[pj];
     }

@@ -249,7 +249,7 @@ __device__ __forceinline__ void dot16<float>(const uint4& a, const uint4& x, flo
 // ------------------------------------------------------------ smem layout
 constexpr int kMaxPiecePages = kMaxRank > kShrinkRows * kMaxChunks ? kMaxRank : kShrinkRows * kMaxChunks;
 struct PieceMeta {
-    int32_t kind, item, nt, r, ra, row0, nrows, dcol0, dcols, proj, arp, n_sp, n_ep;
+    int32_t kind, item, nt, r, ra, row0, nrows, dcol0, dcols, doff, proj, arp, n_sp, n_ep;
     float scale;
     int32_t pi;                   // projection index in the call's mask order
     int64_t vbase;                // v index of (token 0, rank row 0) of this item
@@ -965,12 +965,18 @@ __global__ void __launch_bounds__(kThreads, 1) mbgmv_kernel(const __grid_constan
                 const int proj = p.proj_ids[pi];
                 const int div = (MODE == kExpand) ? 1 : p.a_div[proj];
                 const int arp = (MODE == kExpand) ? 1 : p.a_row_pages[proj];
-                const int32_t* tab = itab + int64_t((p.layer * 4 + proj) * 2) * rank;
+                // the adapter's tables of (layer, proj): A entries (stored rows x arp), then B (r x brp)
+                const int32_t* tab = itab + int64_t(rank) * (int64_t(p.layer) * p.layer_units + p.proj_off[proj]);
+                int doff = 0;
                 if (lane < nt) M.tok[lane] = H.tok_idx[tok_off + lane];
                 if (kind == kPieceS) {
-                    for (int w = lane; w < pbn * arp; w += 32) M.pages[w] = tab[(pa + w / arp) * arp + w % arp];
-                } else {
-                    for (int w = lane; w < rank; w += 32) M.pages[w] = tab[rank + w];
+                    for (int w = lane; w < pbn * arp; w += 32) M.pages[w] = tab[pa * arp + w];
+                } else {  // B rows' pages of the piece's page column (its columns never straddle a page)
+                    const int brp = p.b_row_pages[proj];
+                    const int c = int(pa / P);
+                    doff = pa - int(c * P);
+                    const int32_t* tb = tab + int64_t(rank) * p.a_units[proj] + c;
+                    for (int w = lane; w < rank; w += 32) M.pages[w] = tb[w * brp];
                 }
                 if (lane == q) {
                     M.kind = kind;
@@ -988,6 +994,7 @@ __global__ void __launch_bounds__(kThreads, 1) mbgmv_kernel(const __grid_constan
                     M.vrow = itl.vrow;
                     M.row0 = M.dcol0 = pa;
                     M.nrows = M.dcols = pbn;
+                    M.doff = doff;
                 }
                 __syncwarp();
                 if (lane == 0 && i < 48) TRACE(16 + i);
@@ -1062,7 +1069,7 @@ __global__ void __launch_bounds__(kThreads, 1) mbgmv_kernel(const __grid_constan
                     }
                 } else {
                     for (int q = lane; q < nrow; q += 32)
-                        bulk_g2s(sbase + size_t(q) * (rowb + 16), pool + int64_t(M.pages[base + q]) * P + M.dcol0, rowb,
+                        bulk_g2s(sbase + size_t(q) * (rowb + 16), pool + int64_t(M.pages[base + q]) * P + M.doff, rowb,
                                  &full[rg.slot]);
                 }
                 rg.advance(ns);
@@ -1202,9 +1209,9 @@ __global__ void __launch_bounds__(kThreads, 1) mbgmv_kernel(const __grid_constan
                     shrink_piece_mma<T>(p, M, ring, SS, reinterpret_cast<const unsigned char*>(xsm), zero16, int(K),
                                         srow, lg_rps, full, empty, rg, ns, &xempty[xb], rd, vout, warp, lane, i);
                 } else
-                switch (M.nt * 8 + (xvn <= 1 ? 1 : (xvn == 2 ? 2 : 4))) {
+                switch (M.nt * 16 + (xvn <= 1 ? 1 : (xvn == 2 ? 2 : (xvn <= 4 ? 4 : 8)))) {
 #define SLORA_SHRINK_CASE(N, X)                                                                                  \
-    case N * 8 + X:                                                                                            \
+    case N * 16 + X:                                                                                           \
         shrink_piece<T, N, X>(p, M, ring, SS, xsm, nvec, srow, rps_s, full, empty, rg, ns, &xempty[xb], rd,      \
                               vout, warp, lane, i);                                                             \
         break;
@@ -1212,9 +1219,9 @@ __global__ void __launch_bounds__(kThreads, 1) mbgmv_kernel(const __grid_constan
                     SLORA_SHRINK_CASE(1, 2)
 #else
                     // only the token counts an item can have (NT <= kItemTokCap)
-                    SLORA_SHRINK_CASE(1, 1) SLORA_SHRINK_CASE(1, 2) SLORA_SHRINK_CASE(1, 4)
+                    SLORA_SHRINK_CASE(1, 1) SLORA_SHRINK_CASE(1, 2) SLORA_SHRINK_CASE(1, 4) SLORA_SHRINK_CASE(1, 8)
 #if SLORA_ITEM_TOK >= 2
-                    SLORA_SHRINK_CASE(2, 1) SLORA_SHRINK_CASE(2, 2) SLORA_SHRINK_CASE(2, 4)
+                    SLORA_SHRINK_CASE(2, 1) SLORA_SHRINK_CASE(2, 2) SLORA_SHRINK_CASE(2, 4) SLORA_SHRINK_CASE(2, 8)
 #endif
 #if SLORA_ITEM_TOK >= 3
                     SLORA_SHRINK_CASE(3, 1) SLORA_SHRINK_CASE(3, 2) SLORA_SHRINK_CASE(3, 4)
@@ -1409,22 +1416,23 @@ __global__ void __launch_bounds__(256, 8) scatter_kernel(const T* __restrict__ s
                 }
             }
         } else {
-            // B: row j (cols = P elements) -> page j, 16-byte vectors
+            // B: row j (cols elements) -> its row_pages pages (element e: page e / P, offset e % P),
+            // 16-byte vectors (a vector never straddles a page: P % VE == 0)
             const int64_t nv = jb.cols / VE;
             const bool vec = (jb.cols % VE) == 0 && (jb.src_off % VE) == 0 && (P % VE) == 0;
             if (vec) {
                 for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < int64_t(jb.rows) * nv;
                      i += int64_t(gridDim.x) * blockDim.x) {
-                    const int64_t j = i / nv, e = i % nv;
-                    reinterpret_cast<uint4*>(pool + int64_t(jb.pages[j]) * P)[e] =
-                        reinterpret_cast<const uint4*>(src + j * jb.cols)[e];
+                    const int64_t j = i / nv, e = (i % nv) * VE;
+                    *reinterpret_cast<uint4*>(pool + int64_t(jb.pages[j * jb.row_pages + e / P]) * P + e % P) =
+                        reinterpret_cast<const uint4*>(src + j * jb.cols)[e / VE];
                 }
             } else {
                 const int64_t n = int64_t(jb.rows) * jb.cols;
                 for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
                      i += int64_t(gridDim.x) * blockDim.x) {
                     const int64_t j = i / jb.cols, e = i % jb.cols;
-                    pool[int64_t(jb.pages[j]) * P + e] = src[i];
+                    pool[int64_t(jb.pages[j * jb.row_pages + e / P]) * P + e % P] = src[i];
                 }
             }
         }

@@ -59,6 +59,7 @@ static_assert(sizeof(DevPiece) == 16, "DevPiece layout");
 // the Zipf-head items, whose expand pieces were the stragglers.
 constexpr int kItemTokCap = SLORA_ITEM_TOK;
 constexpr int kMaxRank = 64;     // max rank of the MBGMV path
+constexpr int kMaxProj = 8;      // LoRA'd projections per layer (q,k,v,o by default; NEXT-4: + MLP)
 #ifndef SLORA_SHRINK_ROWS
 #define SLORA_SHRINK_ROWS 8
 #endif
@@ -116,17 +117,22 @@ struct LoraParams {
     const CallHdr* hdr;           // the call's descriptor header (batch_prepare rewrites it)
     int32_t slot;                 // rotating launch slot: sync counters / workspace of this launch
     int32_t nproj;
-    int32_t proj_ids[4];
+    int32_t proj_ids[kMaxProj];
     int32_t layer;
-    int32_t K, D;                 // stored A-row length, B-row length (elements)
-    int32_t a_div[4];             // A rank columns stored = r / a_div[p]
-    int32_t a_row_pages[4];       // pages per stored A row
+    int32_t K, D;                 // stored A-row length (the call's input width), config B width
+    int32_t a_div[kMaxProj];      // A rank columns stored = r / a_div[p]
+    int32_t a_row_pages[kMaxProj];  // pages per stored A row
+    int32_t b_row_pages[kMaxProj];  // pages per stored B row (NEXT-4: d_out > page)
+    int32_t proj_off[kMaxProj];   // projection p's page tables within a layer, in units of the rank:
+    int32_t layer_units;          //   tab(layer, p) = adapter table + r * (layer * layer_units + proj_off[p]);
+                                  //   A entries [0, r*a_row_pages*stored/r), B after them (r x b_row_pages)
+    int32_t a_units[kMaxProj];    // A entries per rank unit (B starts at r * a_units[p])
     int32_t ns;                   // ring slots
     int32_t dbg;                  // debug: bit0 skip shrink math, bit1 skip expand math
     const void* x;
     int64_t ldx;
-    void* y[4];
-    int64_t ldy[4];
+    void* y[kMaxProj];
+    int64_t ldy[kMaxProj];
     long long* trace;             // debug: per-CTA event timestamps (nullptr = off)
     float* v;                     // shrink output (split mode; C-ABI v layout, div as stored); fused: nullptr
     const float* v_in;            // expand input
@@ -177,9 +183,9 @@ struct alignas(64) MgParams {
     int64_t page_elems;
     const MgUnit* units;
     float* v;            // the call's fp32 workspace (MBGMV layout)
-    void* y[4];
-    int64_t ldy[4];
-    int32_t proj_ids[4];
+    void* y[kMaxProj];
+    int64_t ldy[kMaxProj];
+    int32_t proj_ids[kMaxProj];
     int32_t layer, K;
     int32_t ksplit;      // shrink k-split parts (unit.pad = part); the expand sums them in order
     int64_t vpart;       // floats between the parts' v regions
@@ -206,7 +212,7 @@ struct ScatterJob {
                         // 1 = B shard (rows x P row-major)
     int32_t rows;       // A: Krows (input rows of the shard); B: rank rows
     int32_t cols;       // A: stored rank columns; B: P
-    int32_t row_pages;  // A: pages per stored row (Krows / P); B: 1
+    int32_t row_pages;  // pages per stored row: A ceil(Krows / P) (TP q/k/v: N), B ceil(cols / P)
 };
 cudaError_t launch_scatter(const void* staging, const ScatterJob* jobs_dev, int n_jobs, void* pool,
                            int64_t page_elems, int esize, cudaStream_t s);

@@ -19,7 +19,7 @@ LIB_PATH = os.environ.get("SLORA_LIB") or os.path.join(_HERE, "libslora.so")  # 
 
 DTYPES = {"f32": 0, "f16": 1, "bf16": 2}
 ESIZE = {"f32": 4, "f16": 2, "bf16": 2}
-PROJ_BITS = {"q": 1, "k": 2, "v": 4, "o": 8}
+PROJ_BITS = {"q": 1, "k": 2, "v": 4, "o": 8}  # + projection indices 0..7 (ints) for proj_dims pools
 
 STATUS = {
     0: "OK", 1: "INVALID_ARG", 2: "SHAPE", 3: "OUT_OF_PAGES", 4: "ALREADY_RESIDENT",
@@ -42,7 +42,8 @@ class PoolConfig(ctypes.Structure):
                 ("num_layers", ctypes.c_int32), ("tp_size", ctypes.c_int32), ("tp_rank", ctypes.c_int32),
                 ("capacity_pages", ctypes.c_int64), ("device_buffer", ctypes.c_void_p),
                 ("device_buffer_bytes", ctypes.c_int64), ("max_adapters", ctypes.c_int32),
-                ("alloc_order", ctypes.c_int), ("seed", ctypes.c_uint64)]
+                ("alloc_order", ctypes.c_int), ("seed", ctypes.c_uint64), ("num_proj", ctypes.c_int32),
+                ("proj_in", ctypes.c_int64 * 8), ("proj_out", ctypes.c_int64 * 8)]
 
 
 class FragReport(ctypes.Structure):
@@ -175,7 +176,7 @@ def mask_of(projs) -> int:
         return projs
     m = 0
     for p in projs:
-        m |= PROJ_BITS[p]
+        m |= (1 << p) if isinstance(p, int) else PROJ_BITS[p]
     return m
 
 
@@ -184,8 +185,10 @@ class Pool:
 
     def __init__(self, hidden: int, num_layers: int, capacity_pages: int, dtype: str = "f16",
                  device: int = 0, buffer=None, tp_size: int = 1, tp_rank: int = 0,
-                 max_adapters: int = 1024, order: str = "ascending", seed: int = 0):
+                 max_adapters: int = 1024, order: str = "ascending", seed: int = 0, proj_dims=None):
+        """proj_dims: [(in, out)] per LoRA'd projection (NEXT-4); None = q,k,v,o square."""
         self.hidden, self.num_layers, self.dtype = hidden, num_layers, dtype
+        self.proj_dims = [(hidden, hidden)] * 4 if proj_dims is None else [tuple(d) for d in proj_dims]
         self.tp_size, self.tp_rank = tp_size, tp_rank
         self.page_elems = hidden // tp_size
         self.capacity = capacity_pages
@@ -198,9 +201,12 @@ class Pool:
             self.buffer = torch.empty(nbytes, dtype=torch.uint8, device=f"cuda:{device}")
         if self.buffer is not None:
             nbytes = self.buffer.numel() * self.buffer.element_size()
+        pin = (ctypes.c_int64 * 8)(*([d[0] for d in self.proj_dims] + [0] * (8 - len(self.proj_dims))))
+        pout = (ctypes.c_int64 * 8)(*([d[1] for d in self.proj_dims] + [0] * (8 - len(self.proj_dims))))
         cfg = PoolConfig(device, DTYPES[dtype], hidden, num_layers, tp_size, tp_rank, capacity_pages,
                          _ptr(self.buffer) or None, nbytes, max_adapters,
-                         {"ascending": 0, "shuffle": 1}[order], seed)
+                         {"ascending": 0, "shuffle": 1}[order], seed,
+                         0 if proj_dims is None else len(self.proj_dims), pin, pout)
         h = _VP()
         self._inflight, self._retired = {}, []
         _check(lib().slora_pool_create(ctypes.byref(cfg), ctypes.byref(h)))
@@ -224,7 +230,7 @@ class Pool:
         if host_w is None:
             return None, None
         want_item = ESIZE[self.dtype]
-        need = self.num_layers * 4 * 2 * self.hidden * rank * want_item
+        need = self.num_layers * sum(i + o for i, o in self.proj_dims) * rank * want_item
         if hasattr(host_w, "data_ptr"):  # torch CPU tensor
             import torch
             ok = {"f32": (torch.float32,), "f16": (torch.float16,),
@@ -401,12 +407,13 @@ class Batch:
 
     @staticmethod
     def _ys(ys, ldys):
-        yp = (_VP * 4)(*[_ptr(y) or None for y in ys])
-        ld = (_I64 * 4)(*ldys)
+        ys, ldys = list(ys) + [None] * (8 - len(ys)), list(ldys) + [0] * (8 - len(ldys))
+        yp = (_VP * 8)(*[_ptr(y) or None for y in ys])
+        ld = (_I64 * 8)(*ldys)
         return yp, ld
 
     def apply(self, layer: int, projs, x, ldx: int, ys, ldys, stream=None) -> None:
-        """Fused shrink->expand (one GPU): ys/ldys are length-4 (q,k,v,o)."""
+        """Fused shrink->expand (one GPU): ys/ldys indexed by projection id (q,k,v,o, then proj_dims extras)."""
         yp, ld = self._ys(ys, ldys)
         _check(lib().slora_lora_apply(self.pool.h, self.h, layer, mask_of(projs), _ptr(x), ldx, yp, ld,
                                       _stream(stream)))

@@ -41,6 +41,7 @@ class Config:
     num_layers: int = 32
     fixed_requests: list | None = None  # C0: explicit (adapter, length) list
     notes: str = ""
+    proj_dims: tuple | None = None   # NEXT-4: (h_in, d_out) per LoRA'd projection; None = q,k,v,o square
 
 
 CONFIGS = {
@@ -60,7 +61,17 @@ CONFIGS = {
     # configs[4]: Llama-70B (h=8192) 8-way TP, rank 64, decode 256, bf16 (n=10)
     "c4": Config("c4-70b-tp8-r64-decode256-bf16", 4, 8192, 10, (64,), "bf16", 1.0, 256, tp=8,
                  num_layers=80),
+    # NEXT-4 (P:321-327 takes the MLP as its example): C2's batch with LoRA on all seven Llama-7B
+    # projections, q/k/v/o 4096 -> 4096, gate/up 4096 -> 11008, down 11008 -> 4096 (Table model_setting
+    # P:369-378 gives the 7B shapes); index 2: the same batch and attention weights as C2
+    "c2-mlp": Config("c2-7b-qkvo+mlp-decode64-fp16", 2, 4096, 2000, (64, 32, 16, 8), "f16", 1.0, 64,
+                     proj_dims=((4096, 4096),) * 4 + ((4096, 11008), (4096, 11008), (11008, 4096))),
 }
+
+
+def proj_dims(cfg: Config) -> list:
+    """(h_in, d_out) of each LoRA'd projection of the config."""
+    return [(cfg.hidden, cfg.hidden)] * 4 if cfg.proj_dims is None else [tuple(d) for d in cfg.proj_dims]
 
 
 def adapter_rank(cfg: Config, adapter: int) -> int:
@@ -145,9 +156,9 @@ def _normal(rng, shape, std):
 def adapter_weights(cfg: Config, adapter: int, layer: int, proj: int, rank: int | None = None,
                     seed_offset: int = 0):
     """(A: h x r, B: r x d) for one (adapter, layer, projection), stored dtype.
-    A ~ N(0, 1/h), B ~ N(0, 1/r)."""
+    A ~ N(0, 1/h), B ~ N(0, 1/r); h, d = the projection's dims (proj_dims)."""
     r = adapter_rank(cfg, adapter) if rank is None else rank
-    h = d = cfg.hidden
+    h, d = proj_dims(cfg)[proj]
     rng = np.random.default_rng([DATA_SEED + cfg.index, 7 + seed_offset, adapter, layer, proj])
     A = _normal(rng, (h, r), 1.0 / np.sqrt(h))
     B = _normal(rng, (r, d), 1.0 / np.sqrt(r))
@@ -157,11 +168,11 @@ def adapter_weights(cfg: Config, adapter: int, layer: int, proj: int, rank: int 
 def adapter_host_buffer(cfg: Config, adapter: int, num_layers: int, rank: int | None = None,
                         seed_offset: int = 0) -> np.ndarray:
     """Dense host buffer in the C-ABI's canonical layout (include/slora.h):
-    for layer l, for projection p in (q,k,v,o): A (h x r row-major) then
-    B (r x d row-major), contiguous."""
+    for layer l, for projection p (q,k,v,o, then any proj_dims extras): A
+    (h_p x r row-major) then B (r x d_p row-major), contiguous."""
     parts = []
     for l in range(num_layers):
-        for p in range(4):
+        for p in range(len(proj_dims(cfg))):
             A, B = adapter_weights(cfg, adapter, l, p, rank, seed_offset)
             parts.append(A.ravel())
             parts.append(B.ravel())

@@ -29,11 +29,17 @@ def test_library_exports_every_declared_symbol():
     assert set(sl.SIGNATURES) <= set(names)
 
 
-def mk(cap, hidden=8, L=2, tp=1, rank=0, order="ascending", seed=0, max_ad=64):
+def mk(cap, hidden=8, L=2, tp=1, rank=0, order="ascending", seed=0, max_ad=64, dims=None):
     c = sl.Pool(hidden, L, cap, dtype="f16", device=-1, tp_size=tp, tp_rank=rank, order=order, seed=seed,
-                max_adapters=max_ad)
-    m = pm.PoolModel(cap, hidden, L, tp_size=tp, tp_rank=rank, order=order, seed=seed, max_adapters=max_ad)
+                max_adapters=max_ad, proj_dims=dims)
+    m = pm.PoolModel(cap, hidden, L, tp_size=tp, tp_rank=rank, order=order, seed=seed, max_adapters=max_ad,
+                     proj_dims=dims)
     return c, m
+
+
+# NEXT-4 shapes at hidden 16: q, GQA k/v (16 -> 8), o, MLP gate/up (16 -> 40: 3 pages per B row),
+# down (40 -> 16: 3 pages per stored A row)
+MLP_DIMS = [(16, 16), (16, 8), (16, 8), (16, 16), (16, 40), (16, 40), (40, 16)]
 
 
 def same_outcome(fc, fm):
@@ -67,9 +73,10 @@ def compare_state(c, m):
                 assert c.kv_pages(rid, l, kind).tolist() == hd.pages[(l, kind)]
 
 
-@pytest.mark.parametrize("order,tp,rank", [("ascending", 1, 0), ("shuffle", 1, 0), ("shuffle", 4, 3)])
-def test_pool_matches_model_random_ops(order, tp, rank):
-    c, m = mk(2500, hidden=16, L=2, tp=tp, rank=rank, order=order, seed=99)
+@pytest.mark.parametrize("order,tp,rank,dims", [("ascending", 1, 0, None), ("shuffle", 1, 0, None),
+                                                ("shuffle", 4, 3, None), ("shuffle", 1, 0, MLP_DIMS)])
+def test_pool_matches_model_random_ops(order, tp, rank, dims):
+    c, m = mk(2500, hidden=16, L=2, tp=tp, rank=rank, order=order, seed=99, dims=dims)
     rng = np.random.default_rng(7)
     nid = 0
     for step in range(10_000):
@@ -156,6 +163,7 @@ def test_adapter_load_validates_host_buffer():
     import paper_2311_03285_b200.slora as sl2
     p = sl2.Pool.__new__(sl2.Pool)  # a device pool's attributes without creating one
     p.dtype, p.num_layers, p.hidden, p.device, p.h = "f16", 1, 64, 0, None
+    p.proj_dims = [(64, 64)] * 4
     good = np.zeros(1 * 4 * 2 * 64 * 4, np.float16)
     with pytest.raises(ValueError):
         p.adapter_load(1, 4, good.astype(np.float32))  # wider dtype
@@ -216,3 +224,26 @@ def test_prefetch_on_bookkeeping_pool():
         b.adapter_wait(9)
     assert e.value.name == "NOT_RESIDENT"
     assert b.loader_stats()["loads"] == 0
+
+
+def test_projection_shapes_page_accounting():
+    """NEXT-4 (reading R2): a stored row of n elements takes ceil(n / H) pages.  Square
+    projections reduce to P:262 (a rank-R tensor takes R pages: 8R per layer for q,k,v,o);
+    the C++ pool claims exactly the model's pages, in claim order layer, proj, tensor, row, chunk;
+    TP with non-square projections and rows of more than 8 pages are refused."""
+    H, L, r = 16, 3, 4
+    c, m = mk(4096, hidden=H, L=L, dims=MLP_DIMS)
+    want = L * r * sum(-(-i // H) + -(-o // H) for i, o in MLP_DIMS)
+    assert m.adapter_page_count(r) == want == L * r * (2 + 2 + 2 + 2 + 4 + 4 + 4)
+    c.adapter_load(5, r)
+    m.adapter_load(5, r)
+    assert c.adapter_pages(5).tolist() == m.adapters[5].pages
+    assert len(m.adapters[5].pages) == want
+    sq, msq = mk(4096, hidden=H, L=L)
+    assert msq.adapter_page_count(r) == L * 8 * r
+    with pytest.raises(sl.SloraError) as e:
+        mk(64, hidden=H, L=1, tp=2, dims=MLP_DIMS)
+    assert e.value.name == "SHAPE"
+    with pytest.raises(sl.SloraError) as e:
+        mk(64, hidden=H, L=1, dims=[(16, 16 * 9)])
+    assert e.value.name == "SHAPE"
