@@ -1361,7 +1361,8 @@ void build_call(slora_batch* b, const KernelCfg& k, int N, int nproj, uint32_t m
         return n;
     };
     const int srows = kShrinkRows;  // stored A rows per shrink piece
-    const bool use_runs = k.mode == kFused && b->n_runs > 0 && all_square;
+    // (the MBGMM kernels index the default q,k,v,o page-table layout: square pools only)
+    const bool use_runs = k.mode == kFused && b->n_runs > 0 && all_square && pl->square;
     call.mg_s.clear();
     call.mg_e.clear();
     for (int si = 0; si < int(b->segs.size()); ++si) {
@@ -1517,7 +1518,7 @@ extern "C" slora_status slora_batch_prepare(slora_batch_t b, const int64_t* tok_
             return e ? atoi(e) : kMgDefaultTheta;
         }();
         const int mg_rows = mbgmm_rows(p->cfg.hidden);
-        const bool ok_shape = !(b->options & SLORA_BATCH_MBGMV_ONLY) && p->cfg.dtype != SLORA_F32 && p->N() == 1 &&
+        const bool ok_shape = !(b->options & SLORA_BATCH_MBGMV_ONLY) && p->square && p->cfg.dtype != SLORA_F32 && p->N() == 1 &&
                               theta > 0 && p->cfg.hidden % 64 == 0 &&
                               p->cfg.hidden % kMgCols % 64 == 0 && mbgmm_smem(false, p->cfg.hidden, 0) <= 227 * 1024 &&
                               (!mbgmm_shrink_whole_rank() || (p->cfg.hidden / 64) % kMgKsplit == 0);
