@@ -271,6 +271,22 @@ slora_status slora_lora_apply(slora_pool_t pool, slora_batch_t batch, int32_t la
                               uint32_t proj_mask, const void* x, int64_t ldx,
                               void* const y[SLORA_MAX_PROJ], const int64_t ldy[SLORA_MAX_PROJ], void* stream);
 
+/* Many fused calls in one enqueue (the host cost of a decode step: one ABI
+ * crossing instead of one per call).  calls[i] is slora_lora_apply's argument
+ * list; the calls are enqueued in order on `stream`.  Stops at the first
+ * failing call (its index in *failed_out when non-NULL; -1 on success): the
+ * calls before it are enqueued. */
+typedef struct {
+    int32_t layer;
+    uint32_t proj_mask;
+    const void* x;
+    int64_t ldx;
+    void* y[SLORA_MAX_PROJ];
+    int64_t ldy[SLORA_MAX_PROJ];
+} slora_call;
+slora_status slora_lora_apply_many(slora_pool_t pool, slora_batch_t batch, const slora_call* calls,
+                                   int32_t n_calls, void* stream, int32_t* failed_out);
+
 /* Split form (for tensor parallelism).
  * shrink: v = x A_shard in fp32.  For projection p, the stored A shard has
  *   r/div rank columns, div = tp_size for q,k,v and 1 for o (and 1 when

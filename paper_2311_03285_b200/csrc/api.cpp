@@ -1944,6 +1944,20 @@ extern "C" slora_status slora_lora_apply(slora_pool_t p, slora_batch_t b, int32_
     return launch(p, kc, q, stream);
 }
 
+extern "C" slora_status slora_lora_apply_many(slora_pool_t p, slora_batch_t b, const slora_call* calls,
+                                              int32_t n_calls, void* stream, int32_t* failed_out) {
+    if (failed_out) *failed_out = -1;
+    if (n_calls < 0 || (n_calls > 0 && !calls)) return fail(SLORA_ERR_INVALID_ARG, "calls");
+    for (int32_t i = 0; i < n_calls; ++i) {
+        const slora_call& c = calls[i];
+        if (slora_status st = slora_lora_apply(p, b, c.layer, c.proj_mask, c.x, c.ldx, c.y, c.ldy, stream)) {
+            if (failed_out) *failed_out = i;
+            return st;
+        }
+    }
+    return ok();
+}
+
 extern "C" slora_status slora_lora_v_elems(slora_batch_t b, uint32_t mask, int32_t div, int64_t* out) {
     if (!b || !out) return fail(SLORA_ERR_INVALID_ARG, "null argument");
     if (mask == 0 || (mask >> kMaxProj) || div < 1) return fail(SLORA_ERR_INVALID_ARG, "mask/div");

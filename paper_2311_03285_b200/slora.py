@@ -59,6 +59,11 @@ class BatchInfo(ctypes.Structure):
                 ("mbgmm_segments", ctypes.c_int32)]
 
 
+class Call(ctypes.Structure):  # slora_call
+    _fields_ = [("layer", ctypes.c_int32), ("proj_mask", ctypes.c_uint32), ("x", ctypes.c_void_p),
+                ("ldx", ctypes.c_int64), ("y", ctypes.c_void_p * 8), ("ldy", ctypes.c_int64 * 8)]
+
+
 class LoaderStats(ctypes.Structure):
     _fields_ = [("loads", ctypes.c_int64), ("direct_loads", ctypes.c_int64), ("bytes", ctypes.c_int64),
                 ("busy_s", ctypes.c_double), ("queued", ctypes.c_int64)]
@@ -106,6 +111,7 @@ SIGNATURES = {
     "slora_tp_lora_o": [_VP, _VP, _I32, _VP, _I64, _VP, _I64, _VP],
     "slora_tp_get_stats": [_VP, ctypes.POINTER(TPStats)],
     "slora_batch_set_options": [_VP, ctypes.c_uint32],
+    "slora_lora_apply_many": [_VP, _VP, _VP, _I32, _VP, ctypes.POINTER(_I32)],
     "slora_adapter_prefetch": [_VP, _I64, _I32, _VP, ctypes.c_float, ctypes.POINTER(_I32)],
     "slora_adapter_wait": [_VP, _I64],
     "slora_adapter_query": [_VP, _I64, ctypes.POINTER(_I32)],
@@ -417,6 +423,24 @@ class Batch:
         yp, ld = self._ys(ys, ldys)
         _check(lib().slora_lora_apply(self.pool.h, self.h, layer, mask_of(projs), _ptr(x), ldx, yp, ld,
                                       _stream(stream)))
+
+    @staticmethod
+    def make_calls(calls) -> "ctypes.Array":
+        """Pack [(layer, projs, x, ldx, ys, ldys)] into a slora_call array (build once, reuse every step)."""
+        arr = (Call * len(calls))()
+        for c, (layer, projs, x, ldx, ys, ldys) in zip(arr, calls):
+            c.layer, c.proj_mask, c.x, c.ldx = layer, mask_of(projs), _ptr(x) or None, ldx
+            ys, ldys = list(ys) + [None] * (8 - len(ys)), list(ldys) + [0] * (8 - len(ldys))
+            for i in range(8):
+                c.y[i] = _ptr(ys[i]) or None
+                c.ldy[i] = ldys[i]
+        return arr
+
+    def apply_many(self, calls, stream=None) -> None:
+        """slora_lora_apply_many: a packed call array (make_calls) enqueued with one ABI crossing."""
+        failed = _I32(-1)
+        _check(lib().slora_lora_apply_many(self.pool.h, self.h, ctypes.addressof(calls), len(calls),
+                                           _stream(stream), ctypes.byref(failed)))
 
     def shrink(self, layer: int, projs, x, ldx: int, v, stream=None) -> None:
         _check(lib().slora_lora_shrink(self.pool.h, self.h, layer, mask_of(projs), _ptr(x), ldx, _ptr(v),

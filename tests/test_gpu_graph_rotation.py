@@ -94,3 +94,43 @@ def test_graph_replays_rotating_batches():
                 assert err <= TOL[cfg.dtype], (it, l, p, err)
     b.close()
     pool.close()
+
+
+def test_apply_many_equals_per_call_applies():
+    """slora_lora_apply_many enqueues the same launches as one slora_lora_apply per call:
+    bit-identical outputs; a bad call stops the list at its index."""
+    import torch
+    from paper_2311_03285_b200 import Batch, Pool
+    from paper_2311_03285_b200.slora import SloraError
+    cfg = wl.CONFIGS["c1"]
+    L, h = 3, cfg.hidden
+    batch = wl.make_batch(cfg)
+    need = sum(L * 8 * r for r in batch.ranks.values())
+    pool = Pool(h, L, need + 16, dtype=cfg.dtype, device=0, max_adapters=128)
+    s = torch.cuda.current_stream()
+    for a in batch.unique:
+        pool.adapter_load(a, batch.ranks[a], wl.adapter_host_buffer(cfg, a, L), stream=s)
+    b = Batch(pool)
+    b.prepare(batch.token_adapter, stream=s)
+    T = batch.T
+    td = torch.float16
+    g = torch.Generator(device="cuda").manual_seed(3)
+    X = torch.randn((L, T, h), generator=g, device="cuda").to(td)
+    Y0 = torch.randn((L, 4, T, h), generator=g, device="cuda").to(td)
+    Y1 = Y0.clone()
+    for l in range(L):
+        b.apply(l, "qkv", X[l], h, [Y0[l, p] for p in range(4)], [h] * 4, stream=s)
+        b.apply(l, "o", X[l], h, [Y0[l, p] for p in range(4)], [h] * 4, stream=s)
+    calls = []
+    for l in range(L):
+        calls.append((l, "qkv", X[l], h, [Y1[l, p] for p in range(4)], [h] * 4))
+        calls.append((l, "o", X[l], h, [Y1[l, p] for p in range(4)], [h] * 4))
+    b.apply_many(Batch.make_calls(calls), stream=s)
+    torch.cuda.synchronize()
+    assert torch.equal(Y0, Y1)
+    bad = Batch.make_calls(calls[:2] + [(L + 5, "q", X[0], h, [Y1[0, p] for p in range(4)], [h] * 4)])
+    with pytest.raises(SloraError) as e:
+        b.apply_many(bad, stream=s)
+    assert e.value.name == "INVALID_ARG"
+    b.close()
+    pool.close()
