@@ -325,6 +325,53 @@ def timed_steps(W, stream, steps, ws):
     return ms, per
 
 
+def lora_comm_overhead(W, stream, steps):
+    """P:532 ("S-LoRA with and without LoRA communication"): the TP step replayed from a graph
+    with the library's collectives (slora_tp_lora_qkv / _o) and from a graph of the same shrink
+    and expand kernels with the exchange steps left out (slora_lora_shrink / _expand on
+    workspaces: results not meaningful, timing only).  Device time per step of each."""
+    import torch
+    b, N, k, H, P = W.dbatch, W.N, W.k, W.H, W.P
+    vloc = torch.zeros(b.v_elems("qkv", N), dtype=torch.float32, device="cuda")
+    vall = torch.zeros(b.v_elems("qkv", 1), dtype=torch.float32, device="cuda")
+    u = torch.zeros(b.v_elems("o", 1), dtype=torch.float32, device="cuda")
+
+    def nocomm():
+        st = torch.cuda.current_stream()
+        for l in range(W.L):
+            b.shrink(l, "qkv", W.x[l], H, vloc, stream=st)
+            b.expand(l, "qkv", vall, N, [W.y[l, p] for p in range(3)], [P] * 3, stream=st)
+            b.shrink(l, "o", W.z[l], P, u, stream=st)
+            ys = W.base[l][:, k * P:(k + 1) * P]
+            b.expand(l, "o", u, 1, [None, None, None, ys], [0, 0, 0, H], stream=st)
+
+    def timed(replay):
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        for _ in range(2):
+            replay()
+        torch.cuda.synchronize()
+        ev[0].record(stream)
+        for _ in range(steps):
+            b.prepare(W.batch.token_adapter, stream=stream)
+            replay()
+        ev[1].record(stream)
+        torch.cuda.synchronize()
+        return ev[0].elapsed_time(ev[1]) / steps
+
+    nocomm()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    cs = torch.cuda.Stream()
+    with torch.cuda.graph(g, stream=cs):
+        nocomm()
+    with_ms = timed(W.graph.replay)
+    without_ms = timed(g.replay)
+    return {"with_lora_comm_ms": round(with_ms, 4), "without_lora_comm_ms": round(without_ms, 4),
+            "overhead": round(with_ms / without_ms - 1.0, 4),
+            "note": "P:532: the same TP step with and without the q/k/v all-gather and o all-reduce of the LoRA "
+                    "intermediate (graph replays, device time per step)"}
+
+
 def rotating_steps(W, stream, steps):
     """Like timed_steps, but every step prepares a different batch (re-drawn token maps over
     the resident adapters) and replays the SAME graph: the launches read the descriptors
@@ -592,6 +639,11 @@ def run_ours(args):
                                            P337_allreduce_elems=2 * (ws - 1) * NR // ws * layers,
                                            source="counts from the arguments passed to ncclAllGather/"
                                                   "ncclAllReduce (slora_tp_get_stats)")
+    if use_graph and tp_path:
+        try:
+            out["lora_comm"] = lora_comm_overhead(W, stream, max(5, args.steps // 2))
+        except Exception as e:
+            out["lora_comm"] = {"error": f"{type(e).__name__}: {e}"}
     if use_graph and not tp_path and W.dbatch.info()["mbgmm_segments"] == 0:
         rot = rotating_steps(W, stream, args.steps)
         rot["vs_fixed_batch"] = round(rot["ms_per_step"] / ms, 3)
