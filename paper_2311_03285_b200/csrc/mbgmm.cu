@@ -302,16 +302,36 @@ __global__ void __launch_bounds__(kMgThreads, 2) mbgmm_expand_kernel(const __gri
     const int64_t yr1 = t1 < u.nt ? (p.yrow ? p.yrow[u.row0 + t1] : u.row0 + t1) : 0;
     T* y0 = y + yr0 * ldy + u.a;
     T* y1 = y + yr1 * ldy + u.a;
-    // y of this sub-chunk is loaded into registers before its MMAs (the loads fly
-    // while the tensor cores work), then read-modify-written once
+#ifndef SLORA_MG_NO_YPF
+    // the slab's y rows into L2 now (one 128-byte line per prefetch, lanes c == 0 of each row
+    // pair): the sub-chunk loads below then wait for L2, not HBM
+    if (c == 0) {
+        for (int l = 0; l < nc * ES; l += 128) {
+            if (t0 < u.nt) asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const char*>(y0) + l));
+            if (t1 < u.nt) asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const char*>(y1) + l));
+        }
+    }
+#endif
+    // y is software-pipelined one 64-column sub-chunk ahead: the next sub-chunk's
+    // loads fly while this one's MMAs run; each y element is read-modify-written once
+    uint32_t yn[8][2];
+    auto load_y = [&](int sc, uint32_t (&dst)[8][2]) {
+#pragma unroll
+        for (int n = 0; n < 8; ++n) {
+            const int col = sc + 8 * n + 2 * c;
+            dst[n][0] = t0 < u.nt ? *reinterpret_cast<const uint32_t*>(y0 + col) : 0u;
+            dst[n][1] = t1 < u.nt ? *reinterpret_cast<const uint32_t*>(y1 + col) : 0u;
+        }
+    };
+    load_y(0, yn);
     for (int sc = 0; sc < nc; sc += 64) {
         uint32_t yv[8][2];
 #pragma unroll
         for (int n = 0; n < 8; ++n) {
-            const int col = sc + 8 * n + 2 * c;
-            yv[n][0] = t0 < u.nt ? *reinterpret_cast<const uint32_t*>(y0 + col) : 0u;
-            yv[n][1] = t1 < u.nt ? *reinterpret_cast<const uint32_t*>(y1 + col) : 0u;
+            yv[n][0] = yn[n][0];
+            yv[n][1] = yn[n][1];
         }
+        if (sc + 64 < nc) load_y(sc + 64, yn);
         float d[8][4] = {};
         for (int k = 0; k < rp; k += 16) {
             uint32_t ah[4], alw[4];
