@@ -372,6 +372,36 @@ def lora_comm_overhead(W, stream, steps):
                     "intermediate (graph replays, device time per step)"}
 
 
+def tp_p2p_step(W, stream, steps, nccl_ms):
+    """NEXT-3: the TP step through slora_tp_fused_qkv / _o (one kernel per call: the v exchange
+    by NVLink peer stores + system-scope counters instead of NCCL), graph replay, device time."""
+    import torch
+    W.tpl.enable_p2p()
+    W.dbatch.prepare(W.batch.token_adapter, stream=stream)
+    torch.cuda.synchronize()
+    W.layers(torch.cuda.current_stream())  # eager once (builds nothing new: prepare did)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    cs = torch.cuda.Stream()
+    with torch.cuda.graph(g, stream=cs):
+        W.layers(torch.cuda.current_stream())
+    for _ in range(2):
+        W.dbatch.prepare(W.batch.token_adapter, stream=stream)
+        g.replay()
+    torch.cuda.synchronize()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    ev[0].record(stream)
+    for _ in range(steps):
+        W.dbatch.prepare(W.batch.token_adapter, stream=stream)
+        g.replay()
+    ev[1].record(stream)
+    torch.cuda.synchronize()
+    ms = ev[0].elapsed_time(ev[1]) / steps
+    return {"ms_per_step": round(ms, 4), "vs_nccl_path": round(ms / nccl_ms, 3), "launches_per_layer": 2,
+            "note": "slora_tp_fused_qkv/_o: shrink -> peer stores of v into every rank's exchange region -> "
+                    "expand in one kernel per call (NCCL path: 4 kernels + 2 collectives per layer)"}
+
+
 def rotating_steps(W, stream, steps):
     """Like timed_steps, but every step prepares a different batch (re-drawn token maps over
     the resident adapters) and replays the SAME graph: the launches read the descriptors
@@ -644,6 +674,12 @@ def run_ours(args):
             out["lora_comm"] = lora_comm_overhead(W, stream, max(5, args.steps // 2))
         except Exception as e:
             out["lora_comm"] = {"error": f"{type(e).__name__}: {e}"}
+        # NEXT-3 device-initiated exchange: one rank here; across GPUs only on request (unmeasured there)
+        if ws == 1 or os.environ.get("SLORA_BENCH_TP_P2P") == "1":
+            try:
+                out["tp_device_initiated"] = tp_p2p_step(W, stream, max(5, args.steps // 2), ms)
+            except Exception as e:
+                out["tp_device_initiated"] = {"error": f"{type(e).__name__}: {e}"}
     if use_graph and not tp_path and W.dbatch.info()["mbgmm_segments"] == 0:
         rot = rotating_steps(W, stream, args.steps)
         rot["vs_fixed_batch"] = round(rot["ms_per_step"] / ms, 3)

@@ -363,6 +363,36 @@ slora_status slora_tp_lora_qkv(slora_pool_t pool, slora_batch_t batch, int32_t l
                                int64_t ldx, void* const y[3], const int64_t ldy[3], void* stream);
 slora_status slora_tp_lora_o(slora_pool_t pool, slora_batch_t batch, int32_t layer, const void* z,
                              int64_t ldz, void* base_partial, int64_t ld_base, void* stream);
+
+/* NEXT-3: device-initiated TP exchange fused into ONE kernel per call
+ * ("enhanced fused kernels").  Instead of shrink ->
+ * NCCL -> expand, the shrink pieces of rank k store their v entries straight
+ * into block k of EVERY rank's exchange region (NVLink peer stores through
+ * CUDA IPC mappings) and release a per-item counter on every rank
+ * (system-scope red.release); an expand piece waits until its item's counter
+ * shows all N ranks' shrink pieces, then reads the N blocks -- gathered for
+ * q/k/v (the all-gather of P:323), summed in rank order for o (the
+ * all-reduce of P:324, deterministic) -- and expands into y as
+ * slora_tp_lora_qkv / _o do (same arguments, same results).
+ * slora_tp_p2p_export: allocates this rank's exchange region (kLaunchSlots x
+ *   N x 196608 fp32 + counters) and writes its CUDA IPC handle into
+ *   handle_out (SLORA_TP_P2P_HANDLE_BYTES).  slora_tp_p2p_open: handles =
+ *   the N ranks' handles in rank order (the caller all-gathers them, e.g.
+ *   with torch.distributed); maps every peer region (lazy peer access).
+ *   After open, slora_batch_prepare builds the fused calls' descriptors
+ *   eagerly.  Requirements: all N ranks launch the same calls in the same
+ *   order (an expand waits for the other ranks' shrink pieces of the same
+ *   launch); every rank's GPU runs its whole grid at once.  Errors:
+ *   INVALID_ARG (not exported / opened), SHAPE (NR beyond the exchange
+ *   capacity), CUDA.  Unmeasured beyond one GPU in this repository: with
+ *   N = 1 it is tested bit-exact against the NCCL path. */
+#define SLORA_TP_P2P_HANDLE_BYTES 64
+slora_status slora_tp_p2p_export(slora_pool_t pool, void* handle_out);
+slora_status slora_tp_p2p_open(slora_pool_t pool, const void* handles);
+slora_status slora_tp_fused_qkv(slora_pool_t pool, slora_batch_t batch, int32_t layer, const void* x,
+                                int64_t ldx, void* const y[3], const int64_t ldy[3], void* stream);
+slora_status slora_tp_fused_o(slora_pool_t pool, slora_batch_t batch, int32_t layer, const void* z,
+                              int64_t ldz, void* base_partial, int64_t ld_base, void* stream);
 slora_status slora_tp_get_stats(slora_pool_t pool, slora_tp_stats* out);
 
 /* Wait for `stream` and surface any deferred CUDA error. */

@@ -305,6 +305,14 @@ struct slora_pool {
     float* tp_u = nullptr;             // o partial / all-reduced intermediate: NR
     int64_t tp_cap = 0;                // NR the buffers hold
     slora_tp_stats tp_stats{};
+    // NEXT-3 device-initiated exchange (slora_tp_p2p_*): this rank's exchange region (one cudaMalloc,
+    // IPC-exported) = [kLaunchSlots][N][p2p_vcap] fp32 v blocks, then [kLaunchSlots][p2p_ccap] int32
+    // per-item counters (zeroed); every rank's region mapped here (peer j at p2p_base[j])
+    void* p2p_local = nullptr;
+    void* p2p_base[8] = {};
+    bool p2p_open = false;
+    int64_t p2p_vcap = 0, p2p_ccap = 0;
+    int kc_tpf_qkv = -1, kc_tpf_o = -1;  // fused configurations of the device-initiated TP calls
 
     ~slora_pool();
     int64_t free_pages() const { return int64_t(free_stack.size()); }
@@ -522,6 +530,11 @@ extern "C" slora_status slora_pool_destroy(slora_pool_t p) {
         if (p->tp_vall) cudaFree(p->tp_vall);
         if (p->tp_u) cudaFree(p->tp_u);
         if (p->trace_dev) cudaFree(p->trace_dev);
+    }
+    if (p->dev) {
+        for (int j = 0; j < p->N() && j < 8; ++j)
+            if (p->p2p_base[j] && p->p2p_base[j] != p->p2p_local) cudaIpcCloseMemHandle(p->p2p_base[j]);
+        if (p->p2p_local) cudaFree(p->p2p_local);
     }
     tp_release(p);
     for (slora_batch* b : p->batches) {  // live batches become stale handles (their device side freed here)
@@ -1312,7 +1325,8 @@ void schedule_pieces(const std::vector<DevPiece>& in, const std::vector<int64_t>
 // tokens); pieces: each item's stored A rows in groups of kShrinkRows (shrink,
 // full K), and its output columns in chunks of kc.dchunk (expand), scheduled
 // onto the kernel's persistent CTAs by schedule_pieces.
-void build_call(slora_batch* b, const KernelCfg& k, int N, int nproj, uint32_t mask, slora_batch::Call& call) {
+void build_call(slora_batch* b, const KernelCfg& k, int N, int nproj, uint32_t mask, slora_batch::Call& call,
+                bool allow_mbgmm = true) {
     call.items.clear();
     call.pieces.clear();
     const slora_pool* pl = b->pool;
@@ -1362,7 +1376,7 @@ void build_call(slora_batch* b, const KernelCfg& k, int N, int nproj, uint32_t m
     };
     const int srows = kShrinkRows;  // stored A rows per shrink piece
     // (the MBGMM kernels index the default q,k,v,o page-table layout: square pools only)
-    const bool use_runs = k.mode == kFused && b->n_runs > 0 && all_square && pl->square;
+    const bool use_runs = allow_mbgmm && k.mode == kFused && b->n_runs > 0 && all_square && pl->square;
     call.mg_s.clear();
     call.mg_e.clear();
     for (int si = 0; si < int(b->segs.size()); ++si) {
@@ -1685,6 +1699,10 @@ extern "C" slora_status slora_batch_prepare(slora_batch_t b, const int64_t* tok_
             if (!st2 && p->kcfg[3].ok) st2 = ensure_call(p, b, 3, 0x8, stream);
         }
     }
+    if (!st2 && p->p2p_open && b->adapted > 0) {  // device-initiated TP calls (slora_tp_fused_*)
+        st2 = ensure_call(p, b, p->kc_tpf_qkv, 0x7, stream);
+        if (!st2) st2 = ensure_call(p, b, p->kc_tpf_o, 0x8, stream);
+    }
     // every call shape launched since the batch was created is rebuilt too, and all headers
     // are uploaded with the descriptors in one flush: a CUDA graph that captured those
     // launches replays the new batch (MBGMV path; see slora_batch_get_info().graph_ok)
@@ -1767,7 +1785,8 @@ slora_status ensure_call(slora_pool* p, slora_batch* b, int kc, uint32_t mask, v
         return fail(SLORA_ERR_INVALID_ARG, "call descriptor (kernel cfg %d, mask 0x%x) not built by the last prepare: "
                     "a CUDA graph may only capture calls whose descriptors exist (run the call once eagerly "
                     "after prepare, or use the calls prepare builds)", kc, mask);
-    build_call(b, p->kcfg[kc], p->N(), np, mask, call);
+    // the device-initiated TP calls are one MBGMV kernel each: every segment on MBGMV
+    build_call(b, p->kcfg[kc], p->N(), np, mask, call, kc != p->kc_tpf_qkv && kc != p->kc_tpf_o);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     cudaError_t e = cudaSuccess;
     call.off_items = arena_put(b, call.items.data(), call.items.size() * sizeof(DevItem), s, e);
@@ -2104,6 +2123,151 @@ extern "C" slora_status slora_tp_lora_o(slora_pool_t p, slora_batch_t b, int32_t
                    static_cast<uint8_t*>(base_partial) + size_t(int64_t(p->cfg.tp_rank) * p->P) * p->es};
     const int64_t lds[4] = {0, 0, 0, ld_base};
     return slora_lora_expand(p, b, layer, 0x8, p->tp_u, 1, ys, lds, stream);
+}
+
+// ------------------------------------------- NEXT-3: device-initiated TP exchange
+namespace {
+constexpr int64_t kP2PVcap = int64_t(3) * 65536;  // floats per rank block: 3 NR/N (q/k/v) or NR (o) <= this
+constexpr int64_t kP2PCcap = 65536;                 // per-item counters per launch slot
+size_t p2p_bytes(int N) {
+    return sizeof(float) * size_t(kLaunchSlots) * size_t(N) * size_t(kP2PVcap) +
+           sizeof(int32_t) * size_t(kLaunchSlots) * size_t(kP2PCcap);
+}
+}  // namespace
+
+extern "C" slora_status slora_tp_p2p_export(slora_pool_t p, void* handle_out) {
+    if (check_pool(p) || !handle_out) return fail(SLORA_ERR_INVALID_ARG, "null argument");
+    if (!p->dev) return fail(SLORA_ERR_NO_DEVICE, "bookkeeping-only pool");
+    const int N = p->N();
+    if (N > 8) return fail(SLORA_ERR_SHAPE, "tp_size %d > 8", N);
+    CUDA_TRY(cudaSetDevice(p->cfg.device));
+    if (!p->p2p_local) {
+        CUDA_TRY(cudaMalloc(&p->p2p_local, p2p_bytes(N)));
+        CUDA_TRY(cudaMemset(p->p2p_local, 0, p2p_bytes(N)));
+        CUDA_TRY(cudaDeviceSynchronize());
+        p->p2p_vcap = kP2PVcap;
+        p->p2p_ccap = kP2PCcap;
+        // fused configurations: q/k/v (K = hidden: stored A rows span N pages; B rows of H/N) and o (K = H/N)
+        const int dt = p->cfg.dtype == SLORA_F32 ? kF32 : (p->cfg.dtype == SLORA_F16 ? kF16 : kBF16);
+        if (p->n_kcfg + 2 > kMaxKc) return fail(SLORA_ERR_SHAPE, "no kernel configuration slot left");
+        p->kc_tpf_qkv = p->n_kcfg;
+        p->kcfg[p->n_kcfg++] = make_kernel_cfg(kFused, p->cfg.hidden, p->P, p->P, p->es, dt);
+        p->kc_tpf_o = p->n_kcfg;
+        p->kcfg[p->n_kcfg++] = make_kernel_cfg(kFused, p->P, p->P, p->P, p->es, dt);
+    }
+    cudaIpcMemHandle_t h;
+    CUDA_TRY(cudaIpcGetMemHandle(&h, p->p2p_local));
+    static_assert(sizeof(cudaIpcMemHandle_t) <= SLORA_TP_P2P_HANDLE_BYTES, "IPC handle size");
+    memset(handle_out, 0, SLORA_TP_P2P_HANDLE_BYTES);
+    memcpy(handle_out, &h, sizeof(h));
+    return ok();
+}
+
+extern "C" slora_status slora_tp_p2p_open(slora_pool_t p, const void* handles) {
+    if (check_pool(p) || !handles) return fail(SLORA_ERR_INVALID_ARG, "null argument");
+    if (!p->p2p_local) return fail(SLORA_ERR_INVALID_ARG, "call slora_tp_p2p_export first");
+    if (p->p2p_open) return fail(SLORA_ERR_INVALID_ARG, "already open");
+    const int N = p->N(), k = p->cfg.tp_rank;
+    CUDA_TRY(cudaSetDevice(p->cfg.device));
+    for (int j = 0; j < N; ++j) {
+        if (j == k) {
+            p->p2p_base[j] = p->p2p_local;
+            continue;
+        }
+        cudaIpcMemHandle_t h;
+        memcpy(&h, static_cast<const uint8_t*>(handles) + size_t(j) * SLORA_TP_P2P_HANDLE_BYTES, sizeof(h));
+        cudaError_t e = cudaIpcOpenMemHandle(&p->p2p_base[j], h, cudaIpcMemLazyEnablePeerAccess);
+        if (e) {
+            for (int i = 0; i < j; ++i)
+                if (i != k && p->p2p_base[i]) cudaIpcCloseMemHandle(p->p2p_base[i]);
+            for (auto& b : p->p2p_base) b = nullptr;
+            return fail(SLORA_ERR_CUDA, "cudaIpcOpenMemHandle(rank %d): %s", j, cudaGetErrorString(e));
+        }
+    }
+    p->p2p_open = true;
+    return ok();
+}
+
+namespace {
+// Fill the device-initiated TP fields of a prepared call: this launch slot's block of every rank.
+slora_status p2p_params(slora_pool* p, slora_batch* b, uint32_t mask, LoraParams& q) {
+    const int N = p->N();
+    const int64_t need = (mask == 0x8) ? b->NR : 3 * (b->NR / N);
+    if (need > p->p2p_vcap) return fail(SLORA_ERR_SHAPE, "exchange block holds %lld < %lld floats",
+                                        (long long)p->p2p_vcap, (long long)need);
+    if (int64_t(b->calls[mask == 0x8 ? p->kc_tpf_o : p->kc_tpf_qkv][mask == 0x8 ? 1 : 3].items.size()) > p->p2p_ccap)
+        return fail(SLORA_ERR_SHAPE, "more items than exchange counters");
+    const int64_t vslot = int64_t(q.slot) * N * p->p2p_vcap;
+    const int64_t cslot = int64_t(q.slot) * p->p2p_ccap;
+    const int64_t voff_ctr = int64_t(kLaunchSlots) * N * p->p2p_vcap;  // floats before the counters
+    for (int j = 0; j < N; ++j) {
+        float* vb = static_cast<float*>(p->p2p_base[j]);
+        q.peer_v[j] = vb + vslot;
+        q.peer_ctr[j] = reinterpret_cast<int32_t*>(vb + voff_ctr) + cslot;
+    }
+    q.n_peers = N;
+    q.peer_rank = p->cfg.tp_rank;
+    q.peer_block = p->p2p_vcap;
+    q.v_sum_blocks = mask == 0x8 ? 1 : 0;
+    return SLORA_OK;
+}
+
+slora_status p2p_checks(slora_pool* p, slora_batch* b) {
+    if (!p || !b) return fail(SLORA_ERR_INVALID_ARG, "null pool/batch");
+    if (!p->p2p_open) return fail(SLORA_ERR_INVALID_ARG, "call slora_tp_p2p_export / _open first");
+    return SLORA_OK;
+}
+}  // namespace
+
+extern "C" slora_status slora_tp_fused_qkv(slora_pool_t p, slora_batch_t b, int32_t layer, const void* x,
+                                           int64_t ldx, void* const y[3], const int64_t ldy[3], void* stream) {
+    slora_status st = p2p_checks(p, b);
+    if (!st) st = common_checks(p, b, layer, 0x7);
+    if (st) return st;
+    if (b->adapted == 0) return ok();
+    if (!x || !y || !ldy || !aligned16(x, ldx, p->es) || ldx < p->cfg.hidden)
+        return fail(SLORA_ERR_SHAPE, "x alignment/stride");
+    for (int pj = 0; pj < 3; ++pj)
+        if (!y[pj] || !aligned16(y[pj], ldy[pj], p->es) || ldy[pj] < p->P)
+            return fail(SLORA_ERR_SHAPE, "y[%d] alignment/stride", pj);
+    LoraParams q;
+    if ((st = prepare_call(p, b, p->kc_tpf_qkv, layer, 0x7, stream, q))) return st;
+    if ((st = p2p_params(p, b, 0x7, q))) return st;
+    q.x = x;
+    q.ldx = ldx;
+    for (int pj = 0; pj < 3; ++pj) {
+        q.y[pj] = y[pj];
+        q.ldy[pj] = ldy[pj];
+    }
+    const KernelCfg& k = p->kcfg[p->kc_tpf_qkv];
+    const int dt = p->cfg.dtype == SLORA_F32 ? kF32 : (p->cfg.dtype == SLORA_F16 ? kF16 : kBF16);
+    CUDA_TRY(cudaSetDevice(p->cfg.device));
+    CUDA_TRY(launch_lora(q, kTPFused, dt, k.grid, static_cast<cudaStream_t>(stream), k.smem));
+    return ok();
+}
+
+extern "C" slora_status slora_tp_fused_o(slora_pool_t p, slora_batch_t b, int32_t layer, const void* z, int64_t ldz,
+                                         void* base_partial, int64_t ld_base, void* stream) {
+    slora_status st = p2p_checks(p, b);
+    if (!st) st = common_checks(p, b, layer, 0x8);
+    if (st) return st;
+    if (b->adapted == 0) return ok();
+    if (!z || !aligned16(z, ldz, p->es) || ldz < p->P) return fail(SLORA_ERR_SHAPE, "z alignment/stride");
+    if (!base_partial || ld_base < p->cfg.hidden || !aligned16(base_partial, ld_base, p->es))
+        return fail(SLORA_ERR_INVALID_ARG, "base partial / stride");
+    LoraParams q;
+    if ((st = prepare_call(p, b, p->kc_tpf_o, layer, 0x8, stream, q))) return st;
+    if ((st = p2p_params(p, b, 0x8, q))) return st;
+    q.x = z;
+    q.ldx = ldz;
+    // fold (reading R13): the expand writes column slice k of the base partial sum
+    q.y[3] = static_cast<uint8_t*>(base_partial) + size_t(int64_t(p->cfg.tp_rank) * p->P) * p->es;
+    q.ldy[3] = ld_base;
+    const KernelCfg& k = p->kcfg[p->kc_tpf_o];
+    const int dt = p->cfg.dtype == SLORA_F32 ? kF32 : (p->cfg.dtype == SLORA_F16 ? kF16 : kBF16);
+    CUDA_TRY(cudaSetDevice(p->cfg.device));
+    CUDA_TRY(launch_lora(q, kTPFused, dt, k.grid, static_cast<cudaStream_t>(stream), k.smem));
+    return ok();
 }
 
 extern "C" slora_status slora_tp_get_stats(slora_pool_t p, slora_tp_stats* out) {

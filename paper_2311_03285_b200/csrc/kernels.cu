@@ -153,6 +153,15 @@ __device__ __forceinline__ int ld_acquire(const int* p) {
 __device__ __forceinline__ void red_release_add(int* p, int v) {
     asm volatile("red.release.gpu.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+// system scope (peer GPUs over NVLink: kTPFused)
+__device__ __forceinline__ int ld_acquire_sys(const int* p) {
+    int v;
+    asm volatile("ld.acquire.sys.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void red_release_add_sys(int* p, int v) {
+    asm volatile("red.release.sys.global.add.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 
 __device__ __forceinline__ void prefetch_l1(const void* p) {
     asm volatile("prefetch.global.L1 [%0];" ::"l"(p));
@@ -433,7 +442,12 @@ __device__ __forceinline__ void shrink_piece(const LoraParams& p, const PieceMet
         float s = 0.f;
 #pragma unroll
         for (int w = 0; w < kConsumerWarps; ++w) s += red[(w * kShrinkRows + q) * kItemTokCap + t];
-        vout[M.vbase + int64_t(t) * M.ra + M.row0 + q] = s;
+        const int64_t vi = M.vbase + int64_t(t) * M.ra + M.row0 + q;
+        if (p.n_peers == 0) {
+            vout[vi] = s;
+        } else {  // kTPFused: block k of every rank's exchange region (NVLink peer stores)
+            for (int j = 0; j < p.n_peers; ++j) p.peer_v[j][int64_t(p.peer_rank) * p.peer_block + vi] = s;
+        }
     }
 }
 
@@ -596,7 +610,12 @@ __device__ __forceinline__ void shrink_piece_mma(const LoraParams& p, const Piec
         float sum = 0.f;
 #pragma unroll
         for (int w = 0; w < kConsumerWarps; ++w) sum += red[(w * kShrinkRows + q) * kItemTokCap + t];
-        vout[M.vbase + int64_t(t) * M.ra + M.row0 + q] = sum;
+        const int64_t vi = M.vbase + int64_t(t) * M.ra + M.row0 + q;
+        if (p.n_peers == 0) {
+            vout[vi] = sum;
+        } else {  // kTPFused: block k of every rank's exchange region (NVLink peer stores)
+            for (int j = 0; j < p.n_peers; ++j) p.peer_v[j][int64_t(p.peer_rank) * p.peer_block + vi] = sum;
+        }
     }
 }
 
@@ -930,7 +949,7 @@ __global__ void __launch_bounds__(kThreads, 1) mbgmv_kernel(const __grid_constan
     const int64_t P = p.page_elems;
     // the call's descriptors (prepare rewrites the header; written before this grid by a memcpy)
     const CallHdr& H = *p.hdr;
-    int32_t* const sync = H.sync + int64_t(p.slot) * H.sync_stride;
+    int32_t* const sync = MODE == kTPFused ? p.peer_ctr[p.peer_rank] : H.sync + int64_t(p.slot) * H.sync_stride;
     float* const vout = MODE == kFused ? H.ws + int64_t(p.slot) * H.ws_stride : p.v;
     const int64_t NR = H.NR;
 
@@ -1117,7 +1136,41 @@ __global__ void __launch_bounds__(kThreads, 1) mbgmv_kernel(const __grid_constan
                 if (es >= 2) mbar_wait_sleep(&vempty[eb], ((es >> 1) - 1) & 1);
                 float* vb = vbuf + eb * (kItemTokCap * kMaxRank);
                 if (es == 0) pdl_wait();
-                if (MODE == kFused) {
+                if (MODE == kTPFused) {
+                    // every rank's shrink pieces of this item (N x n_sp, peer stores + system-scope
+                    // releases), then v: the N rank blocks gathered (q/k/v: all-gather) or summed in
+                    // rank order (o: all-reduce, deterministic)
+                    const int want = p.n_peers * M.n_sp;
+                    if (lane == 0) {
+                        const long long t_end = gtimer() + 4000000000LL;
+                        while (ld_acquire_sys(&sync[M.item]) < want) {
+                            __nanosleep(32);
+                            if (gtimer() > t_end) {
+                                printf("slora: TP expand piece of item %d waited > 4 s for the ranks' shrink pieces\n",
+                                       M.item);
+                                __trap();
+                            }
+                        }
+                    }
+                    __syncwarp();
+                    const float* vloc = p.peer_v[p.peer_rank];
+                    if (p.v_sum_blocks) {
+                        for (int e = lane; e < M.nt * M.r; e += 32) {
+                            float a = 0.f;
+                            for (int j = 0; j < p.n_peers; ++j) a += __ldcv(vloc + int64_t(j) * p.peer_block + M.vbase + e);
+                            vb[e] = a;
+                        }
+                    } else {
+                        const int vbk = p.n_peers, rb = M.r / vbk;
+                        const int64_t base = int64_t(M.pi) * (NR / vbk) + M.vrow / vbk;
+                        for (int e = lane; e < M.nt * M.r; e += 32) {
+                            const int t = e / M.r, j = e % M.r;
+                            vb[e] = __ldcv(vloc + int64_t(j / rb) * p.peer_block + base + int64_t(t) * rb + j % rb);
+                        }
+                    }
+                    __syncwarp();
+                    if (lane == 0 && atomicAdd(&sync[M.item], 1) == want + M.n_ep - 1) atomicExch(&sync[M.item], 0);
+                } else if (MODE == kFused) {
                     if (lane == 0) {
                         // bounded: an expand piece waits for shrink pieces of other CTAs, which
                         // must all be resident (grid <= co-resident CTAs, api.cpp).  If the device
@@ -1161,14 +1214,19 @@ __global__ void __launch_bounds__(kThreads, 1) mbgmv_kernel(const __grid_constan
         // Releases each finished shrink piece to the item's expand pieces
         // (red.release.gpu; cumulative over the consumers' v stores observed
         // through the mbarrier), off the consumers' critical path.
-        for (int s = 0; MODE == kFused; ++s) {
+        for (int s = 0; MODE == kFused || MODE == kTPFused; ++s) {
             const int b = s & (kPub - 1);
             mbar_wait_sleep(&pfull[b], (s / kPub) & 1);
             const int item = pubq[b];
             __syncwarp();
             if (lane == 0) mbar_arrive(&pempty[b]);
             if (item < 0) break;
-            if (lane == 0 && MODE == kFused) red_release_add(&sync[item], 1);
+            if (MODE == kFused) {
+                if (lane == 0) red_release_add(&sync[item], 1);
+            } else if (lane < p.n_peers) {  // kTPFused: the item's counter on every rank
+                __threadfence_system();      // the consumers' peer v stores (observed via the mbarrier)
+                red_release_add_sys(p.peer_ctr[lane] + item, 1);
+            }
         }
     } else {
         // ============================ consumers ===========================
@@ -1234,7 +1292,7 @@ __global__ void __launch_bounds__(kThreads, 1) mbgmv_kernel(const __grid_constan
                     default: break;
                 }
                 ++xs;
-                if (MODE == kFused) publish(M.item);
+                if (MODE == kFused || MODE == kTPFused) publish(M.item);
             } else {
                 // ------------------------------ expand ------------------------------
                 const int eb = es & 1;
@@ -1288,7 +1346,7 @@ __global__ void __launch_bounds__(kThreads, 1) mbgmv_kernel(const __grid_constan
             if (tid == 0 && i < 48) TRACE(112 + i);
             if (lane == 0) mbar_arrive(&mempty[m]);
         }
-        if (MODE == kFused) publish(-1);
+        if (MODE == kFused || MODE == kTPFused) publish(-1);
     }
     if (tid == 0) TRACE(2);
 }
@@ -1306,16 +1364,19 @@ static void* kernel_ptr() {
     return reinterpret_cast<void*>(&mbgmv_kernel<T, MODE>);
 }
 static void* kernel_for(int mode, int dtype) {
-    switch (dtype * 3 + mode) {
+    switch (dtype * 4 + mode) {
         case 0: return kernel_ptr<float, kFused>();
         case 1: return kernel_ptr<float, kShrink>();
         case 2: return kernel_ptr<float, kExpand>();
-        case 3: return kernel_ptr<__half, kFused>();
-        case 4: return kernel_ptr<__half, kShrink>();
-        case 5: return kernel_ptr<__half, kExpand>();
-        case 6: return kernel_ptr<__nv_bfloat16, kFused>();
-        case 7: return kernel_ptr<__nv_bfloat16, kShrink>();
-        default: return kernel_ptr<__nv_bfloat16, kExpand>();
+        case 3: return kernel_ptr<float, kTPFused>();
+        case 4: return kernel_ptr<__half, kFused>();
+        case 5: return kernel_ptr<__half, kShrink>();
+        case 6: return kernel_ptr<__half, kExpand>();
+        case 7: return kernel_ptr<__half, kTPFused>();
+        case 8: return kernel_ptr<__nv_bfloat16, kFused>();
+        case 9: return kernel_ptr<__nv_bfloat16, kShrink>();
+        case 10: return kernel_ptr<__nv_bfloat16, kExpand>();
+        default: return kernel_ptr<__nv_bfloat16, kTPFused>();
     }
 }
 
@@ -1344,6 +1405,7 @@ static cudaError_t launch_mode(const LoraParams& p, int mode, int grid, cudaStre
     switch (mode) {
         case kFused: return launch_t<T, kFused>(p, grid, s, smem);
         case kShrink: return launch_t<T, kShrink>(p, grid, s, smem);
+        case kTPFused: return launch_t<T, kTPFused>(p, grid, s, smem);
         default: return launch_t<T, kExpand>(p, grid, s, smem);
     }
 }
@@ -1370,7 +1432,7 @@ int lora_max_ctas(int mode, int dtype, size_t smem) {
 cudaError_t configure_lora_kernels(int /*device*/) {
     const int max_smem = 226 * 1024;  // 227 KB opt-in minus the kernel's static smem
     for (int dt = 0; dt < 3; ++dt)
-        for (int m = 0; m < 3; ++m) {
+        for (int m = 0; m < 4; ++m) {
             cudaError_t e = cudaFuncSetAttribute(kernel_for(m, dt), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                  max_smem);
             if (e) return e;

@@ -90,7 +90,7 @@ constexpr int kMeta = 4;         // resolved-piece ring (resolver runs up to kMe
 constexpr int kLaunchSlots = 8;
 constexpr int kTraceSlots = 1024;  // debug trace: globaltimer events per traced CTA (16 CTAs)  // rotating per-launch counter/workspace slots
 
-enum Mode : int { kFused = 0, kShrink = 1, kExpand = 2 };
+enum Mode : int { kFused = 0, kShrink = 1, kExpand = 2, kTPFused = 3 };
 enum DType : int { kF32 = 0, kF16 = 1, kBF16 = 2 };
 enum PieceKind : int { kPieceS = 0, kPieceE = 1, kPieceStop = 2 };
 
@@ -137,6 +137,14 @@ struct LoraParams {
     float* v;                     // shrink output (split mode; C-ABI v layout, div as stored); fused: nullptr
     const float* v_in;            // expand input
     int32_t v_blocks;
+    // kTPFused (NEXT-3, device-initiated TP exchange): every rank's exchange region is mapped into
+    // every process (CUDA IPC over NVLink); this launch's slot of each region:
+    float* peer_v[8];             //   v blocks [rank][proj][seg][token][r/div] of peer j (j = 0..N-1)
+    int32_t* peer_ctr[8];         //   per-item done counters of peer j
+    int32_t n_peers;              //   N
+    int32_t peer_rank;            //   this rank k: its shrink writes block k of every peer
+    int64_t peer_block;           //   floats per block (nproj * NR / div)
+    int32_t v_sum_blocks;         //   1: the expand sums the N blocks (o: all-reduce); 0: gathers them (q/k/v)
 };
 
 // Per-launch kernel configuration (chosen on the host, see api.cpp).

@@ -28,6 +28,7 @@ STATUS = {
     14: "CUDA", 15: "NO_DEVICE", 16: "NCCL",
 }
 TP_ID_BYTES = 128
+TP_P2P_HANDLE_BYTES = 64
 
 
 class SloraError(RuntimeError):
@@ -111,6 +112,10 @@ SIGNATURES = {
     "slora_tp_lora_o": [_VP, _VP, _I32, _VP, _I64, _VP, _I64, _VP],
     "slora_tp_get_stats": [_VP, ctypes.POINTER(TPStats)],
     "slora_batch_set_options": [_VP, ctypes.c_uint32],
+    "slora_tp_p2p_export": [_VP, _VP],
+    "slora_tp_p2p_open": [_VP, _VP],
+    "slora_tp_fused_qkv": [_VP, _VP, _I32, _VP, _I64, _VP, _VP, _VP],
+    "slora_tp_fused_o": [_VP, _VP, _I32, _VP, _I64, _VP, _I64, _VP],
     "slora_lora_apply_many": [_VP, _VP, _VP, _I32, _VP, ctypes.POINTER(_I32)],
     "slora_adapter_prefetch": [_VP, _I64, _I32, _VP, ctypes.c_float, ctypes.POINTER(_I32)],
     "slora_adapter_wait": [_VP, _I64],
@@ -361,6 +366,18 @@ class Pool:
         buf = ctypes.create_string_buffer(bytes(unique_id), TP_ID_BYTES)
         _check(lib().slora_tp_init(self.h, buf, rank, size))
 
+    def tp_p2p_export(self) -> bytes:
+        """NEXT-3: this rank's exchange region (allocated here) as a CUDA IPC handle."""
+        buf = ctypes.create_string_buffer(TP_P2P_HANDLE_BYTES)
+        _check(lib().slora_tp_p2p_export(self.h, buf))
+        return buf.raw
+
+    def tp_p2p_open(self, handles) -> None:
+        """Map every rank's exchange region (handles: the N ranks' export bytes, rank order)."""
+        blob = b"".join(bytes(h) for h in handles)
+        buf = ctypes.create_string_buffer(blob, len(blob))
+        _check(lib().slora_tp_p2p_open(self.h, buf))
+
     def tp_stats(self) -> dict:
         r = TPStats()
         _check(lib().slora_tp_get_stats(self.h, ctypes.byref(r)))
@@ -456,6 +473,17 @@ class Batch:
         """TP o: shrink -> NCCL all-reduce -> expand into column slice k of the base partial."""
         _check(lib().slora_tp_lora_o(self.pool.h, self.h, layer, _ptr(z), ldz, _ptr(base_partial), ld_base,
                                      _stream(stream)))
+
+    def tp_fused_qkv(self, layer: int, x, ldx: int, ys, ldys, stream=None) -> None:
+        """NEXT-3: TP q/k/v in one kernel, the v exchange by NVLink peer stores (slora_tp_fused_qkv)."""
+        yp = (_VP * 3)(*[_ptr(y) or None for y in ys])
+        ld = (_I64 * 3)(*ldys)
+        _check(lib().slora_tp_fused_qkv(self.pool.h, self.h, layer, _ptr(x), ldx, yp, ld, _stream(stream)))
+
+    def tp_fused_o(self, layer: int, z, ldz: int, base_partial, ld_base: int, stream=None) -> None:
+        """NEXT-3: TP o in one kernel, the all-reduce by peer stores summed in rank order (slora_tp_fused_o)."""
+        _check(lib().slora_tp_fused_o(self.pool.h, self.h, layer, _ptr(z), ldz, _ptr(base_partial), ld_base,
+                                      _stream(stream)))
 
     def expand(self, layer: int, projs, v, v_blocks: int, ys, ldys, stream=None) -> None:
         yp, ld = self._ys(ys, ldys)

@@ -122,11 +122,30 @@ class LibraryTP:
             uid = obj[0]
         pool.tp_init(uid, self.rank, self.N)
 
+    def enable_p2p(self, group=None):
+        """NEXT-3: map every rank's exchange region (CUDA IPC handles all-gathered over
+        torch.distributed); qkv/o then run the fused device-initiated kernels."""
+        h = self.pool.tp_p2p_export()
+        handles = [h]
+        if self.N > 1:
+            handles = [None] * self.N
+            dist.all_gather_object(handles, h, group=group)
+        self.pool.tp_p2p_open(handles)
+        self.p2p = True
+
+    p2p = False
+
     def qkv(self, batch, layer, x, ldx, y_shards, ld_y, stream=None):
-        batch.tp_qkv(layer, x, ldx, list(y_shards), list(ld_y), stream)
+        if self.p2p:
+            batch.tp_fused_qkv(layer, x, ldx, list(y_shards), list(ld_y), stream)
+        else:
+            batch.tp_qkv(layer, x, ldx, list(y_shards), list(ld_y), stream)
 
     def o(self, batch, layer, z_shard, ldz, base_partial, ld_base, stream=None):
-        batch.tp_o(layer, z_shard, ldz, base_partial, ld_base, stream)
+        if self.p2p:
+            batch.tp_fused_o(layer, z_shard, ldz, base_partial, ld_base, stream)
+        else:
+            batch.tp_o(layer, z_shard, ldz, base_partial, ld_base, stream)
 
     def stats(self):
         return self.pool.tp_stats()
