@@ -138,3 +138,56 @@ def test_tp_orchestration_world_size_2_gloo():
         # all-gather 3(N-1)Br/N, all-reduce 2(N-1)Br/N (B r -> sum of ranks)
         assert sent["allgather"] == 3 * (N - 1) * NR // N
         assert sent["allreduce"] == 2 * (N - 1) * NR // N
+
+
+class FakePool:
+    """Records what LibraryTP hands the library (no device)."""
+    tp_size = N
+
+    def __init__(self, rank):
+        self.tp_rank = rank
+        self.opened = None
+
+    def tp_init(self, uid, rank, size):
+        self.init = (rank, size)
+
+    def tp_p2p_export(self):
+        return bytes([self.tp_rank + 1]) * 64
+
+    def tp_p2p_open(self, handles):
+        self.opened = [bytes(h) for h in handles]
+
+
+def p2p_worker(rank, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=N)
+    try:
+        from paper_2311_03285_b200 import slora as sl
+        from paper_2311_03285_b200.tp import LibraryTP
+        sl.tp_unique_id = lambda: b"u" * 128  # rank 0's NCCL id draw (no device here)
+        pool = FakePool(rank)
+        tpl = LibraryTP(pool)
+        tpl.enable_p2p()
+        q.put((rank, pool.init, pool.opened, tpl.p2p))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_tp_p2p_handle_exchange_world_size_2_gloo():
+    """NEXT-3 host logic: every rank exports its exchange-region handle, the handles are
+    all-gathered over torch.distributed and every rank opens the SAME list in rank order (the
+    kernel indexes peers by rank)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = free_port()
+    procs = [ctx.Process(target=p2p_worker, args=(r, port, q)) for r in range(N)]
+    for pr in procs:
+        pr.start()
+    res = sorted(q.get(timeout=120) for _ in range(N))
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    want = [bytes([r + 1]) * 64 for r in range(N)]
+    for rank, init, opened, on in res:
+        assert init == (rank, N) and on
+        assert opened == want, (rank, opened)
