@@ -696,13 +696,14 @@ def run_ours(args):
     W.close()
     if ws == 1 and not tp_path and not args.no_secondary and name == "c2":
         sec = {}
-        for sname, sl in (("c2-mixed", 32), ("c1", 32), ("c4", 8)):
+        for sname, sl in (("c2-mixed", 32), ("c2-uniform", 32), ("c1", 32), ("c3", 40), ("c4", 8)):
             try:
                 sec[sname] = measure(sname, sl, 10, 3, stream)
             except Exception as e:  # reported, never silently dropped
                 sec[sname] = {"error": f"{type(e).__name__}: {e}"}
         sec["c4"]["note"] = "70B shapes unsharded on one GPU (the TP8 config's N=1 point); 8 layers (670 MB of " \
                             "adapter pages rotate, >> L2)"
+        sec["c3"]["note"] = "13B shapes unsharded on one GPU (the TP4 config's N=1 point), 40 layers"
         try:
             sec["c2-mlp"] = measure_mlp(stream)
         except Exception as e:

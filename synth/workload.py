@@ -53,6 +53,8 @@ CONFIGS = {
     "c1": Config("c1-7b-r8-decode64-fp16", 1, 4096, 1000, (8,), "f16", 1.0, 64),
     # configs[2]: Llama-7B, 2000 adapters ranks {64,32,16,8} Zipf, fp16 (S2)
     "c2": Config("c2-7b-mixedrank-decode64-fp16", 2, 4096, 2000, (64, 32, 16, 8), "f16", 1.0, 64),
+    # C2 with uniform adapter popularity (SURVEY 8(d) variant (ii): ~63 distinct adapters of 64 tokens)
+    "c2-uniform": Config("c2-7b-mixedrank-decode64-uniform-fp16", 2, 4096, 2000, (64, 32, 16, 8), "f16", None, 64),
     "c2-mixed": Config("c2-7b-mixedrank-prefill8+decode56-fp16", 2, 4096, 2000, (64, 32, 16, 8), "f16",
                        1.0, 56, prefill_requests=8),
     # configs[3]: Llama-13B (h=5120), ranks {64,32,16}, 4-way TP (n=400, Table default_trace 13B@A100-80G)
