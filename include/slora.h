@@ -105,7 +105,10 @@ typedef struct {
      * one partly used (reading R2): per adapter and layer, projection p takes
      * r * (ceil(proj_in[p]/P) + ceil(proj_out[p]/P)) pages.  Non-square
      * projections need tp_size == 1; every dim is a multiple of 16 bytes of
-     * the dtype and spans <= 8 pages; the host buffer of slora_adapter_load
+     * the dtype and spans <= 8 pages; a fused call's input width must fit
+     * one 32 KB ring slot (proj_in * esize + 16 <= 32768: 16376 for
+     * fp16/bf16, 8188 for fp32), else the call fails with SHAPE; the host
+     * buffer of slora_adapter_load
      * holds, per layer and projection p in order, A (proj_in x r) then B
      * (r x proj_out), row-major. */
     int32_t num_proj;           /* 1..8, or 0 = 4 (q,k,v,o)                    */
