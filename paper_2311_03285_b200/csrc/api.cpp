@@ -367,14 +367,16 @@ struct slora_batch {
     size_t off_tok = 0;
     // device arena (bump allocated per prepare) + its pinned staging mirror
     size_t arena_cap = 0, arena_used = 0;
-    void* arena_host = nullptr;
+    void* arena_host_buf[2] = {nullptr, nullptr};  // pinned mirrors, alternating per prepare (the host may
+                                                     // run one step further ahead of the GPU)
     void* arena_dev = nullptr;
     size_t dirty_lo = 0, dirty_hi = 0;  // host arena bytes not yet uploaded (arena_flush)
-    cudaEvent_t upload_ev = nullptr;
-    bool upload_pending = false;
+    cudaEvent_t upload_evs[2] = {nullptr, nullptr};
+    bool pending[2] = {false, false};
+    int cur = 0;                          // the mirror pair this prepare writes
     // call headers at fixed device addresses ([kernel cfg][nproj]); prepare rewrites them
     CallHdr* hdr_dev = nullptr;
-    CallHdr* hdr_host = nullptr;          // pinned mirror
+    CallHdr* hdr_host_buf[2] = {nullptr, nullptr};  // pinned header mirrors (with arena_host_buf)
     uint32_t used_masks[kMaxKc][kNpSlots] = {};  // call shapes launched since create: rebuilt by every prepare
     bool in_prepare = false;
     uint32_t options = 0;                 // slora_batch_set_options
@@ -1189,33 +1191,39 @@ extern "C" slora_status slora_batch_create(slora_pool_t p, slora_batch_t* out) {
     b->pool = p;
     p->batches.insert(b);
     if (p->dev) {
-        cudaError_t e = cudaEventCreateWithFlags(&b->upload_ev, cudaEventDisableTiming);
+        cudaError_t e = cudaEventCreateWithFlags(&b->upload_evs[0], cudaEventDisableTiming);
+        if (!e) e = cudaEventCreateWithFlags(&b->upload_evs[1], cudaEventDisableTiming);
         if (!e) e = cudaMalloc(&b->hdr_dev, sizeof(CallHdr) * kMaxKc * kNpSlots);
         if (!e) e = cudaMemset(b->hdr_dev, 0, sizeof(CallHdr) * kMaxKc * kNpSlots);
-        if (!e) e = cudaHostAlloc(&b->hdr_host, sizeof(CallHdr) * kMaxKc * kNpSlots, cudaHostAllocDefault);
+        for (int i = 0; i < 2 && !e; ++i)
+            e = cudaHostAlloc(&b->hdr_host_buf[i], sizeof(CallHdr) * kMaxKc * kNpSlots, cudaHostAllocDefault);
         if (e) {
             if (b->hdr_dev) cudaFree(b->hdr_dev);
             p->batches.erase(b);
             delete b;
             return fail(SLORA_ERR_CUDA, "batch create: %s", cudaGetErrorString(e));
         }
-        memset(b->hdr_host, 0, sizeof(CallHdr) * kMaxKc * kNpSlots);
+        for (int i = 0; i < 2; ++i) memset(b->hdr_host_buf[i], 0, sizeof(CallHdr) * kMaxKc * kNpSlots);
     }
     *out = b;
     return ok();
 }
 
 static void batch_free_device(slora_batch* b) {
-    if (b->upload_pending) cudaEventSynchronize(b->upload_ev);
+    for (int i = 0; i < 2; ++i) {
+        if (b->pending[i]) cudaEventSynchronize(b->upload_evs[i]);
+        if (b->arena_host_buf[i]) cudaFreeHost(b->arena_host_buf[i]);
+        if (b->hdr_host_buf[i]) cudaFreeHost(b->hdr_host_buf[i]);
+        if (b->upload_evs[i]) cudaEventDestroy(b->upload_evs[i]);
+        b->arena_host_buf[i] = nullptr;
+        b->hdr_host_buf[i] = nullptr;
+        b->upload_evs[i] = nullptr;
+        b->pending[i] = false;
+    }
     if (b->arena_dev) cudaFree(b->arena_dev);
-    if (b->arena_host) cudaFreeHost(b->arena_host);
     if (b->hdr_dev) cudaFree(b->hdr_dev);
-    if (b->hdr_host) cudaFreeHost(b->hdr_host);
     b->hdr_dev = nullptr;
-    b->hdr_host = nullptr;
-    cudaEventDestroy(b->upload_ev);
-    b->arena_dev = b->arena_host = nullptr;
-    b->upload_pending = false;
+    b->arena_dev = nullptr;
 }
 
 extern "C" slora_status slora_batch_destroy(slora_batch_t b) {
@@ -1244,7 +1252,7 @@ size_t arena_put(slora_batch* b, const void* src, size_t n, cudaStream_t, cudaEr
         return 0;
     }
     if (n) {
-        memcpy(static_cast<uint8_t*>(b->arena_host) + off, src, n);
+        memcpy(static_cast<uint8_t*>(b->arena_host_buf[b->cur]) + off, src, n);
         if (b->dirty_hi == b->dirty_lo) b->dirty_lo = off;
         b->dirty_hi = off + n;
     }
@@ -1256,7 +1264,7 @@ size_t arena_put(slora_batch* b, const void* src, size_t n, cudaStream_t, cudaEr
 void set_hdr(slora_pool* p, slora_batch* b, int kc, int np) {
     const slora_batch::Call& call = b->calls[kc][np];
     uint8_t* base = static_cast<uint8_t*>(b->arena_dev);
-    CallHdr& h = b->hdr_host[kc * kNpSlots + np];
+    CallHdr& h = b->hdr_host_buf[b->cur][kc * kNpSlots + np];
     h.tok_idx = reinterpret_cast<const int32_t*>(base + b->off_tok);
     h.items = reinterpret_cast<const DevItem*>(base + call.off_items);
     h.pieces = reinterpret_cast<const DevPiece*>(base + call.off_pieces);
@@ -1276,12 +1284,13 @@ cudaError_t arena_flush(slora_batch* b, cudaStream_t s) {
     cudaError_t e = cudaSuccess;
     if (b->dirty_hi > b->dirty_lo)
         e = cudaMemcpyAsync(static_cast<uint8_t*>(b->arena_dev) + b->dirty_lo,
-                            static_cast<uint8_t*>(b->arena_host) + b->dirty_lo, b->dirty_hi - b->dirty_lo,
+                            static_cast<uint8_t*>(b->arena_host_buf[b->cur]) + b->dirty_lo, b->dirty_hi - b->dirty_lo,
                             cudaMemcpyHostToDevice, s);
     b->dirty_lo = b->dirty_hi = 0;
-    if (!e) e = cudaMemcpyAsync(b->hdr_dev, b->hdr_host, sizeof(CallHdr) * kMaxKc * kNpSlots, cudaMemcpyHostToDevice, s);
-    if (!e) e = cudaEventRecord(b->upload_ev, s);
-    b->upload_pending = true;
+    if (!e) e = cudaMemcpyAsync(b->hdr_dev, b->hdr_host_buf[b->cur], sizeof(CallHdr) * kMaxKc * kNpSlots,
+                                cudaMemcpyHostToDevice, s);
+    if (!e) e = cudaEventRecord(b->upload_evs[b->cur], s);
+    b->pending[b->cur] = true;
     return e;
 }
 
@@ -1621,15 +1630,22 @@ extern "C" slora_status slora_batch_prepare(slora_batch_t b, const int64_t* tok_
                                                    size_t(max_items * max_pieces_per_item) * sizeof(DevPiece));
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     CUDA_TRY(cudaSetDevice(p->cfg.device));
-    if (b->upload_pending) CUDA_TRY(cudaEventSynchronize(b->upload_ev));  // pinned arena free again
-    b->upload_pending = false;
+    // the mirror pair of two prepares ago: free once its uploads completed (the host runs up to one
+    // step ahead of the GPU without waiting)
+    b->cur ^= 1;
+    if (b->pending[b->cur]) CUDA_TRY(cudaEventSynchronize(b->upload_evs[b->cur]));
+    b->pending[b->cur] = false;
     if (need > b->arena_cap) {
-        if (b->arena_host) CUDA_TRY(cudaFreeHost(b->arena_host));
+        for (int i = 0; i < 2; ++i) {
+            if (b->pending[i]) CUDA_TRY(cudaEventSynchronize(b->upload_evs[i]));
+            b->pending[i] = false;
+            if (b->arena_host_buf[i]) CUDA_TRY(cudaFreeHost(b->arena_host_buf[i]));
+            b->arena_host_buf[i] = nullptr;
+        }
         if (b->arena_dev) CUDA_TRY(cudaFreeAsync(b->arena_dev, s));
-        b->arena_host = nullptr;
         b->arena_dev = nullptr;
         const size_t cap = need + need / 4;  // sized from this batch's call shapes; grows at a later prepare
-        CUDA_TRY(cudaHostAlloc(&b->arena_host, cap, cudaHostAllocDefault));
+        for (int i = 0; i < 2; ++i) CUDA_TRY(cudaHostAlloc(&b->arena_host_buf[i], cap, cudaHostAllocDefault));
         CUDA_TRY(cudaMallocAsync(&b->arena_dev, cap, s));
         b->arena_cap = cap;
     }
@@ -1798,7 +1814,7 @@ slora_status ensure_call(slora_pool* p, slora_batch* b, int kc, uint32_t mask, v
     call.built = true;
     call.mask = mask;
     if (p->dev) {
-        if (!b->in_prepare && b->upload_pending) cudaEventSynchronize(b->upload_ev);  // pinned header mirror free
+        if (!b->in_prepare && b->pending[b->cur]) cudaEventSynchronize(b->upload_evs[b->cur]);  // mirror free
         set_hdr(p, b, kc, np);
         if (!b->in_prepare) {  // built lazily by a call: upload now (prepare flushes once at its end)
             if ((e = arena_flush(b, s))) return fail(SLORA_ERR_CUDA, "call descriptor upload: %s", cudaGetErrorString(e));
