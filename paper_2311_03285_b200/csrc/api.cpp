@@ -1117,7 +1117,12 @@ extern "C" slora_status slora_adapter_evict(slora_pool_t p, int64_t id, void* st
     if (it->second.pinned) return fail(SLORA_ERR_PINNED, "adapter %lld", (long long)id);
     Adapter& ad = it->second;
     // a load still in flight: its scatters must land before the pages can be reused
-    if (slora_status st = load_fence(p, ad, static_cast<cudaStream_t>(stream))) return st;
+    if (load_fence(p, ad, static_cast<cudaStream_t>(stream)) != SLORA_OK) {
+        // the load failed: nothing of it may still be writing once the copy stream drained; the
+        // adapter is released all the same (otherwise it could never leave the pool)
+        cudaStreamSynchronize(p->ld.stream);
+        cudaGetLastError();
+    }
     if (ad.load) cudaEventDestroy(ad.load->ready);  // still pending: destruction is deferred by CUDA
     for (int32_t pg : ad.pages) {
         p->owner[size_t(pg)] = kFree;
