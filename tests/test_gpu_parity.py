@@ -203,3 +203,39 @@ def test_bf16_70b_shapes_single_gpu():
     case = Case(cfg1, batch)
     x, ys, out = run_apply(case)
     check_all(case, x, ys, out)
+
+
+# ------------------------------------------------ degenerate / ragged ranks
+@pytest.mark.parametrize("dtype,hidden", [("f32", 512), ("f16", 4096), ("bf16", 5120)])
+def test_odd_ranks_bit_exact(dtype, hidden):
+    """Ranks that are not multiples of the 8-row shrink piece or the 4-row expand unroll (1, 3, 5,
+    7, 9, 33, 63): the ragged tails of both phases, bit-exact in the integer regime."""
+    ranks = (1, 3, 5, 7, 9, 33, 63)
+    cfg = wl.Config(f"odd-{dtype}", 12, hidden, 14, ranks, dtype, None, 40, num_layers=1)
+    batch = wl.make_batch(cfg)
+    case = Case(cfg, batch, order="shuffle", seed=21, weight_fn=int_weights(cfg), kv_interleave=1)
+    rng = np.random.default_rng(3)
+    x = wl.round_to(rng.integers(-1, 2, size=(batch.T, hidden)).astype(np.float32), dtype)
+    ys = [wl.round_to(rng.integers(-32, 33, size=(batch.T, hidden)).astype(np.float32), dtype)
+          for _ in range(4)]
+    x, ys, out = run_apply(case, x=x, ys=ys)
+    for p in range(4):
+        ref = case.oracle_proj(x, ys[p], 0, p)
+        assert np.array_equal(out[p], ref), f"proj {p}: max diff {np.abs(out[p] - ref).max()}"
+
+
+def test_single_token_single_adapter_and_all_tokens_one_adapter():
+    """Degenerate batches: one token; and every token on one rank-64 adapter (one segment of 64
+    scattered decode tokens: the gathered-MBGMM route)."""
+    from oracle import to_f64
+    cfg = wl.Config("one", 13, 4096, 1, (64,), "f16", None, 1, num_layers=1)
+    batch = wl.make_batch(cfg)
+    case = Case(cfg, batch, order="shuffle", seed=2)
+    x, ys, out = run_apply(case)
+    check_all(case, x, ys, out)
+    cfg = wl.Config("all-one", 14, 4096, 1, (64,), "f16", None, 64, num_layers=1)
+    batch = wl.make_batch(cfg)
+    assert len(batch.ranks) == 1
+    case = Case(cfg, batch, order="shuffle", seed=2)
+    x, ys, out = run_apply(case)
+    check_all(case, x, ys, out)
