@@ -168,7 +168,10 @@ cudaError_t configure_lora_kernels(int device);
 // Long prefill runs (>= theta consecutive x rows of one adapter) go to the
 // tensor-core MBGMM kernels (mbgmm.cu); units are built on the host.
 constexpr int kMgTileTok = 64;   // tokens per tile (4 mma m-tiles)
-constexpr int kMgRows = 16;      // stored A rows per shrink unit
+#ifndef SLORA_MG_ROWS
+#define SLORA_MG_ROWS 16
+#endif
+constexpr int kMgRows = SLORA_MG_ROWS;  // stored A rows per shrink unit
 constexpr int kMgCols = 1024;    // output columns per expand unit (rank <= 32; 512 above)
 // expand slab width: B slab of r x cols 16-bit <= 64 KB (two CTAs per SM)
 inline int mbgmm_expand_cols(int rank) { return rank <= 32 ? kMgCols : kMgCols / 2; }
