@@ -129,15 +129,22 @@ constexpr int kXTileBytes = kMgTileTok * 64 * 2;       // 64 tokens x 64 element
 
 __host__ __device__ inline size_t al(size_t x, size_t a) { return (x + a - 1) & ~(a - 1); }
 
-// shrink smem: [bars][A rows R x (K*2+16)][x ring 8 x 8 KB, 1 KB aligned], R = 16 stored
-// A rows per unit, or 8 when 16 rows of K do not fit (K = 8192: 16 rows would be 256 KB)
-__host__ __device__ inline size_t mg_shrink_smem_rows(int64_t K, int rows) {
-    return al(256 + size_t(rows) * (K * 2 + 16), 1024) + size_t(kXStages) * kXTileBytes + 1024;
+// shrink smem: [bars][A rows R x (K*2+16)][x ring of 8 KB stages, 1 KB aligned]: R = 16 stored A
+// rows per unit with as many x stages as fit (<= kXStages), or 8 rows when 16 rows leave room for
+// fewer than 8 stages (K = 8192: 16 rows alone would be 256 KB)
+__host__ __device__ inline size_t mg_shrink_base(int64_t K, int rows) {
+    return al(256 + size_t(rows) * (K * 2 + 16), 1024) + 1024;
 }
-__host__ __device__ inline int mg_rows(int64_t K) {
-    return mg_shrink_smem_rows(K, kMgRows) <= size_t(227) * 1024 ? kMgRows : kMgRows / 2;
+__host__ __device__ inline int mg_xstages_rows(int64_t K, int rows) {
+    const size_t base = mg_shrink_base(K, rows), lim = size_t(227) * 1024;
+    const int st = base >= lim ? 0 : int((lim - base) / kXTileBytes);
+    return st < kXStages ? st : kXStages;
 }
-__host__ __device__ inline size_t mg_shrink_smem(int64_t K) { return mg_shrink_smem_rows(K, mg_rows(K)); }
+__host__ __device__ inline int mg_rows(int64_t K) { return mg_xstages_rows(K, kMgRows) >= 8 ? kMgRows : kMgRows / 2; }
+__host__ __device__ inline int mg_xstages(int64_t K) { return mg_xstages_rows(K, mg_rows(K)); }
+__host__ __device__ inline size_t mg_shrink_smem(int64_t K) {
+    return mg_shrink_base(K, mg_rows(K)) + size_t(mg_xstages(K)) * kXTileBytes;
+}
 // expand smem: [bars][B slab r x (nc*2+16)][v hi, lo: 64 x (rp+8) 16-bit each]; the host
 // sizes slabs (mbgmm_expand_cols) so that two CTAs fit on an SM (one loads while one computes)
 __host__ __device__ inline size_t mg_expand_smem_unit(int r, int nc) {
@@ -163,9 +170,10 @@ __global__ void __launch_bounds__(kMgThreads, 1) mbgmm_shrink_kernel(const __gri
     xring = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(xring) + 1023) & ~uintptr_t(1023));
     const int nrows = u.b;
     const int nkc = K / 64;
+    const int xst = mg_xstages(K);  // x ring stages
     if (tid == 0) {
         bar_init(abar, 1);
-        for (int s = 0; s < kXStages; ++s) {
+        for (int s = 0; s < xst; ++s) {
             bar_init(&xfull[s], 1);
             bar_init(&xempty[s], kMgConsumers);
         }
@@ -185,8 +193,8 @@ __global__ void __launch_bounds__(kMgThreads, 1) mbgmm_shrink_kernel(const __gri
         grid_wait();
         if (lane == 0)
             for (int kc = 0; kc < nkc; ++kc) {
-                const int s = kc % kXStages;
-                if (kc >= kXStages) bar_wait(&xempty[s], ((kc / kXStages) - 1) & 1);
+                const int s = kc % xst;
+                if (kc >= xst) bar_wait(&xempty[s], ((kc / xst) - 1) & 1);
                 bar_expect(&xfull[s], kXTileBytes);
                 tma_2d(xring + size_t(s) * kXTileBytes, &p.xmap, kc * 64, u.row0, &xfull[s]);
             }
@@ -202,8 +210,8 @@ __global__ void __launch_bounds__(kMgThreads, 1) mbgmm_shrink_kernel(const __gri
     float d[2][4] = {};
     bar_wait(abar, 0);
     for (int kc = 0; kc < nkc; ++kc) {
-        const int s = kc % kXStages;
-        bar_wait(&xfull[s], (kc / kXStages) & 1);
+        const int s = kc % xst;
+        bar_wait(&xfull[s], (kc / xst) & 1);
         const uint32_t xs = xbase + uint32_t(s) * kXTileBytes;
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk) {
