@@ -172,7 +172,10 @@ constexpr int kMgTileTok = 64;   // tokens per tile (4 mma m-tiles)
 #define SLORA_MG_ROWS 16
 #endif
 constexpr int kMgRows = SLORA_MG_ROWS;  // stored A rows per shrink unit
-constexpr int kMgCols = 1024;    // output columns per expand unit (rank <= 32; 512 above)
+#ifndef SLORA_MG_COLS
+#define SLORA_MG_COLS 1024
+#endif
+constexpr int kMgCols = SLORA_MG_COLS;  // output columns per expand unit (rank <= 32; half above)
 // expand slab width: B slab of r x cols 16-bit <= 64 KB (two CTAs per SM)
 inline int mbgmm_expand_cols(int rank) { return rank <= 32 ? kMgCols : kMgCols / 2; }
 constexpr int kMgDefaultTheta = 32;  // run length from which MBGMM is used (SLORA_MBGMM_MIN)
