@@ -897,6 +897,8 @@ def run_e2e(W, stream, steps):
     batch from the host token map, runs the layers and reads every updated
     output back D2H."""
     import torch
+    if not W.tp_path:
+        return run_e2e_pipelined(W, stream, steps)
     ins = [W.x, W.y] + ([W.z, W.base] if W.tp_path else [])
     outs = [W.y] + ([W.base] if W.tp_path else [])
     hin = [t.cpu().pin_memory() for t in ins]
@@ -924,6 +926,65 @@ def run_e2e(W, stream, steps):
     ms = t0.elapsed_time(t1) / steps
     return {"value": round(W.Tad * W.L / (ms / 1e3), 1), "unit": UNIT, "h2d_bytes_per_step": int(bi),
             "d2h_bytes_per_step": int(bo), "ms_per_step": round(ms, 4)}
+
+
+def run_e2e_pipelined(W, stream, steps):
+    """e2e on one GPU with the host<->device copies pipelined by layer: a copy-in stream moves
+    layer l's x and y from pinned host memory while the compute stream runs layer l-1 (one
+    slora_lora_apply_many call per layer: q/k/v, o) and a copy-out stream returns layer l-2's y.
+    Layer l's buffers are refilled for the next step only after their copy-out (per-layer events).
+    Same bytes as the serial form; the step ends when its last output is on the host."""
+    import torch
+    from paper_2311_03285_b200 import Batch
+    L, H = W.L, W.H
+    hx = W.x.cpu().pin_memory()
+    hy = W.y.cpu().pin_memory()
+    hyo = torch.empty_like(W.y, device="cpu").pin_memory()
+    bi = hx.numel() * hx.element_size() + hy.numel() * hy.element_size() + W.T * 8
+    bo = hyo.numel() * hyo.element_size()
+    calls = [Batch.make_calls([(l, "qkv", W.x[l], H, [W.y[l, p] for p in range(4)], [H] * 4),
+                               (l, "o", W.x[l], H, [W.y[l, p] for p in range(4)], [H] * 4)]) for l in range(L)]
+    s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
+    ev_in = [torch.cuda.Event() for _ in range(L)]
+    ev_c = [torch.cuda.Event() for _ in range(L)]
+    ev_out = [torch.cuda.Event() for _ in range(L)]
+    started = [False]
+
+    def one():
+        W.dbatch.prepare(W.batch.token_adapter, stream=stream)
+        for l in range(L):
+            if started[0]:
+                s_in.wait_event(ev_out[l])  # layer l's previous outputs are on the host
+            with torch.cuda.stream(s_in):
+                W.x[l].copy_(hx[l], non_blocking=True)
+                W.y[l].copy_(hy[l], non_blocking=True)
+            ev_in[l].record(s_in)
+        for l in range(L):
+            stream.wait_event(ev_in[l])
+            W.dbatch.apply_many(calls[l], stream=stream)
+            ev_c[l].record(stream)
+            s_out.wait_event(ev_c[l])
+            with torch.cuda.stream(s_out):
+                hyo[l].copy_(W.y[l], non_blocking=True)
+            ev_out[l].record(s_out)
+        started[0] = True
+        stream.wait_event(ev_out[L - 1])  # the step is done when its last output is on the host
+
+    for _ in range(2):
+        one()
+    torch.cuda.synchronize()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for _ in range(steps):
+        one()
+    t1.record(stream)
+    torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1) / steps
+    return {"value": round(W.Tad * W.L / (ms / 1e3), 1), "unit": UNIT, "h2d_bytes_per_step": int(bi),
+            "d2h_bytes_per_step": int(bo), "ms_per_step": round(ms, 4),
+            "note": "per layer: pinned H2D of x, y on a copy stream || slora_lora_apply_many (q/k/v, o) || D2H of y "
+                    "on another copy stream; eager launches (no graph)"}
 
 
 # --------------------------------------------------------------- oracle arm
