@@ -928,12 +928,13 @@ def run_e2e(W, stream, steps):
             "d2h_bytes_per_step": int(bo), "ms_per_step": round(ms, 4)}
 
 
-def run_e2e_pipelined(W, stream, steps):
-    """e2e on one GPU with the host<->device copies pipelined by layer: a copy-in stream moves
-    layer l's x and y from pinned host memory while the compute stream runs layer l-1 (one
-    slora_lora_apply_many call per layer: q/k/v, o) and a copy-out stream returns layer l-2's y.
-    Layer l's buffers are refilled for the next step only after their copy-out (per-layer events).
-    Same bytes as the serial form; the step ends when its last output is on the host."""
+def run_e2e_pipelined(W, stream, steps, chunk=4):
+    """e2e on one GPU with the host<->device copies pipelined by groups of `chunk` layers: a
+    copy-in stream moves group g's x and y from pinned host memory while the compute stream runs
+    group g-1 (one slora_lora_apply_many call per group: q/k/v, o of each layer) and a copy-out
+    stream returns group g-2's y.  A group's buffers are refilled for the next step only after
+    their copy-out (per-group events).  Same bytes as the serial form; the step ends when its
+    last output is on the host."""
     import torch
     from paper_2311_03285_b200 import Batch
     L, H = W.L, W.H
@@ -942,33 +943,40 @@ def run_e2e_pipelined(W, stream, steps):
     hyo = torch.empty_like(W.y, device="cpu").pin_memory()
     bi = hx.numel() * hx.element_size() + hy.numel() * hy.element_size() + W.T * 8
     bo = hyo.numel() * hyo.element_size()
-    calls = [Batch.make_calls([(l, "qkv", W.x[l], H, [W.y[l, p] for p in range(4)], [H] * 4),
-                               (l, "o", W.x[l], H, [W.y[l, p] for p in range(4)], [H] * 4)]) for l in range(L)]
+    groups = [(g, min(g + chunk, L)) for g in range(0, L, chunk)]
+    calls = []
+    for a, b in groups:
+        cl = []
+        for l in range(a, b):
+            ys = [W.y[l, p] for p in range(4)]
+            cl += [(l, "qkv", W.x[l], H, ys, [H] * 4), (l, "o", W.x[l], H, ys, [H] * 4)]
+        calls.append(Batch.make_calls(cl))
     s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
-    ev_in = [torch.cuda.Event() for _ in range(L)]
-    ev_c = [torch.cuda.Event() for _ in range(L)]
-    ev_out = [torch.cuda.Event() for _ in range(L)]
+    n = len(groups)
+    ev_in = [torch.cuda.Event() for _ in range(n)]
+    ev_c = [torch.cuda.Event() for _ in range(n)]
+    ev_out = [torch.cuda.Event() for _ in range(n)]
     started = [False]
 
     def one():
         W.dbatch.prepare(W.batch.token_adapter, stream=stream)
-        for l in range(L):
+        for i, (a, b) in enumerate(groups):
             if started[0]:
-                s_in.wait_event(ev_out[l])  # layer l's previous outputs are on the host
+                s_in.wait_event(ev_out[i])  # the group's previous outputs are on the host
             with torch.cuda.stream(s_in):
-                W.x[l].copy_(hx[l], non_blocking=True)
-                W.y[l].copy_(hy[l], non_blocking=True)
-            ev_in[l].record(s_in)
-        for l in range(L):
-            stream.wait_event(ev_in[l])
-            W.dbatch.apply_many(calls[l], stream=stream)
-            ev_c[l].record(stream)
-            s_out.wait_event(ev_c[l])
+                W.x[a:b].copy_(hx[a:b], non_blocking=True)
+                W.y[a:b].copy_(hy[a:b], non_blocking=True)
+            ev_in[i].record(s_in)
+        for i, (a, b) in enumerate(groups):
+            stream.wait_event(ev_in[i])
+            W.dbatch.apply_many(calls[i], stream=stream)
+            ev_c[i].record(stream)
+            s_out.wait_event(ev_c[i])
             with torch.cuda.stream(s_out):
-                hyo[l].copy_(W.y[l], non_blocking=True)
-            ev_out[l].record(s_out)
+                hyo[a:b].copy_(W.y[a:b], non_blocking=True)
+            ev_out[i].record(s_out)
         started[0] = True
-        stream.wait_event(ev_out[L - 1])  # the step is done when its last output is on the host
+        stream.wait_event(ev_out[n - 1])  # the step is done when its last output is on the host
 
     for _ in range(2):
         one()
@@ -983,8 +991,8 @@ def run_e2e_pipelined(W, stream, steps):
     ms = t0.elapsed_time(t1) / steps
     return {"value": round(W.Tad * W.L / (ms / 1e3), 1), "unit": UNIT, "h2d_bytes_per_step": int(bi),
             "d2h_bytes_per_step": int(bo), "ms_per_step": round(ms, 4),
-            "note": "per layer: pinned H2D of x, y on a copy stream || slora_lora_apply_many (q/k/v, o) || D2H of y "
-                    "on another copy stream; eager launches (no graph)"}
+            "note": f"groups of {chunk} layers: pinned H2D of x, y on a copy stream || slora_lora_apply_many "
+                    "(q/k/v, o of each layer) || D2H of y on another copy stream; eager launches (no graph)"}
 
 
 # --------------------------------------------------------------- oracle arm
