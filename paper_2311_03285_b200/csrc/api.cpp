@@ -1305,7 +1305,8 @@ cudaError_t arena_flush(slora_batch* b, cudaStream_t s) {
 // deadlock-freedom argument, kernels.cu header).  The per-piece constant
 // stands for the fixed cost of a piece (barriers, v exchange).
 void schedule_pieces(const std::vector<DevPiece>& in, const std::vector<int64_t>& cost, int grid,
-                     std::vector<DevPiece>& out, std::vector<int32_t>& cta_off) {
+                     std::vector<DevPiece>& out, std::vector<int32_t>& cta_off,
+                     const std::vector<int32_t>* prio = nullptr) {
     grid = std::max(1, grid);
     std::vector<std::vector<int32_t>> lists(static_cast<size_t>(grid));
     std::vector<int64_t> load(static_cast<size_t>(grid), 0);
@@ -1316,8 +1317,12 @@ void schedule_pieces(const std::vector<DevPiece>& in, const std::vector<int64_t>
         std::vector<int32_t> idx;
         for (int32_t i = 0; i < int32_t(in.size()); ++i)
             if (in[size_t(i)].kind == kind) idx.push_back(i);
-        std::stable_sort(idx.begin(), idx.end(),
-                         [&](int32_t a, int32_t c) { return cost[size_t(a)] > cost[size_t(c)]; });
+        // largest first; equal costs (most shrink pieces: 8 full A rows) by priority: the pieces of
+        // the items whose expand pieces are largest first, so that their v is ready earliest
+        std::stable_sort(idx.begin(), idx.end(), [&](int32_t a, int32_t c) {
+            if (cost[size_t(a)] != cost[size_t(c)]) return cost[size_t(a)] > cost[size_t(c)];
+            return prio && (*prio)[size_t(a)] > (*prio)[size_t(c)];
+        });
         for (int32_t i : idx) {
             HE h = heap.top();
             heap.pop();
@@ -1457,7 +1462,15 @@ void build_call(slora_batch* b, const KernelCfg& k, int N, int nproj, uint32_t m
     }
     std::vector<DevPiece> pieces;
     std::vector<int64_t> cost;
-    const int64_t kPieceOverhead = 4096;
+    std::vector<int32_t> prio;  // tie-break among equal-cost pieces: the item's rank (see schedule_pieces)
+    static const int64_t kPieceOverhead = [] {  // bytes-equivalent fixed cost of a piece (LPT weight)
+        const char* e = getenv("SLORA_PIECE_OVH");
+        return e ? int64_t(atoll(e)) : int64_t(4096);
+    }();
+    static const bool by_rank = [] {
+        const char* e = getenv("SLORA_SCHED_PRIO");
+        return !(e && atoi(e) == 0);
+    }();
     for (int32_t ii = 0; ii < int32_t(call.items.size()); ++ii) {
         const DevItem& it = call.items[size_t(ii)];
         const int proj = proj_ids[it.pi];
@@ -1467,14 +1480,16 @@ void build_call(slora_batch* b, const KernelCfg& k, int N, int nproj, uint32_t m
                 const int nr = std::min(srows, ra - r0);
                 pieces.push_back({kPieceS, ii, r0, nr});
                 cost.push_back(int64_t(nr) * k.K * es + kPieceOverhead);
+                prio.push_back(by_rank ? it.rank : 0);
             }
         if (k.mode != kShrink)
             for_expand_chunks(proj_D(proj), item_dchunk(it.rank), [&](int64_t c0, int64_t dc) {
                 pieces.push_back({kPieceE, ii, int32_t(c0), int32_t(dc)});
                 cost.push_back(int64_t(it.rank) * dc * es + kPieceOverhead);
+                prio.push_back(by_rank ? it.rank : 0);
             });
     }
-    schedule_pieces(pieces, cost, k.grid, call.pieces, call.cta_off);
+    schedule_pieces(pieces, cost, k.grid, call.pieces, call.cta_off, &prio);
 }
 slora_status ensure_call(slora_pool* p, slora_batch* b, int kc, uint32_t mask, void* stream);
 
