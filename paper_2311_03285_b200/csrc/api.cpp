@@ -1366,13 +1366,13 @@ void build_call(slora_batch* b, const KernelCfg& k, int N, int nproj, uint32_t m
         const char* e = getenv("SLORA_HIRANK_SPLIT");
         return e ? atoi(e) : 0;
     }();
-    // Single-projection (o) calls: items of rank >= 32 get half-width expand
+    // Single-projection (o) calls: items of rank >= 64 get half-width expand
     // pieces, whose rank-64 pieces are otherwise the launch's stragglers
-    // (measured on C2 decode: 1.249 -> 1.237 ms/step; SLORA_O_HIRANK=r to
-    // move the threshold, 0 = off)
+    // (measured on C2 decode with the rank-ordered schedule: o launch 14.06 us
+    // at threshold 32, 13.56 at 64, 13.60 off; SLORA_O_HIRANK=r to move it, 0 = off)
     static const int o_hirank = [] {
         const char* e = getenv("SLORA_O_HIRANK");
-        return e ? atoi(e) : 32;
+        return e ? atoi(e) : 64;
     }();
     auto item_dchunk = [&](int rank) -> int64_t {  // divides the page (k.dchunk | P): pieces never straddle a page
         const int64_t half = k.dchunk / 2;
