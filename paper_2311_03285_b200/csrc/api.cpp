@@ -1393,7 +1393,18 @@ void build_call(slora_batch* b, const KernelCfg& k, int N, int nproj, uint32_t m
         for_expand_chunks(proj_D(pj), item_dchunk(rank), [&](int64_t, int64_t) { ++n; });
         return n;
     };
-    const int srows = kShrinkRows;  // stored A rows per shrink piece
+    // stored A rows per shrink piece: 16 for calls of several projections, 8 for single-projection
+    // (o) calls (measured on C2 decode with the rank-ordered schedule: q/k/v launch 22.80 -> 21.50 us
+    // with 16 rows, o launch 13.57 -> 14.07 us: its shorter chain wants more, smaller pieces)
+    static const int srows_multi = [] {
+        const char* e = getenv("SLORA_SHRINK_ROWS_MULTI");
+        return e ? std::max(1, std::min(kShrinkRows, atoi(e))) : std::min(kShrinkRows, 16);
+    }();
+    static const int srows_single = [] {
+        const char* e = getenv("SLORA_SHRINK_ROWS_SINGLE");
+        return e ? std::max(1, std::min(kShrinkRows, atoi(e))) : std::min(kShrinkRows, 8);
+    }();
+    const int srows = np == 1 ? srows_single : srows_multi;
     // (the MBGMM kernels index the default q,k,v,o page-table layout: square pools only)
     const bool use_runs = allow_mbgmm && k.mode == kFused && b->n_runs > 0 && all_square && pl->square;
     call.mg_s.clear();
@@ -1641,7 +1652,7 @@ extern "C" slora_status slora_batch_prepare(slora_batch_t b, const int64_t* tok_
     }
     (void)max_in;
     const int64_t max_pieces_per_item =
-        (kMaxRank + kShrinkRows - 1) / kShrinkRows + (max_out + dmin - 1) / dmin + (max_out + p->P - 1) / p->P;
+        kMaxRank /* shrink pieces: at most one per rank row */ + (max_out + dmin - 1) / dmin + (max_out + p->P - 1) / p->P;
     int n_shapes = 6;  // eager shapes + those launched since create (rebuilt below)
     for (auto& row : b->used_masks)
         for (uint32_t m : row) n_shapes += m ? 1 : 0;

@@ -518,9 +518,9 @@ __device__ __forceinline__ void shrink_piece_mma(const LoraParams& p, const Piec
         const int ge = min(gb + 8, nrows);
         const int need = (ge - 1) >> lg_rps;  // last slot this group reads
         for (; waited <= need; ++waited) {
-            int a = s0 + waited;
+            int a = s0 + waited;  // a piece may span more than one lap of the ring (16 rows of 16 KB)
             uint32_t lap = l0;
-            if (a >= ns) { a -= ns; ++lap; }
+            while (a >= ns) { a -= ns; ++lap; }
             mbar_wait(&full[a], lap & 1);
             if (warp == 0 && lane == 0) {
                 const int sq = int(lap) * ns + a;
@@ -533,7 +533,7 @@ __device__ __forceinline__ void shrink_piece_mma(const LoraParams& p, const Piec
             // row; their columns of D are discarded)
             const int row = min(gb + rr, ge - 1);
             int a = s0 + (row >> lg_rps);
-            if (a >= ns) a -= ns;
+            while (a >= ns) a -= ns;
             const uint32_t bbase = ring_u32 + uint32_t(a) * uint32_t(SS) + uint32_t(row & (rps - 1)) * srow +
                                    uint32_t(k0w + mi * 8) * ES;
             const int npair = kslice >> 5;  // k-step pairs
@@ -596,7 +596,7 @@ __device__ __forceinline__ void shrink_piece_mma(const LoraParams& p, const Piec
         __syncwarp();
         for (; released < fin; ++released) {
             int a = s0 + released;
-            if (a >= ns) a -= ns;
+            while (a >= ns) a -= ns;
             if (lane == 0) mbar_arrive(&empty[a]);
         }
     }

@@ -61,9 +61,9 @@ constexpr int kItemTokCap = SLORA_ITEM_TOK;
 constexpr int kMaxRank = 64;     // max rank of the MBGMV path
 constexpr int kMaxProj = 8;      // LoRA'd projections per layer (q,k,v,o by default; NEXT-4: + MLP)
 #ifndef SLORA_SHRINK_ROWS
-#define SLORA_SHRINK_ROWS 8
+#define SLORA_SHRINK_ROWS 16
 #endif
-constexpr int kShrinkRows = SLORA_SHRINK_ROWS;  // A rows per shrink piece
+constexpr int kShrinkRows = SLORA_SHRINK_ROWS;  // max A rows per shrink piece (the host picks <= this per call)
 constexpr int kConsumerWarps = 8;
 // warp roles: 0-7 consumers, then streamer 0, resolver, streamer 1, expand-v
 // prefetcher, shrink publisher, streamers 2.. (bulk-copy issue costs ~90 ns
