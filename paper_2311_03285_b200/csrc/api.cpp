@@ -2006,6 +2006,9 @@ extern "C" slora_status slora_lora_apply(slora_pool_t p, slora_batch_t b, int32_
     if (!call.mg_s.empty()) {
         st = launch_mbgmm_pair(p, b, call, q, x, ldx, stream);
         if (st) return st;
+        // every token went to MBGMM: no MBGMV launch (a batch with MBGMM segments is outside the
+        // replay-across-batches guarantee anyway, see slora_batch_set_options)
+        if (call.pieces.empty()) return ok();
     }
     return launch(p, kc, q, stream);
 }

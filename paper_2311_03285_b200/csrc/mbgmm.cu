@@ -616,20 +616,26 @@ int mbgmm_rows(int64_t K) { return mg_rows(K); }
 
 // Gathered MBGMM input: out row i = x row idx[i] (K elements, 16-byte vectors).
 // Launched without PDL: it reads x, which the previous kernel may write.
+// blockIdx.y splits a row into parts so that every SM has rows to move (a 256-row batch of 16 KB
+// rows is otherwise 256 CTAs, each latency-bound on its own row)
 __global__ void gather_rows_kernel(const uint4* __restrict__ x, int64_t ldx16, const int32_t* __restrict__ idx, int n,
                                    uint4* __restrict__ out, int64_t k16) {
+    const int64_t part = (k16 + gridDim.y - 1) / gridDim.y;
+    const int64_t c0 = int64_t(blockIdx.y) * part, c1 = c0 + part < k16 ? c0 + part : k16;
     for (int i = blockIdx.x; i < n; i += gridDim.x) {
         const uint4* src = x + int64_t(__ldg(idx + i)) * ldx16;
         uint4* dst = out + int64_t(i) * k16;
-        for (int64_t c = threadIdx.x; c < k16; c += blockDim.x) dst[c] = __ldcs(src + c);
+        for (int64_t c = c0 + threadIdx.x; c < c1; c += blockDim.x) dst[c] = __ldcs(src + c);
     }
 }
 cudaError_t launch_gather_rows(const void* x, int64_t ldx, const int32_t* idx, int n, void* out, int64_t K, int es,
                                cudaStream_t s) {
     if (n <= 0) return cudaSuccess;
     count_launch();
-    gather_rows_kernel<<<std::min(n, 148 * 8), 256, 0, s>>>(static_cast<const uint4*>(x), ldx * es / 16, idx, n,
-                                                            static_cast<uint4*>(out), K * es / 16);
+    const int64_t k16 = K * es / 16;
+    const int parts = int(std::max<int64_t>(1, std::min<int64_t>((148 * 8 + n - 1) / n, k16 / 256)));
+    gather_rows_kernel<<<dim3(unsigned(std::min(n, 148 * 8)), unsigned(parts)), 256, 0, s>>>(
+        static_cast<const uint4*>(x), ldx * es / 16, idx, n, static_cast<uint4*>(out), k16);
     return cudaGetLastError();
 }
 
