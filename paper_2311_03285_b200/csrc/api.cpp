@@ -295,7 +295,7 @@ struct slora_pool {
     float* ws_dev = nullptr;
     int64_t ws_stride = 0;            // floats per slot
     float* ws_slot_base = nullptr;    // slot of the call being launched
-    int64_t ws_region = 0;            // floats per workspace region: ring v, warp-task v, MBGMM v (kMgKsplit parts)
+    int64_t ws_region = 0;            // floats per workspace region: ring v, warp-task v, MBGMM v (kMgVParts k-split parts)
     uint64_t launch_seq = 0;
     int sms = 148;
     // tensor parallelism (slora_tp_*): the library's NCCL communicator and fp32 exchange buffers
@@ -1454,8 +1454,9 @@ void build_call(slora_batch* b, const KernelCfg& k, int N, int nproj, uint32_t m
                     u.scale = s.scale;
                     const bool whole = mbgmm_shrink_whole_rank();
                     const int srows = whole ? s.rank : mbgmm_rows(k.K);  // A rows per shrink unit
+                    const int split = mbgmm_split(k.K);
                     for (int r0 = 0; r0 < s.rank; r0 += srows)
-                        for (int ks = 0; ks < (whole ? kMgKsplit : 1); ++ks) {  // tcgen05: k-split parts
+                        for (int ks = 0; ks < split; ++ks) {  // k-split parts (the expand adds them in order)
                             u.a = r0;
                             u.b = std::min(srows, s.rank - r0);
                             u.pad = ks;
@@ -1572,10 +1573,11 @@ extern "C" slora_status slora_batch_prepare(slora_batch_t b, const int64_t* tok_
             return e ? atoi(e) : kMgDefaultTheta;
         }();
         const int mg_rows = mbgmm_rows(p->cfg.hidden);
+        const int mg_split = mbgmm_split(p->cfg.hidden);
         const bool ok_shape = !(b->options & SLORA_BATCH_MBGMV_ONLY) && p->square && p->cfg.dtype != SLORA_F32 && p->N() == 1 &&
                               theta > 0 && p->cfg.hidden % 64 == 0 &&
                               p->cfg.hidden % kMgCols % 64 == 0 && mbgmm_smem(false, p->cfg.hidden, 0) <= 227 * 1024 &&
-                              (!mbgmm_shrink_whole_rank() || (p->cfg.hidden / 64) % kMgKsplit == 0);
+                              (p->cfg.hidden / 64) % mg_split == 0;
         for (size_t si = 0; ok_shape && si < b->segs.size(); ++si) {
             const DevSeg& sg = b->segs[si];
             int32_t t = 0;
@@ -1587,7 +1589,7 @@ extern "C" slora_status slora_batch_prepare(slora_batch_t b, const int64_t* tok_
                     b->runs[si].push_back({t, e2});
                     ++b->n_runs;
                     const int64_t tiles = (e2 - t + kMgTileTok - 1) / kMgTileTok;
-                    b->mg_units_max += 4 * tiles * ((sg.rank + mg_rows - 1) / mg_rows +
+                    b->mg_units_max += 4 * tiles * (mg_split * ((sg.rank + mg_rows - 1) / mg_rows) +
                                                     (p->cfg.hidden + kMgCols / 2 - 1) / (kMgCols / 2));
                 }
                 t = e2;
@@ -1625,7 +1627,7 @@ extern "C" slora_status slora_batch_prepare(slora_batch_t b, const int64_t* tok_
                 ++b->n_runs;
                 b->mg_gather = true;
                 const int64_t tiles = (sg.n_tok + kMgTileTok - 1) / kMgTileTok;
-                b->mg_units_max += 4 * tiles * ((sg.rank + mg_rows - 1) / mg_rows +
+                b->mg_units_max += 4 * tiles * (mg_split * ((sg.rank + mg_rows - 1) / mg_rows) +
                                                 (p->cfg.hidden + kMgCols / 2 - 1) / (kMgCols / 2));
             }
     }
@@ -1713,7 +1715,7 @@ extern "C" slora_status slora_batch_prepare(slora_batch_t b, const int64_t* tok_
     }
     if (ws_need > p->ws_stride) {
         if (p->ws_dev) CUDA_TRY(cudaFreeAsync(p->ws_dev, s));
-        const int64_t st = ws_need * (2 + kMgKsplit);
+        const int64_t st = ws_need * (2 + kMgVParts);
         CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&p->ws_dev), sizeof(float) * st * kLaunchSlots, s));
         CUDA_TRY(cudaMemsetAsync(p->ws_dev, 0xFF, sizeof(float) * st * kLaunchSlots, s));
         p->ws_stride = st;
@@ -1956,7 +1958,8 @@ slora_status launch_mbgmm_pair(slora_pool* p, slora_batch* b, const slora_batch:
     m.yrow = b->mg_gather ? tok_dev : nullptr;
     m.page_elems = p->P;
     m.v = p->ws_slot_base + 2 * p->ws_region;  // the slot's MBGMM regions (see slora_batch_prepare)
-    m.ksplit = mbgmm_shrink_whole_rank() ? kMgKsplit : 1;
+    m.ksplit = mbgmm_split(H);
+    m.srows = mbgmm_rows(H);
     m.vpart = p->ws_region;
     for (int pj = 0; pj < 4; ++pj) {
         m.y[pj] = q.y[pj];

@@ -126,24 +126,30 @@ constexpr int kMgThreads = (kMgConsumers + 1) * 32;    // + producer warp
 #endif
 constexpr int kXStages = SLORA_MG_XSTAGES;  // 96 KB of x in flight per CTA (measured: 4 stages -9%, 8 -> 12 +1.5% on C2-mixed)
 constexpr int kXTileBytes = kMgTileTok * 64 * 2;       // 64 tokens x 64 elements (8 KB)
+constexpr int kMgMaxRows = 32;                          // stored A rows per shrink unit, at most
 
 __host__ __device__ inline size_t al(size_t x, size_t a) { return (x + a - 1) & ~(a - 1); }
 
-// shrink smem: [bars][A rows R x (K*2+16)][x ring of 8 KB stages, 1 KB aligned]: R = 16 stored A
-// rows per unit with as many x stages as fit (<= kXStages), or 8 rows when 16 rows leave room for
-// fewer than 8 stages (K = 8192: 16 rows alone would be 256 KB)
-__host__ __device__ inline size_t mg_shrink_base(int64_t K, int rows) {
-    return al(256 + size_t(rows) * (K * 2 + 16), 1024) + 1024;
+// shrink smem: [bars][A rows R x (Kp*2+16)][x ring of 8 KB stages, 1 KB aligned]: a unit holds R
+// stored A rows over Kp = K / split columns (its K part), with as many x stages as fit (<= kXStages).
+// The host picks (split, R) per hidden size (mg_plan): the x tile streams through the SM once per
+// R A rows, so fewer, taller units move less x; splitting K makes room for taller units.
+__host__ __device__ inline size_t mg_shrink_base(int64_t Kp, int rows) {
+    return al(256 + size_t(rows) * (Kp * 2 + 16), 1024) + 1024;
 }
-__host__ __device__ inline int mg_xstages_rows(int64_t K, int rows) {
-    const size_t base = mg_shrink_base(K, rows), lim = size_t(227) * 1024;
+__host__ __device__ inline int mg_xstages_rows(int64_t Kp, int rows) {
+    const size_t base = mg_shrink_base(Kp, rows), lim = size_t(227) * 1024;
     const int st = base >= lim ? 0 : int((lim - base) / kXTileBytes);
     return st < kXStages ? st : kXStages;
 }
-__host__ __device__ inline int mg_rows(int64_t K) { return mg_xstages_rows(K, kMgRows) >= 8 ? kMgRows : kMgRows / 2; }
-__host__ __device__ inline int mg_xstages(int64_t K) { return mg_xstages_rows(K, mg_rows(K)); }
-__host__ __device__ inline size_t mg_shrink_smem(int64_t K) {
-    return mg_shrink_base(K, mg_rows(K)) + size_t(mg_xstages(K)) * kXTileBytes;
+// the tallest unit (32, 16 or 8 A rows) that leaves room for >= 8 x stages
+__host__ __device__ inline int mg_rows_kp(int64_t Kp) {
+    for (int r = kMgMaxRows; r > 8; r /= 2)
+        if (mg_xstages_rows(Kp, r) >= 8) return r;
+    return 8;
+}
+__host__ __device__ inline size_t mg_shrink_smem_kp(int64_t Kp, int rows) {
+    return mg_shrink_base(Kp, rows) + size_t(mg_xstages_rows(Kp, rows)) * kXTileBytes;
 }
 // expand smem: [bars][B slab r x (nc*2+16)][v hi, lo: 64 x (rp+8) 16-bit each]; the host
 // sizes slabs (mbgmm_expand_cols) so that two CTAs fit on an SM (one loads while one computes)
@@ -152,25 +158,27 @@ __host__ __device__ inline size_t mg_expand_smem_unit(int r, int nc) {
     return 256 + size_t(r) * (size_t(nc) * 2 + 16) + 2 * size_t(kMgTileTok) * (rp + 8) * 2 + 128;
 }
 
-template <typename T>
+// NG = 16-row groups per unit (1: <= 16 A rows, 2: <= 32)
+template <typename T, int NG>
 __global__ void __launch_bounds__(kMgThreads, 1) mbgmm_shrink_kernel(const __grid_constant__ MgParams p) {
     using O = Mma<T>;
     constexpr int ES = 2;
     extern __shared__ __align__(1024) unsigned char sm[];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const MgUnit u = p.units[blockIdx.x];
-    const int K = p.K;
-    const uint32_t arow = uint32_t(K) * ES + 16;  // staggered A row stride
+    const int Kp = p.K / p.ksplit;                  // this unit's part of K (u.pad = part)
+    const int kb0 = u.pad * (Kp / 64);              // its first 64-column x block
+    const uint32_t arow = uint32_t(Kp) * ES + 16;  // staggered A row stride
     uint64_t* abar = reinterpret_cast<uint64_t*>(sm);
     uint64_t* xfull = abar + 1;
     uint64_t* xempty = xfull + kXStages;
     unsigned char* arows = sm + 256;
-    unsigned char* xring = sm + al(256 + size_t(mg_rows(K)) * arow, 1024);
+    unsigned char* xring = sm + al(256 + size_t(p.srows) * arow, 1024);
     // the dynamic smem base is 1 KB aligned only up to the driver's guarantee: align the ring explicitly
     xring = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(xring) + 1023) & ~uintptr_t(1023));
     const int nrows = u.b;
-    const int nkc = K / 64;
-    const int xst = mg_xstages(K);  // x ring stages
+    const int nkc = Kp / 64;
+    const int xst = mg_xstages_rows(Kp, p.srows);  // x ring stages
     if (tid == 0) {
         bar_init(abar, 1);
         for (int s = 0; s < xst; ++s) {
@@ -185,18 +193,19 @@ __global__ void __launch_bounds__(kMgThreads, 1) mbgmm_shrink_kernel(const __gri
         // ---- producer: the group's A rows (pages: loader-written, safe before the PDL wait), then x tiles
         const int proj = p.proj_ids[u.pi];
         const int32_t* tab = u.tab + int64_t((p.layer * 4 + proj) * 2) * u.rank;  // [A rows][B rows]
-        if (lane == 0) bar_expect(abar, uint32_t(nrows) * uint32_t(K) * ES);
+        if (lane == 0) bar_expect(abar, uint32_t(nrows) * uint32_t(Kp) * ES);
         __syncwarp();
         if (lane < nrows)
-            copy_g2s(arows + size_t(lane) * arow, static_cast<const T*>(p.pool) + int64_t(tab[u.a + lane]) * p.page_elems,
-                     uint32_t(K) * ES, abar);
+            copy_g2s(arows + size_t(lane) * arow,
+                     static_cast<const T*>(p.pool) + int64_t(tab[u.a + lane]) * p.page_elems + int64_t(kb0) * 64,
+                     uint32_t(Kp) * ES, abar);
         grid_wait();
         if (lane == 0)
             for (int kc = 0; kc < nkc; ++kc) {
                 const int s = kc % xst;
                 if (kc >= xst) bar_wait(&xempty[s], ((kc / xst) - 1) & 1);
                 bar_expect(&xfull[s], kXTileBytes);
-                tma_2d(xring + size_t(s) * kXTileBytes, &p.xmap, kc * 64, u.row0, &xfull[s]);
+                tma_2d(xring + size_t(s) * kXTileBytes, &p.xmap, (kb0 + kc) * 64, u.row0, &xfull[s]);
             }
         return;
     }
@@ -204,10 +213,15 @@ __global__ void __launch_bounds__(kMgThreads, 1) mbgmm_shrink_kernel(const __gri
     const int mi = lane >> 3, rr = lane & 7, g = lane >> 2, c = lane & 3;
     const int xrow = warp * 16 + ((mi & 1) << 3) + rr;      // A-operand (x) row of this lane's ldmatrix
     const int achk = mi >> 1;                               // its 16-byte chunk within the k-step
-    const int brow = min(((mi >> 1) << 3) + rr, nrows - 1); // B-operand (A row); padding rows repeat a real one
-    const uint32_t bbase = su32(arows) + uint32_t(brow) * arow + uint32_t((mi & 1) << 4);
+    uint32_t bbase[NG];
+#pragma unroll
+    for (int q = 0; q < NG; ++q) {
+        // B-operand (A row) of this lane in 16-row group q; padding rows repeat a real one
+        const int brow = min(16 * q + ((mi >> 1) << 3) + rr, nrows - 1);
+        bbase[q] = su32(arows) + uint32_t(brow) * arow + uint32_t((mi & 1) << 4);
+    }
     const uint32_t xbase = su32(xring) + uint32_t(xrow) * 128u;
-    float d[2][4] = {};
+    float d[2 * NG][4] = {};
     bar_wait(abar, 0);
     for (int kc = 0; kc < nkc; ++kc) {
         const int s = kc % xst;
@@ -215,26 +229,31 @@ __global__ void __launch_bounds__(kMgThreads, 1) mbgmm_shrink_kernel(const __gri
         const uint32_t xs = xbase + uint32_t(s) * kXTileBytes;
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk) {
-            uint32_t a[4], b[4];
+            uint32_t a[4];
             const int chunk = 2 * kk + achk;  // 128-byte swizzle: 16-byte chunk j of row r sits at j ^ (r & 7)
             ldm4(xs + uint32_t((chunk ^ (xrow & 7)) << 4), a);
-            ldm4(bbase + uint32_t(kc * 64 + kk * 16) * ES, b);
-            O::run(d[0], a, b[0], b[1]);
-            O::run(d[1], a, b[2], b[3]);
+#pragma unroll
+            for (int q = 0; q < NG; ++q) {
+                uint32_t b[4];
+                ldm4(bbase[q] + uint32_t(kc * 64 + kk * 16) * ES, b);
+                O::run(d[2 * q], a, b[0], b[1]);
+                O::run(d[2 * q + 1], a, b[2], b[3]);
+            }
         }
         __syncwarp();
         if (lane == 0) bar_arrive(&xempty[s]);
     }
     // d[n][0..1]: token 16w+g, A rows 8n+2c, 8n+2c+1; d[n][2..3]: token 16w+g+8
+    float* vout = p.v + int64_t(u.pad) * p.vpart;
 #pragma unroll
-    for (int n = 0; n < 2; ++n)
+    for (int n = 0; n < 2 * NG; ++n)
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
             const int t = warp * 16 + g + 8 * h;
 #pragma unroll
             for (int e = 0; e < 2; ++e) {
                 const int row = 8 * n + 2 * c + e;
-                if (t < u.nt && row < nrows) p.v[u.vbase + int64_t(t) * u.rank + u.a + row] = d[n][2 * h + e];
+                if (t < u.nt && row < nrows) vout[u.vbase + int64_t(t) * u.rank + u.a + row] = d[n][2 * h + e];
             }
         }
 }
@@ -612,7 +631,32 @@ static bool use_tc() {
     return on;
 }
 
-int mbgmm_rows(int64_t K) { return mg_rows(K); }
+// (split, rows) of the mma.sync shrink for hidden size K: SLORA_MG_SPLIT (K parts) and
+// SLORA_MG_SROWS (A rows per unit, <= 32) override the defaults
+int mbgmm_split(int64_t K) {
+    if (use_tc()) return kMgKsplit;
+    static const int env = [] {
+        const char* e = getenv("SLORA_MG_SPLIT");
+        return e ? atoi(e) : 0;
+    }();
+    // default: K parts of 2048 columns at K >= 8192 (32-row units, x streamed twice per rank-64
+    // tile instead of eight times: C4 60.6 -> 50.5 us per launch), whole K below (K = 4096 on
+    // C2-mixed: split 2 / 4 measured 12% / 10% slower, its long runs already fill the GPU)
+    int sp = env > 0 ? env : (K >= 8192 ? int(K / 2048) : 1);
+    while (sp > 1 && ((K / 64) % sp != 0 || sp > kMgVParts)) sp /= 2;
+    return sp;
+}
+int mbgmm_rows(int64_t K) {
+    static const int env = [] {
+        const char* e = getenv("SLORA_MG_SROWS");
+        return e ? atoi(e) : 0;
+    }();
+    const int64_t Kp = K / mbgmm_split(K);
+    const int auto_rows = mg_rows_kp(Kp);
+    if (env == 8 || env == 16 || env == 32)
+        return mg_xstages_rows(Kp, env) >= 2 ? env : auto_rows;
+    return auto_rows;
+}
 
 // Gathered MBGMM input: out row i = x row idx[i] (K elements, 16-byte vectors).
 // Launched without PDL: it reads x, which the previous kernel may write.
@@ -641,14 +685,17 @@ cudaError_t launch_gather_rows(const void* x, int64_t ldx, const int32_t* idx, i
 
 size_t mbgmm_smem(bool expand, int64_t K, int rmax) {
     return expand ? mg_expand_smem_unit(rmax, mbgmm_expand_cols(rmax))
-                  : (use_tc() ? mg_shrink_tc_smem(K) : mg_shrink_smem(K));
+                  : (use_tc() ? mg_shrink_tc_smem(K) : mg_shrink_smem_kp(K / mbgmm_split(K), mbgmm_rows(K)));
 }
 
 cudaError_t configure_mbgmm_kernels() {
     const int lim = 227 * 1024;
     cudaError_t e;
-    if ((e = cudaFuncSetAttribute(mbgmm_shrink_kernel<__half>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim))) return e;
-    if ((e = cudaFuncSetAttribute(mbgmm_shrink_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim)))
+    if ((e = cudaFuncSetAttribute(mbgmm_shrink_kernel<__half, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim))) return e;
+    if ((e = cudaFuncSetAttribute(mbgmm_shrink_kernel<__nv_bfloat16, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim)))
+        return e;
+    if ((e = cudaFuncSetAttribute(mbgmm_shrink_kernel<__half, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim))) return e;
+    if ((e = cudaFuncSetAttribute(mbgmm_shrink_kernel<__nv_bfloat16, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim)))
         return e;
     if ((e = cudaFuncSetAttribute(mbgmm_shrink_tc_kernel<__half>, cudaFuncAttributeMaxDynamicSharedMemorySize, lim)))
         return e;
@@ -671,11 +718,14 @@ cudaError_t launch_mbgmm(const MgParams& p, bool expand, int dtype, int n_units,
         return dtype == kF16 ? launch_kernel<__half>(mbgmm_shrink_tc_kernel<__half>, p, n_units, smem, s, pdl, kTcThreads)
                              : launch_kernel<__nv_bfloat16>(mbgmm_shrink_tc_kernel<__nv_bfloat16>, p, n_units, smem, s,
                                                             pdl, kTcThreads);
-    if (dtype == kF16)
-        return expand ? launch_kernel<__half>(mbgmm_expand_kernel<__half>, p, n_units, smem, s, pdl)
-                      : launch_kernel<__half>(mbgmm_shrink_kernel<__half>, p, n_units, smem, s, pdl);
-    return expand ? launch_kernel<__nv_bfloat16>(mbgmm_expand_kernel<__nv_bfloat16>, p, n_units, smem, s, pdl)
-                  : launch_kernel<__nv_bfloat16>(mbgmm_shrink_kernel<__nv_bfloat16>, p, n_units, smem, s, pdl);
+    if (expand)
+        return dtype == kF16 ? launch_kernel<__half>(mbgmm_expand_kernel<__half>, p, n_units, smem, s, pdl)
+                             : launch_kernel<__nv_bfloat16>(mbgmm_expand_kernel<__nv_bfloat16>, p, n_units, smem, s, pdl);
+    if (p.srows > 16)
+        return dtype == kF16 ? launch_kernel<__half>(mbgmm_shrink_kernel<__half, 2>, p, n_units, smem, s, pdl)
+                             : launch_kernel<__nv_bfloat16>(mbgmm_shrink_kernel<__nv_bfloat16, 2>, p, n_units, smem, s, pdl);
+    return dtype == kF16 ? launch_kernel<__half>(mbgmm_shrink_kernel<__half, 1>, p, n_units, smem, s, pdl)
+                         : launch_kernel<__nv_bfloat16>(mbgmm_shrink_kernel<__nv_bfloat16, 1>, p, n_units, smem, s, pdl);
 }
 
 }  // namespace slora

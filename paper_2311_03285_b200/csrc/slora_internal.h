@@ -202,6 +202,7 @@ struct alignas(64) MgParams {
     int32_t proj_ids[kMaxProj];
     int32_t layer, K;
     int32_t ksplit;      // shrink k-split parts (unit.pad = part); the expand sums them in order
+    int32_t srows;       // mma.sync shrink: stored A rows per unit (smem layout; <= 32)
     int64_t vpart;       // floats between the parts' v regions
     const int32_t* yrow; // gathered mode: y row of x-map row i (the batch's tok_idx); nullptr: row i
 };
@@ -209,8 +210,11 @@ struct alignas(64) MgParams {
 #define SLORA_MG_KSPLIT 2
 #endif
 constexpr int kMgKsplit = SLORA_MG_KSPLIT;  // tcgen05 shrink: K parts per (tile, projection)
+constexpr int kMgVParts = 8;                // MBGMM v workspace regions (k-split parts), >= kMgKsplit
+static_assert(kMgKsplit <= kMgVParts, "MBGMM v parts");
+int mbgmm_split(int64_t K);      // K parts of the MBGMM shrink (tcgen05: kMgKsplit; mma.sync: SLORA_MG_SPLIT, default 1)
 size_t mbgmm_smem(bool expand, int64_t K, int rmax);
-int mbgmm_rows(int64_t K);       // stored A rows per mma.sync shrink unit (16, or 8 when 16 rows of K do not fit)
+int mbgmm_rows(int64_t K);       // stored A rows per mma.sync shrink unit (32, 16 or 8: the tallest whose K part fits)
 cudaError_t launch_gather_rows(const void* x, int64_t ldx, const int32_t* idx, int n, void* out, int64_t K, int es,
                                cudaStream_t s);
 bool mbgmm_shrink_whole_rank();  // tcgen05 shrink: one unit per (tile, projection) covering all r A rows
