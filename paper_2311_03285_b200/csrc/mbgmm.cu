@@ -320,26 +320,37 @@ __global__ void __launch_bounds__(kMgThreads, 2) mbgmm_expand_kernel(const __gri
     named_sync(1, kMgConsumers * 32);
     bar_wait(bbar, 0);
     const int mi = lane >> 3, rr = lane & 7, g = lane >> 2, c = lane & 3;
-    // A operand (v): row = token 16w + (mi&1)*8 + rr, k chunk (mi>>1)*8
-    const int arow_ = warp * 16 + ((mi & 1) << 3) + rr;
+    // warps -> (16-token m-tile, column group): a tile of <= 16 / <= 32 tokens (gathered decode
+    // segments) gives each m-tile 4 / 2 warps that split the slab's 64-column sub-chunks, so all
+    // four warps keep y loads in flight instead of idling on empty m-tiles
+#ifndef SLORA_MG_NO_WSPLIT
+    const int wpm = u.nt <= 16 ? 4 : (u.nt <= 32 ? 2 : 1);
+#else
+    const int wpm = 1;
+#endif
+    const int mt = warp / wpm, cg = warp % wpm;
+    // A operand (v): row = token 16mt + (mi&1)*8 + rr, k chunk (mi>>1)*8
+    const int arow_ = mt * 16 + ((mi & 1) << 3) + rr;
     const uint32_t ahi = su32(vhi) + uint32_t(arow_ * vst + ((mi >> 1) << 3)) * ES;
     const uint32_t alo = su32(vlo) + uint32_t(arow_ * vst + ((mi >> 1) << 3)) * ES;
     T* y = reinterpret_cast<T*>(p.y[p.proj_ids[u.pi]]);
     const int64_t ldy = p.ldy[p.proj_ids[u.pi]];
-    const int t0 = warp * 16 + g, t1 = t0 + 8;
+    const int t0 = mt * 16 + g, t1 = t0 + 8;
     // gathered mode (segments of scattered tokens): x-map row i is token p.yrow[i]
     const int64_t yr0 = t0 < u.nt ? (p.yrow ? p.yrow[u.row0 + t0] : u.row0 + t0) : 0;
     const int64_t yr1 = t1 < u.nt ? (p.yrow ? p.yrow[u.row0 + t1] : u.row0 + t1) : 0;
     T* y0 = y + yr0 * ldy + u.a;
     T* y1 = y + yr1 * ldy + u.a;
+    const int sc0 = cg * 64, scs = wpm * 64;  // this warp's first sub-chunk and its stride
 #ifndef SLORA_MG_NO_YPF
-    // the slab's y rows into L2 now (one 128-byte line per prefetch, lanes c == 0 of each row
+    // the warp's y row lines into L2 now (one 128-byte line per prefetch, lanes c == 0 of each row
     // pair): the sub-chunk loads below then wait for L2, not HBM
     if (c == 0) {
-        for (int l = 0; l < nc * ES; l += 128) {
-            if (t0 < u.nt) asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const char*>(y0) + l));
-            if (t1 < u.nt) asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const char*>(y1) + l));
-        }
+        for (int sc = sc0; sc < nc; sc += scs)
+            for (int l = sc * ES; l < (sc + 64) * ES && l < nc * ES; l += 128) {
+                if (t0 < u.nt) asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const char*>(y0) + l));
+                if (t1 < u.nt) asm volatile("prefetch.global.L2 [%0];" ::"l"(reinterpret_cast<const char*>(y1) + l));
+            }
     }
 #endif
     // y is software-pipelined one 64-column sub-chunk ahead: the next sub-chunk's
@@ -353,15 +364,16 @@ __global__ void __launch_bounds__(kMgThreads, 2) mbgmm_expand_kernel(const __gri
             dst[n][1] = t1 < u.nt ? *reinterpret_cast<const uint32_t*>(y1 + col) : 0u;
         }
     };
-    load_y(0, yn);
-    for (int sc = 0; sc < nc; sc += 64) {
+    if (mt * 16 >= u.nt) return;  // (wpm = 1: an m-tile past the tile's tokens)
+    if (sc0 < nc) load_y(sc0, yn);
+    for (int sc = sc0; sc < nc; sc += scs) {
         uint32_t yv[8][2];
 #pragma unroll
         for (int n = 0; n < 8; ++n) {
             yv[n][0] = yn[n][0];
             yv[n][1] = yn[n][1];
         }
-        if (sc + 64 < nc) load_y(sc + 64, yn);
+        if (sc + scs < nc) load_y(sc + scs, yn);
         float d[8][4] = {};
         for (int k = 0; k < rp; k += 16) {
             uint32_t ah[4], alw[4];
