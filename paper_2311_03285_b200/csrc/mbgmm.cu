@@ -293,19 +293,30 @@ __global__ void __launch_bounds__(kMgThreads, 2) mbgmm_expand_kernel(const __gri
     // v tile -> smem, split into hi + lo (zero beyond the tile's tokens and the rank)
     // (eight independent loads in flight per thread, then the conversions: a serial
     // load -> store loop waits one L2 round trip per element)
-    constexpr int kU = 8;
+    // the k-split parts are summed part by part with kU loads in flight per round (a per-element
+    // loop over the parts waited one L2 round trip per part and element batch)
+#ifndef SLORA_MG_VU
+#define SLORA_MG_VU 8
+#endif
+    constexpr int kU = SLORA_MG_VU;
     const int nel = kMgTileTok * rp;
     for (int e0 = tid; e0 < nel; e0 += kU * kMgConsumers * 32) {
         float val[kU];
 #pragma unroll
-        for (int q = 0; q < kU; ++q) {
-            const int e = e0 + q * kMgConsumers * 32;
-            const int t = e / rp, j = e % rp;
-            float a = 0.f;
-            if (e < nel && t < u.nt && j < r)
-                for (int ks = 0; ks < p.ksplit; ++ks) a += __ldcg(p.v + ks * p.vpart + u.vbase + int64_t(t) * r + j);
-            val[q] = a;  // the shrink's k-split partial sums, added in part order (deterministic)
-        }
+        for (int q = 0; q < kU; ++q) val[q] = 0.f;
+        if (e0 < u.nt * rp)
+            for (int ks = 0; ks < p.ksplit; ++ks) {
+                const float* vp = p.v + ks * p.vpart + u.vbase;
+                float tmp[kU];
+#pragma unroll
+                for (int q = 0; q < kU; ++q) {
+                    const int e = e0 + q * kMgConsumers * 32;
+                    const int t = e / rp, j = e % rp;
+                    tmp[q] = (e < nel && t < u.nt && j < r) ? __ldcg(vp + int64_t(t) * r + j) : 0.f;
+                }
+#pragma unroll
+                for (int q = 0; q < kU; ++q) val[q] += tmp[q];  // parts added in order (deterministic)
+            }
 #pragma unroll
         for (int q = 0; q < kU; ++q) {
             const int e = e0 + q * kMgConsumers * 32;
