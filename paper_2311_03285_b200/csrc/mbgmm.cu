@@ -153,9 +153,12 @@ __host__ __device__ inline size_t mg_shrink_smem_kp(int64_t Kp, int rows) {
 }
 // expand smem: [bars][B slab r x (nc*2+16)][v hi, lo: 64 x (rp+8) 16-bit each]; the host
 // sizes slabs (mbgmm_expand_cols) so that two CTAs fit on an SM (one loads while one computes)
+// [y staging: one 16-row x 64-column tile per consumer warp, rows kYs 16-bit elements apart]
+constexpr int kYs = 72;  // 144-byte rows: the accumulator-layout accesses hit 32 distinct banks
 __host__ __device__ inline size_t mg_expand_smem_unit(int r, int nc) {
     const int rp = (r + 15) & ~15;
-    return 256 + size_t(r) * (size_t(nc) * 2 + 16) + 2 * size_t(kMgTileTok) * (rp + 8) * 2 + 128;
+    return 256 + size_t(r) * (size_t(nc) * 2 + 16) + 2 * size_t(kMgTileTok) * (rp + 8) * 2 +
+           size_t(kMgConsumers) * 16 * kYs * 2 + 128;
 }
 
 // NG = 16-row groups per unit (1: <= 16 A rows, 2: <= 32)
@@ -364,27 +367,33 @@ __global__ void __launch_bounds__(kMgThreads, 2) mbgmm_expand_kernel(const __gri
             }
     }
 #endif
-    // y is software-pipelined one 64-column sub-chunk ahead: the next sub-chunk's
-    // loads fly while this one's MMAs run; each y element is read-modify-written once
-    uint32_t yn[8][2];
-    auto load_y = [&](int sc, uint32_t (&dst)[8][2]) {
-#pragma unroll
-        for (int n = 0; n < 8; ++n) {
-            const int col = sc + 8 * n + 2 * c;
-            dst[n][0] = t0 < u.nt ? *reinterpret_cast<const uint32_t*>(y0 + col) : 0u;
-            dst[n][1] = t1 < u.nt ? *reinterpret_cast<const uint32_t*>(y1 + col) : 0u;
-        }
-    };
     if (mt * 16 >= u.nt) return;  // (wpm = 1: an m-tile past the tile's tokens)
-    if (sc0 < nc) load_y(sc0, yn);
-    for (int sc = sc0; sc < nc; sc += scs) {
-        uint32_t yv[8][2];
+    // y moves through a warp-private smem tile in whole 128-byte rows (coalesced 16-byte vectors:
+    // lane = row 4i + lane/8, 16-byte chunk lane%8), one 64-column sub-chunk ahead in registers;
+    // the accumulator-layout read-modify-write happens in smem; each y element is read and
+    // written once
+    uint16_t* ys = vlo + kMgTileTok * vst + warp * 16 * kYs;
+    const int vr = lane >> 3, vc = (lane & 7) * 8;
+    T* yrow4[4];
+    bool live[4];
 #pragma unroll
-        for (int n = 0; n < 8; ++n) {
-            yv[n][0] = yn[n][0];
-            yv[n][1] = yn[n][1];
-        }
-        if (sc + scs < nc) load_y(sc + scs, yn);
+    for (int i = 0; i < 4; ++i) {
+        const int t = mt * 16 + 4 * i + vr;
+        live[i] = t < u.nt;
+        yrow4[i] = y + (live[i] ? (p.yrow ? p.yrow[u.row0 + t] : u.row0 + t) : 0) * ldy + u.a + vc;
+    }
+    uint4 yn[4];
+    auto load_y = [&](int sc) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+            if (live[i]) yn[i] = *reinterpret_cast<const uint4*>(yrow4[i] + sc);
+    };
+    if (sc0 < nc) load_y(sc0);
+    for (int sc = sc0; sc < nc; sc += scs) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+            *reinterpret_cast<uint4*>(ys + (4 * i + vr) * kYs + vc) = yn[i];
+        if (sc + scs < nc) load_y(sc + scs);
         float d[8][4] = {};
         for (int k = 0; k < rp; k += 16) {
             uint32_t ah[4], alw[4];
@@ -405,19 +414,22 @@ __global__ void __launch_bounds__(kMgThreads, 2) mbgmm_expand_kernel(const __gri
 #endif
             }
         }
-        // y += scale * D: d[n][0..1] token t0, columns sc + 8n + 2c (+1); d[n][2..3] token t1
+        __syncwarp();
+        // y += scale * D: d[n][0..1] row g, columns 8n + 2c (+1); d[n][2..3] row g + 8
 #pragma unroll
-        for (int n = 0; n < 8; ++n) {
-            const int col = sc + 8 * n + 2 * c;
-            if (t0 < u.nt) {
-                const float2 f = O::unpack2(yv[n][0]);
-                *reinterpret_cast<uint32_t*>(y0 + col) = O::pack2(f.x + u.scale * d[n][0], f.y + u.scale * d[n][1]);
+        for (int n = 0; n < 8; ++n)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                uint32_t* e = reinterpret_cast<uint32_t*>(ys + (g + 8 * h) * kYs + 8 * n + 2 * c);
+                const float2 f = O::unpack2(*e);
+                *e = O::pack2(f.x + u.scale * d[n][2 * h], f.y + u.scale * d[n][2 * h + 1]);
             }
-            if (t1 < u.nt) {
-                const float2 f = O::unpack2(yv[n][1]);
-                *reinterpret_cast<uint32_t*>(y1 + col) = O::pack2(f.x + u.scale * d[n][2], f.y + u.scale * d[n][3]);
-            }
-        }
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+            if (live[i])
+                *reinterpret_cast<uint4*>(yrow4[i] + sc) = *reinterpret_cast<const uint4*>(ys + (4 * i + vr) * kYs + vc);
+        __syncwarp();
     }
 }
 
