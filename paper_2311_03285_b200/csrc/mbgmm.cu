@@ -674,10 +674,12 @@ int mbgmm_split(int64_t K) {
         const char* e = getenv("SLORA_MG_SPLIT");
         return e ? atoi(e) : 0;
     }();
-    // default: K parts of 2048 columns at K >= 8192 (32-row units, x streamed twice per rank-64
-    // tile instead of eight times: C4 60.6 -> 50.5 us per launch), whole K below (K = 4096 on
-    // C2-mixed: split 2 / 4 measured 12% / 10% slower, its long runs already fill the GPU)
-    int sp = env > 0 ? env : (K >= 8192 ? int(K / 2048) : 1);
+    // default: K parts of 4096 columns at K >= 8192 (16-row units, x streamed four times per
+    // rank-64 tile instead of eight: C4 60.6 -> 50.6 us per launch with 2048-column parts and
+    // 32-row units at first; after the expand's v-part and y changes, 4096-column parts are
+    // 2% faster: 43.7 -> 42.7), whole K below (K = 4096 on C2-mixed: split 2 / 4 measured
+    // 6% / 26% slower, its long runs already fill the GPU)
+    int sp = env > 0 ? env : (K >= 8192 ? int(K / 4096) : 1);
     while (sp > 1 && ((K / 64) % sp != 0 || sp > kMgVParts)) sp /= 2;
     return sp;
 }

@@ -5,7 +5,7 @@ phase).  With no consecutive prefill runs, segments of >= 4 tokens and rank
 tensor-core MBGMM kernels on x rows gathered into a contiguous workspace, y
 written back through the token index; the rest of the batch stays on MBGMV.
 Exact-integer inputs make the result bit-exact against the fp64 oracle; C4
-shapes (h = 8192, bf16: 32-row shrink units over four 2048-column K parts)
+shapes (h = 8192, bf16: 16-row shrink units over two 4096-column K parts)
 are checked within tolerance.
 Mark: gpu.
 """
@@ -66,7 +66,7 @@ def test_gathered_mbgmm_adapterless_rows_untouched():
 
 
 def test_gathered_mbgmm_c4_shapes_bf16():
-    """70B shapes on one GPU: h = 8192 (32-row shrink units over 2048-column K parts), 10 rank-64
+    """70B shapes on one GPU: h = 8192 (16-row shrink units over two 4096-column K parts), 10 rank-64
     adapters, 256 decode tokens, bf16."""
     cfg = wl.CONFIGS["c4"]
     cfg1 = wl.Config(cfg.name, cfg.index, cfg.hidden, cfg.n_adapters, cfg.rank_list, cfg.dtype, 1.0, 256,

@@ -2,7 +2,7 @@
 
 The mma.sync shrink holds R stored A rows (8, 16 or 32) over one of `split`
 parts of K ("K-split shrink units"); the expand adds the
-parts in order.  The defaults (whole K at h = 4096, four 2048-column parts at
+parts in order.  The defaults (whole K at h = 4096, two 4096-column parts at
 h = 8192) run in the other MBGMM suites.  The choice is read once per process
 from SLORA_MG_SPLIT / SLORA_MG_SROWS, so each setting re-runs the MBGMM parity
 suites (bit-exact integer regime + tolerance cases, against the fp64 oracle)
@@ -19,7 +19,7 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-@pytest.mark.parametrize("split,srows", [(2, 32), (4, 16), (8, 0), (1, 8)])
+@pytest.mark.parametrize("split,srows", [(2, 32), (4, 16), (4, 0), (8, 0), (1, 8)])
 def test_mbgmm_suites_under_split(split, srows):
     env = dict(os.environ, SLORA_MG_SPLIT=str(split), SLORA_MG_SROWS=str(srows))
     r = subprocess.run(

@@ -2,7 +2,7 @@
 (VERDICT r01, weak 2):
 
 * gathered MBGMM at C4 shapes (h = 8192, bf16, 10 rank-64 adapters, 256
-  decode tokens, 32-row shrink units over 2048-column K parts) in the exact-integer regime with
+  decode tokens, 16-row shrink units over two 4096-column K parts) in the exact-integer regime with
   y_in = 0 (|delta| <= 4 * 64 = 256, exact in bf16: SURVEY.md G2), compared
   BIT-exactly with the fp64 oracle;
 * the fused MBGMV kernel at K = 5120 (C3 unsharded) and K = 8192 (C4),
